@@ -1,0 +1,115 @@
+/*
+ * hmmscan.h — C ABI of the B200-native temporally parallel HMM inference library (libhmmscan.so).
+ *
+ * Implements the parallel sum-product smoother (Algorithm 3) and the parallel
+ * max-product MAP estimator (Definition 5 + Propositions 2-3, with argmax
+ * backpointers instead of Eq. 21's per-step assembly, see DESIGN.md "Readings" #6) for the HMM of
+ * Eqs. 4-6, on sm_100a.  All compute runs in this library's CUDA kernels.
+ *
+ * Conventions (all functions):
+ *   - D      number of states, 1 <= D <= HMM_MAX_D.
+ *   - T      number of time steps (>= 1); t is 0-based here (the paper is 1-based).
+ *   - log_pi [D]      fp32, log p(x_0 = d)                                  (prior)
+ *   - log_A  [D*D]    fp32 row-major, log_A[i*D+j] = log p(x_t=j | x_{t-1}=i)
+ *   - log_lik[T*D]    fp32 row-major, log p(y_t | x_t = d)
+ *     Inputs are general log-potentials: they need not be normalised; -inf is allowed anywhere
+ *     (a forbidden transition / impossible observation).  NaN and +inf are errors (info = -1).
+ *   - The potentials are psi_0(x_0) = exp(log_pi + log_lik_0) and
+ *     psi_t(x_{t-1}, x_t) = exp(log_A + log_lik_t) (Eq. 5).
+ *   - ALL data pointers are DEVICE pointers (cudaMalloc / torch CUDA tensors) unless the function
+ *     name says _host.  Scalars outputs (log_likelihood, log_prob, info) are device words too.
+ *   - Every call is asynchronous and stream-ordered on `stream` (a cudaStream_t; NULL = legacy
+ *     default stream).  Nothing is allocated or freed by the library and no host sync happens.
+ *   - workspace: caller-owned device memory of at least hmm_workspace_size(...) bytes, ZERO-FILLED
+ *     ONCE when allocated.  The kernels leave it in its zero state again when they finish, so the
+ *     same workspace can be reused by later calls on the same stream without re-zeroing.  Two calls
+ *     that may run concurrently (different streams) need different workspaces.
+ *   - Determinism: fixed reduction trees; the same inputs, sizes and device give bitwise-identical
+ *     outputs run to run.
+ *
+ * Errors:
+ *   - Host-detected, synchronous, returned: HMM_ERR_INVALID_VALUE (bad sizes, NULL pointer, pointer
+ *     not 4-byte aligned), HMM_ERR_WORKSPACE (workspace too small or NULL), HMM_ERR_UNSUPPORTED
+ *     (shape not supported by this build, e.g. T beyond the per-CTA chunk limit), HMM_ERR_CUDA (a
+ *     launch failed; cudaGetLastError() has the detail).
+ *   - Device-detected, asynchronous, written to info[b]: 0 = ok; t+1 = the smallest t at which no
+ *     state sequence is consistent with the evidence and the transitions up to t (zero forward mass
+ *     for the smoother, all V_t = -inf for Viterbi); -1 = a NaN or +inf input.
+ *     When info != 0 the other outputs of that sequence are undefined (cuSOLVER devInfo idiom).
+ */
+#ifndef HMMSCAN_H
+#define HMMSCAN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HMM_MAX_D 8
+
+typedef enum {
+    HMM_SUCCESS = 0,
+    HMM_ERR_INVALID_VALUE = 1,
+    HMM_ERR_WORKSPACE = 2,
+    HMM_ERR_UNSUPPORTED = 3,
+    HMM_ERR_CUDA = 4
+} hmm_status_t;
+
+typedef enum { HMM_OP_SMOOTH = 0, HMM_OP_VITERBI = 1 } hmm_op_t;
+
+/* Human-readable name of a status code (static storage, never NULL). */
+const char* hmm_status_string(hmm_status_t status);
+
+/* Library version string, e.g. "hmmscan 0.1 sm_100a". */
+const char* hmm_version(void);
+
+/* Bytes of device workspace needed by the hmm_smooth and hmm_viterbi families for (op, D, T, B) on the current
+ * device.  Returns 0 for invalid arguments.  The value depends on the device's SM count. */
+size_t hmm_workspace_size(int op, int D, int64_t T, int64_t B);
+
+/*
+ * Parallel sum-product smoother — Algorithm 3.
+ *   filtered [T*D] out: p(x_t | y_0..y_t), the normalised forward potential a_{0:t} (Thm 1,
+ *                       PAPER.md:304-341; filtering PAPER.md:177).  May be NULL (not written).
+ *   smoothed [T*D] out: p(x_t | y_0..y_{T-1}) = a_{0:t} a_{t:T+1} / Z_t (Eq. 14).
+ *   log_likelihood [1] out (double): log Z, Z the partition function of Eq. 1
+ *                       = log p(y_0..y_{T-1}) when the inputs are normalised probabilities.
+ *   info [1] out (int32): see Errors.
+ */
+hmm_status_t hmm_smooth(int D, int64_t T, const float* log_pi, const float* log_A, const float* log_lik,
+                        float* filtered, float* smoothed, double* log_likelihood, int32_t* info,
+                        void* workspace, size_t workspace_bytes, void* stream);
+
+/*
+ * Parallel max-product MAP (Viterbi) — Definition 5 / Propositions 2-3 for the
+ * forward max-potentials, argmax backpointers (Alg. 4 line 5) and a parallel
+ * backtrack by composition of chunk backpointer maps (DESIGN.md §"Viterbi").
+ *   path [T] out (int32): argmax_x log p(x, y) (Eq. 17); ties broken towards the
+ *                         smallest state index in every argmax (reading 5).
+ *   log_prob [1] out (double): the joint log p(x*, y) = max of the forward max-potential at T-1
+ *                         (Eqs. 16-17, Corollary 1 PAPER.md:621-632) — not the posterior.
+ */
+hmm_status_t hmm_viterbi(int D, int64_t T, const float* log_pi, const float* log_A, const float* log_lik,
+                         int32_t* path, double* log_prob, int32_t* info,
+                         void* workspace, size_t workspace_bytes, void* stream);
+
+/*
+ * Batched variants: B independent sequences of equal length T sharing log_pi and log_A.
+ *   log_lik [B*T*D], filtered/smoothed [B*T*D], log_likelihood [B], path [B*T], log_prob [B], info [B].
+ */
+hmm_status_t hmm_smooth_batched(int D, int64_t T, int64_t B, const float* log_pi, const float* log_A,
+                                const float* log_lik, float* filtered, float* smoothed,
+                                double* log_likelihood, int32_t* info,
+                                void* workspace, size_t workspace_bytes, void* stream);
+
+hmm_status_t hmm_viterbi_batched(int D, int64_t T, int64_t B, const float* log_pi, const float* log_A,
+                                 const float* log_lik, int32_t* path, double* log_prob, int32_t* info,
+                                 void* workspace, size_t workspace_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HMMSCAN_H */

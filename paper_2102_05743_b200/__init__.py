@@ -1,0 +1,162 @@
+"""paper_2102_05743_b200 — B200-native temporally parallel HMM inference (Hassan, Särkkä,
+García-Fernández, "Temporal Parallelization of Inference in Hidden Markov Models", arXiv 2102.05743).
+
+Thin Python binding over the C ABI of ``lib/libhmmscan.so`` (``include/hmmscan.h``): argument
+marshalling only — every step of the hot path runs in the library's sm_100a kernels.  PyTorch is used
+for device memory and streams.  There is no CPU fallback: importing works anywhere, but every compute
+call requires the CUDA library and a CUDA device and raises otherwise.
+
+    filtered, smoothed, log_z, info = smooth(log_pi, log_A, log_lik)       # Algorithm 3
+    path, log_prob, info = viterbi(log_pi, log_A, log_lik)                  # Def. 5 + backpointers
+
+``log_lik`` is [T, D] (single sequence) or [B, T, D] (batched, shared log_pi / log_A).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+
+import torch
+
+from .build import LIB, ROOT
+
+HMM_OP_SMOOTH, HMM_OP_VITERBI = 0, 1
+HMM_MAX_D = 8
+STATUS = {0: "HMM_SUCCESS", 1: "HMM_ERR_INVALID_VALUE", 2: "HMM_ERR_WORKSPACE", 3: "HMM_ERR_UNSUPPORTED",
+          4: "HMM_ERR_CUDA"}
+
+
+class HmmError(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Loads libhmmscan.so (built in-tree by ``__graft_entry__.build()`` / ``build.py``); fails loudly."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB):
+            raise HmmError(f"{LIB} is missing: build it with `python -m paper_2102_05743_b200.build`")
+        L = ctypes.CDLL(LIB)
+        i32, i64, p, sz = ctypes.c_int, ctypes.c_int64, ctypes.c_void_p, ctypes.c_size_t
+        L.hmm_status_string.restype = ctypes.c_char_p
+        L.hmm_status_string.argtypes = [i32]
+        L.hmm_version.restype = ctypes.c_char_p
+        L.hmm_workspace_size.restype = sz
+        L.hmm_workspace_size.argtypes = [i32, i32, i64, i64]
+        L.hmm_smooth.argtypes = [i32, i64, p, p, p, p, p, p, p, p, sz, p]
+        L.hmm_viterbi.argtypes = [i32, i64, p, p, p, p, p, p, p, sz, p]
+        L.hmm_smooth_batched.argtypes = [i32, i64, i64, p, p, p, p, p, p, p, p, sz, p]
+        L.hmm_viterbi_batched.argtypes = [i32, i64, i64, p, p, p, p, p, p, p, sz, p]
+        for f in ("hmm_smooth", "hmm_viterbi", "hmm_smooth_batched", "hmm_viterbi_batched"):
+            getattr(L, f).restype = i32
+        _lib = L
+    return _lib
+
+
+def header_symbols() -> list[str]:
+    """Function names declared in include/hmmscan.h (the boundary contract)."""
+    with open(os.path.join(ROOT, "include", "hmmscan.h")) as f:
+        txt = f.read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(hmm_[a-z_0-9]+)\s*\(", txt)))
+
+
+def _check(status: int, what: str):
+    if status != 0:
+        raise HmmError(f"{what}: {STATUS.get(status, status)}")
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+_ws_cache: dict = {}
+
+
+def workspace_size(op: int, D: int, T: int, B: int = 1) -> int:
+    return int(lib().hmm_workspace_size(op, D, T, B))
+
+
+def workspace(op: int, D: int, T: int, B: int = 1, device=None) -> torch.Tensor:
+    """Zero-filled device workspace (cached per device/shape; the kernels leave it zeroed)."""
+    device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    key = (device, op, D, T, B)
+    ws = _ws_cache.get(key)
+    if ws is None:
+        n = workspace_size(op, D, T, B)
+        if n == 0:
+            raise HmmError(f"unsupported shape op={op} D={D} T={T} B={B}")
+        ws = torch.zeros(n, dtype=torch.uint8, device=device)
+        _ws_cache[key] = ws
+    return ws
+
+
+def _inputs(log_pi, log_A, log_lik):
+    if not (log_lik.is_cuda and log_pi.is_cuda and log_A.is_cuda):
+        raise HmmError("inputs must be CUDA tensors (no CPU fallback)")
+    for t in (log_pi, log_A, log_lik):
+        if t.dtype != torch.float32 or not t.is_contiguous():
+            raise HmmError("inputs must be contiguous float32")
+    batched = log_lik.dim() == 3
+    B = log_lik.shape[0] if batched else 1
+    T, D = log_lik.shape[-2], log_lik.shape[-1]
+    if tuple(log_pi.shape) != (D,) or tuple(log_A.shape) != (D, D):
+        raise HmmError("shape mismatch: log_pi [D], log_A [D, D], log_lik [T, D] or [B, T, D]")
+    return batched, B, T, D
+
+
+def smooth(log_pi, log_A, log_lik, want_filtered: bool = True, out=None, ws=None, stream=None):
+    """Parallel sum-product smoother (Algorithm 3).
+
+    Returns (filtered or None, smoothed, log_likelihood [B] float64, info [B] int32), all on device.
+    """
+    batched, B, T, D = _inputs(log_pi, log_A, log_lik)
+    dev = log_lik.device
+    if out is None:
+        filt = torch.empty_like(log_lik) if want_filtered else None
+        sm = torch.empty_like(log_lik)
+        lz = torch.empty(B, dtype=torch.float64, device=dev)
+        info = torch.empty(B, dtype=torch.int32, device=dev)
+    else:
+        filt, sm, lz, info = out
+    ws = workspace(HMM_OP_SMOOTH, D, T, B, dev) if ws is None else ws
+    L = lib()
+    if batched:
+        st = L.hmm_smooth_batched(D, T, B, _ptr(log_pi), _ptr(log_A), _ptr(log_lik), _ptr(filt), _ptr(sm),
+                                  _ptr(lz), _ptr(info), _ptr(ws), ws.numel(), _stream(stream))
+    else:
+        st = L.hmm_smooth(D, T, _ptr(log_pi), _ptr(log_A), _ptr(log_lik), _ptr(filt), _ptr(sm), _ptr(lz),
+                          _ptr(info), _ptr(ws), ws.numel(), _stream(stream))
+    _check(st, "hmm_smooth")
+    return filt, sm, lz, info
+
+
+def viterbi(log_pi, log_A, log_lik, out=None, ws=None, stream=None):
+    """Parallel max-product MAP path (Def. 5 + backpointers).  Returns (path int32, log_prob f64 [B], info [B])."""
+    batched, B, T, D = _inputs(log_pi, log_A, log_lik)
+    dev = log_lik.device
+    if out is None:
+        path = torch.empty(log_lik.shape[:-1], dtype=torch.int32, device=dev)
+        lp = torch.empty(B, dtype=torch.float64, device=dev)
+        info = torch.empty(B, dtype=torch.int32, device=dev)
+    else:
+        path, lp, info = out
+    ws = workspace(HMM_OP_VITERBI, D, T, B, dev) if ws is None else ws
+    L = lib()
+    if batched:
+        st = L.hmm_viterbi_batched(D, T, B, _ptr(log_pi), _ptr(log_A), _ptr(log_lik), _ptr(path), _ptr(lp),
+                                   _ptr(info), _ptr(ws), ws.numel(), _stream(stream))
+    else:
+        st = L.hmm_viterbi(D, T, _ptr(log_pi), _ptr(log_A), _ptr(log_lik), _ptr(path), _ptr(lp), _ptr(info),
+                           _ptr(ws), ws.numel(), _stream(stream))
+    _check(st, "hmm_viterbi")
+    return path, lp, info

@@ -1,0 +1,206 @@
+// hmm_abi.cu — extern "C" entry points of libhmmscan.so (declared in include/hmmscan.h):
+// argument validation, launch planning (work decomposition, shared memory, workspace layout) and
+// dispatch to the sm_100a kernels.  No compute happens on the host.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+
+#include "../../include/hmmscan.h"
+#include "hmm_plan.h"
+
+namespace hmm {
+cudaError_t launch_small(int D, int op, unsigned G, unsigned B, size_t smem, bool coop, const KParams& kp,
+                         cudaStream_t s);
+}
+
+using hmm::Plan;
+
+namespace {
+
+struct DevInfo {
+    int sms = 0;
+    int smem_optin = 0;
+};
+
+constexpr int kMaxDevices = 64;
+DevInfo g_dev[kMaxDevices];
+std::once_flag g_dev_once[kMaxDevices];
+
+bool dev_info(DevInfo& out) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return false;
+    std::call_once(g_dev_once[dev], [dev]() {
+        cudaDeviceGetAttribute(&g_dev[dev].sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaDeviceGetAttribute(&g_dev[dev].smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    });
+    out = g_dev[dev];
+    return out.sms > 0;
+}
+
+int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+int64_t round_up(int64_t a, int64_t b) { return cdiv(a, b) * b; }
+int pow2_ceil(int x) {
+    int p = 1;
+    while (p < x) p <<= 1;
+    return p;
+}
+
+// Work decomposition for the small-D kernels (see hmm_plan.h and DESIGN.md §"Decomposition").
+bool make_plan(int D, int op, int64_t T, int64_t B, Plan& P) {
+    DevInfo di;
+    if (!dev_info(di)) return false;
+    P = Plan{};
+    P.D = D; P.op = op; P.T = T; P.B = B;
+    P.NT = hmm::small_nt(D);
+    const int NT = P.NT;
+    const size_t smax = (size_t)di.smem_optin;
+    int64_t G;
+    if (B >= di.sms) {
+        G = 1;
+    } else {
+        G = di.sms / B;
+        const int64_t gmax = cdiv(T, (int64_t)NT * 8);  // >= ~8 steps per thread
+        if (G > gmax) G = gmax;
+        if (G < 1) G = 1;
+    }
+    int64_t R = round_up(cdiv(T, G), 8);
+    G = cdiv(T, R);
+    P.G = (int)G;
+    P.R = R;
+    // fused: the whole CTA range stays resident in shared memory
+    hmm::SmemLayout Lf = hmm::small_smem_layout(D, op, (int)std::min<int64_t>(R, 1 << 30), 1);
+    if (R <= (1 << 24) && Lf.total <= smax) {
+        int S = (int)cdiv(R, NT);
+        if ((S & 1) == 0) S += 1;
+        P.S = S;
+        P.chunk = (int)R;
+        P.K = 1;
+        P.KP = 1;
+        P.fused = true;
+        P.smem = Lf.total;
+    } else {
+        int S = 25;
+        for (;;) {
+            const int chunk = NT * S;
+            const int K = (int)cdiv(R, chunk);
+            const int KP = pow2_ceil(K);
+            hmm::SmemLayout L = hmm::small_smem_layout(D, op, chunk, KP);
+            if (L.total <= smax && KP <= 1024) {
+                P.S = S; P.chunk = chunk; P.K = K; P.KP = KP; P.smem = L.total;
+                break;
+            }
+            if (KP > 1024) S += 2; else S -= 2;
+            if (S < 3 || S > 255) return false;
+        }
+        P.fused = false;
+    }
+    P.coop = P.G > 1;
+    // workspace
+    size_t off = 0;
+    P.ws_sync = off;
+    off += hmm::align16((size_t)B * 64);
+    off = (off + 255) & ~(size_t)255;
+    P.slot_bytes = hmm::align16((size_t)D * D * 4) + 32;
+    P.ws_slots = off;
+    off += (size_t)B * P.G * P.slot_bytes;
+    off = (off + 255) & ~(size_t)255;
+    P.chunk_slot = hmm::align16((size_t)D * D * 4);
+    P.ws_chunk = off;
+    if (!P.fused) off += (size_t)B * P.G * P.K * P.chunk_slot;
+    off = (off + 255) & ~(size_t)255;
+    P.ws_bp = off;
+    if (op == 1 && !P.fused) off += (size_t)B * P.G * P.K * (size_t)P.chunk * hmm::small_bpb(D);
+    off = (off + 255) & ~(size_t)255;
+    P.ws_lmap = off;
+    if (op == 1 && !P.fused) off += (size_t)B * P.G * P.K * (size_t)NT * 8;
+    off = (off + 255) & ~(size_t)255;
+    P.ws_total = off;
+    return true;
+}
+
+bool al4(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 3u) == 0; }
+bool al8(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 7u) == 0; }
+
+hmm_status_t run(int op, int D, int64_t T, int64_t B, const float* log_pi, const float* log_A, const float* log_lik,
+                 float* filtered, float* smoothed, int32_t* path, double* scalar, int32_t* info, void* ws,
+                 size_t ws_bytes, void* stream) {
+    if (D < 1 || T < 1 || B < 1 || B > 65535) return HMM_ERR_INVALID_VALUE;
+    if (D > HMM_MAX_D) return HMM_ERR_UNSUPPORTED;
+    if (!log_pi || !log_A || !log_lik || !scalar || !info) return HMM_ERR_INVALID_VALUE;
+    if (op == 0 && !smoothed) return HMM_ERR_INVALID_VALUE;
+    if (op == 1 && !path) return HMM_ERR_INVALID_VALUE;
+    if (!al4(log_pi) || !al4(log_A) || !al4(log_lik) || !al8(scalar) || !al4(info)) return HMM_ERR_INVALID_VALUE;
+    if ((filtered && !al4(filtered)) || (smoothed && !al4(smoothed)) || (path && !al4(path)))
+        return HMM_ERR_INVALID_VALUE;
+    Plan P;
+    if (!make_plan(D, op, T, B, P)) return HMM_ERR_UNSUPPORTED;
+    if (!ws || ws_bytes < P.ws_total || (reinterpret_cast<uintptr_t>(ws) & 255u)) return HMM_ERR_WORKSPACE;
+    hmm::KParams kp;
+    std::memset(&kp, 0, sizeof(kp));
+    kp.T = T; kp.R = P.R; kp.S = P.S; kp.chunk = P.chunk; kp.K = P.K; kp.KP = P.KP; kp.fused = P.fused ? 1 : 0;
+    kp.log_pi = log_pi; kp.log_A = log_A; kp.log_lik = log_lik;
+    kp.filtered = filtered; kp.smoothed = smoothed; kp.path = path; kp.scalar_out = scalar; kp.info = info;
+    kp.ws = static_cast<uint8_t*>(ws);
+    kp.ws_sync = P.ws_sync; kp.ws_slots = P.ws_slots; kp.slot_bytes = P.slot_bytes;
+    kp.ws_chunk = P.ws_chunk; kp.chunk_slot = P.chunk_slot; kp.ws_bp = P.ws_bp; kp.ws_lmap = P.ws_lmap;
+    kp.L = hmm::small_smem_layout(D, op, P.chunk, P.KP);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaError_t e = hmm::launch_small(D, op, (unsigned)P.G, (unsigned)P.B, P.smem, P.coop, kp, s);
+    return e == cudaSuccess ? HMM_SUCCESS : HMM_ERR_CUDA;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* hmm_status_string(hmm_status_t status) {
+    switch (status) {
+        case HMM_SUCCESS: return "HMM_SUCCESS";
+        case HMM_ERR_INVALID_VALUE: return "HMM_ERR_INVALID_VALUE";
+        case HMM_ERR_WORKSPACE: return "HMM_ERR_WORKSPACE";
+        case HMM_ERR_UNSUPPORTED: return "HMM_ERR_UNSUPPORTED";
+        case HMM_ERR_CUDA: return "HMM_ERR_CUDA";
+        default: return "HMM_ERR_UNKNOWN";
+    }
+}
+
+const char* hmm_version(void) { return "hmmscan 0.1 sm_100a"; }
+
+size_t hmm_workspace_size(int op, int D, int64_t T, int64_t B) {
+    if ((op != 0 && op != 1) || D < 1 || D > HMM_MAX_D || T < 1 || B < 1) return 0;
+    Plan P;
+    if (!make_plan(D, op, T, B, P)) return 0;
+    return P.ws_total;
+}
+
+hmm_status_t hmm_smooth(int D, int64_t T, const float* log_pi, const float* log_A, const float* log_lik,
+                        float* filtered, float* smoothed, double* log_likelihood, int32_t* info, void* workspace,
+                        size_t workspace_bytes, void* stream) {
+    return run(0, D, T, 1, log_pi, log_A, log_lik, filtered, smoothed, nullptr, log_likelihood, info, workspace,
+               workspace_bytes, stream);
+}
+
+hmm_status_t hmm_viterbi(int D, int64_t T, const float* log_pi, const float* log_A, const float* log_lik,
+                         int32_t* path, double* log_prob, int32_t* info, void* workspace, size_t workspace_bytes,
+                         void* stream) {
+    return run(1, D, T, 1, log_pi, log_A, log_lik, nullptr, nullptr, path, log_prob, info, workspace,
+               workspace_bytes, stream);
+}
+
+hmm_status_t hmm_smooth_batched(int D, int64_t T, int64_t B, const float* log_pi, const float* log_A,
+                                const float* log_lik, float* filtered, float* smoothed, double* log_likelihood,
+                                int32_t* info, void* workspace, size_t workspace_bytes, void* stream) {
+    return run(0, D, T, B, log_pi, log_A, log_lik, filtered, smoothed, nullptr, log_likelihood, info, workspace,
+               workspace_bytes, stream);
+}
+
+hmm_status_t hmm_viterbi_batched(int D, int64_t T, int64_t B, const float* log_pi, const float* log_A,
+                                 const float* log_lik, int32_t* path, double* log_prob, int32_t* info,
+                                 void* workspace, size_t workspace_bytes, void* stream) {
+    return run(1, D, T, B, log_pi, log_A, log_lik, nullptr, nullptr, path, log_prob, info, workspace,
+               workspace_bytes, stream);
+}
+
+}  // extern "C"

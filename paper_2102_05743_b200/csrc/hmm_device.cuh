@@ -1,0 +1,144 @@
+// hmm_device.cuh — sm_100a device helpers for libhmmscan: TMA bulk copies + mbarrier, grid
+// barriers over a sequence's CTAs, pow2 renormalisation, fast exp2, 3-input max.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace hmm {
+
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+
+__device__ __forceinline__ float neg_inf() { return __int_as_float(0xff800000); }
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// ---------------------------------------------------------------- mbarrier + bulk (TMA) copies
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    while (!mbar_try_wait(bar, parity)) {
+    }
+}
+// Global -> shared bulk copy (cp.async.bulk, SASS UBLKCP), completion counted on `bar`.
+// dst/src 16-B aligned, bytes a multiple of 16.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+// Shared -> global bulk copy (bulk_group completion).
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read_all() {
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// Make generic-proxy shared-memory writes visible to the async proxy (before a bulk store reads them).
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// ---------------------------------------------------------------- global memory ordering
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Grid barrier among the G CTAs that share (count, gen).  count returns to 0 after every barrier
+// (the last arriver resets it), gen only grows, so a zero-filled workspace stays valid across calls.
+// All G CTAs must be co-resident (cooperative launch).
+__device__ __forceinline__ void group_barrier(uint32_t* count, uint32_t* gen, uint32_t G) {
+    __syncthreads();
+    if (threadIdx.x == 0 && G > 1) {
+        uint32_t my_gen = ld_acquire_u32(gen);
+        __threadfence();
+        uint32_t arrived = atomicAdd(count, 1u);
+        if (arrived == G - 1) {
+            atomicExch(count, 0u);
+            __threadfence();
+            atomicAdd(gen, 1u);
+        } else {
+            while (ld_acquire_u32(gen) == my_gen) {
+                __nanosleep(20);
+            }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// ---------------------------------------------------------------- arithmetic helpers
+__device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float rcp(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float max3(float a, float b, float c) {
+    float r;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+// Exact power-of-two factor s with m*s in [1,2) for a positive normal m; 1 for 0 / denormal / huge.
+__device__ __forceinline__ float pow2_inv(float m) {
+    uint32_t e = __float_as_uint(m) & 0x7f800000u;
+    uint32_t s = 0x7f000000u - e;  // biased exponent 254 - e
+    return (e == 0u || e >= 0x7f000000u) ? 1.0f : __uint_as_float(s);
+}
+template <int N>
+__device__ __forceinline__ float vmax(const float* v) {
+    if constexpr (N == 1) {
+        return v[0];
+    } else if constexpr (N == 2) {
+        return fmaxf(v[0], v[1]);
+    } else {
+        float m = max3(v[0], v[1], v[2]);
+        int i = 3;
+#pragma unroll
+        for (; i + 1 < N; i += 2) m = max3(m, v[i], v[i + 1]);
+        if (i < N) m = fmaxf(m, v[i]);
+        return m;
+    }
+}
+template <int N>
+__device__ __forceinline__ float vsum(const float* v) {
+    float s = v[0];
+#pragma unroll
+    for (int i = 1; i < N; i++) s += v[i];
+    return s;
+}
+
+}  // namespace hmm

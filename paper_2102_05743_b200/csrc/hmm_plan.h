@@ -1,0 +1,118 @@
+// hmm_plan.h — launch plan, shared-memory layout and kernel parameter block shared by the host ABI
+// (hmm_abi.cu) and the small-D kernels (hmm_small.cu).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+
+#ifndef __CUDACC__
+#define __host__
+#define __device__
+#endif
+
+namespace hmm {
+
+__host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~static_cast<size_t>(15); }
+
+// Threads (= leaves) per CTA, floats per tree node, bytes per backpointer entry, per D.
+__host__ __device__ constexpr int small_nt(int D) { return D <= 4 ? 256 : 128; }
+__host__ __device__ constexpr int small_ne(int D) { return D * D > 2 * D ? D * D : 2 * D; }
+__host__ __device__ constexpr int small_bpb(int D) { return D <= 4 ? 2 : 4; }
+
+// Shared-memory carve-up (byte offsets from the dynamic smem base).  RC = steps resident per chunk.
+struct SmemLayout {
+    size_t tile, regB, carr, bp, tree, maps, ends, cmaps, cends, misc, total;
+};
+
+__host__ __device__ inline SmemLayout small_smem_layout(int D, int op, int RC, int KP) {
+    const int NT = small_nt(D), NE = small_ne(D);
+    const int NPM = NT > KP ? NT : KP;
+    SmemLayout L{};
+    size_t off = 0;
+    L.tile = off;
+    off += align16((size_t)RC * D * 4);
+    if (op == 0) {
+        size_t rb = (size_t)RC * D * 4;
+        size_t t1 = (size_t)2 * NT * NE * 4, t2 = (size_t)2 * KP * NE * 4;
+        if (t1 > rb) rb = t1;
+        if (t2 > rb) rb = t2;
+        L.regB = off;
+        off += align16(rb);
+        L.carr = off;
+        off += align16((size_t)KP * 2 * D * 4);
+        L.bp = L.tree = L.maps = L.ends = L.cmaps = L.cends = 0;
+    } else {
+        L.bp = off;
+        off += align16((size_t)RC * small_bpb(D));
+        size_t t1 = (size_t)2 * NT * NE * 4, t2 = (size_t)2 * KP * NE * 4;
+        L.tree = off;
+        off += align16(t1 > t2 ? t1 : t2);
+        L.maps = off;
+        off += align16((size_t)2 * NPM * 8);
+        L.ends = off;
+        off += align16((size_t)2 * NPM * 4);
+        L.carr = off;
+        off += align16((size_t)KP * 2 * D * 4);
+        L.cmaps = off;
+        off += align16((size_t)KP * 8);
+        L.cends = off;
+        off += align16((size_t)KP * 4);
+        L.regB = 0;
+    }
+    L.misc = off;
+    off += 512 + (size_t)(NT / 32) * 8;
+    L.total = align16(off);
+    return L;
+}
+
+// Work decomposition (DESIGN.md §"Decomposition"):
+//   sequence b  ->  G CTAs; CTA c owns steps [c*R, min((c+1)*R, T))
+//   CTA range   ->  K chunks of `chunk` steps (K == 1: "fused", the tile stays resident in SMEM)
+//   chunk       ->  NT leaves of S consecutive steps, one leaf per thread (S odd: conflict-free SMEM)
+struct Plan {
+    int D = 0;
+    int op = 0;          // 0 smoother, 1 Viterbi
+    int64_t T = 0;       // steps per sequence
+    int64_t B = 0;       // sequences
+    int G = 1;           // CTAs per sequence
+    int64_t R = 0;       // steps per CTA (multiple of 8)
+    int S = 1;           // steps per leaf (odd)
+    int NT = 256;        // threads (= leaves) per CTA
+    int chunk = 0;       // steps per chunk (multiple of 8)
+    int K = 1;           // max chunks per CTA
+    int KP = 1;          // K rounded up to a power of two
+    bool fused = true;   // K == 1
+    bool coop = false;   // G > 1: grid barrier, cooperative launch required
+    size_t smem = 0;     // dynamic shared memory bytes
+    // workspace layout (byte offsets)
+    size_t ws_sync = 0;      // B * 64 B: barrier/info words per sequence
+    size_t ws_slots = 0;     // B * G * slot_bytes: per-CTA roots, maps, partial sums
+    size_t slot_bytes = 0;
+    size_t ws_chunk = 0;     // B * G * K * chunk_slot: per-chunk roots (non-fused)
+    size_t chunk_slot = 0;
+    size_t ws_bp = 0;        // Viterbi non-fused: backpointers, B*G*K*chunk*bpb bytes
+    size_t ws_lmap = 0;      // Viterbi non-fused: leaf maps, B*G*K*NT*8 bytes
+    size_t ws_total = 0;
+};
+
+struct KParams {
+    int64_t T;
+    int64_t R;
+    int S;
+    int chunk;
+    int K;
+    int KP;
+    int fused;
+    const float* log_pi;
+    const float* log_A;
+    const float* log_lik;
+    float* filtered;
+    float* smoothed;
+    int32_t* path;
+    double* scalar_out;  // log_likelihood or log_prob, [B]
+    int32_t* info;       // [B]
+    uint8_t* ws;
+    size_t ws_sync, ws_slots, slot_bytes, ws_chunk, chunk_slot, ws_bp, ws_lmap;
+    SmemLayout L;
+};
+
+}  // namespace hmm
