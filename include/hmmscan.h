@@ -108,6 +108,17 @@ hmm_status_t hmm_viterbi_batched(int D, int64_t T, int64_t B, const float* log_p
                                  const float* log_lik, int32_t* path, double* log_prob, int32_t* info,
                                  void* workspace, size_t workspace_bytes, void* stream);
 
+/*
+ * Profiling / introspection (not part of the compute path).
+ *   hmm_debug_set_timers: for calls made later from the calling host thread, CTA phase timestamps
+ *     (%globaltimer, ns) are written to device_buf[(b*G + c)*16 + i] (NULL disables).
+ *   hmm_debug_plan: the launch plan for (op, D, T, B): out[0..7] = G (CTAs per sequence), R (steps per
+ *     CTA), S (steps per leaf), chunk, K (chunks per CTA), fused, dynamic smem bytes, threads per CTA.
+ *     Returns 0 if unsupported.
+ */
+void hmm_debug_set_timers(unsigned long long* device_buf);
+int hmm_debug_plan(int op, int D, int64_t T, int64_t B, int64_t* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -51,6 +51,10 @@ def lib() -> ctypes.CDLL:
         L.hmm_viterbi.argtypes = [i32, i64, p, p, p, p, p, p, p, sz, p]
         L.hmm_smooth_batched.argtypes = [i32, i64, i64, p, p, p, p, p, p, p, p, sz, p]
         L.hmm_viterbi_batched.argtypes = [i32, i64, i64, p, p, p, p, p, p, p, sz, p]
+        L.hmm_debug_set_timers.argtypes = [p]
+        L.hmm_debug_set_timers.restype = None
+        L.hmm_debug_plan.argtypes = [i32, i32, i64, i64, p]
+        L.hmm_debug_plan.restype = i32
         for f in ("hmm_smooth", "hmm_viterbi", "hmm_smooth_batched", "hmm_viterbi_batched"):
             getattr(L, f).restype = i32
         _lib = L
@@ -63,6 +67,20 @@ def header_symbols() -> list[str]:
         txt = f.read()
     txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
     return sorted(set(re.findall(r"\b(hmm_[a-z_0-9]+)\s*\(", txt)))
+
+
+def plan(op: int, D: int, T: int, B: int = 1) -> dict:
+    """Launch plan chosen by the library (introspection)."""
+    out = (ctypes.c_int64 * 8)()
+    if not lib().hmm_debug_plan(op, D, T, B, out):
+        raise HmmError("unsupported shape")
+    keys = ["G", "R", "S", "chunk", "K", "fused", "smem", "NT"]
+    return dict(zip(keys, list(out)))
+
+
+def set_timers(buf):
+    """Profiling: device int64 buffer [B*G*16] receiving CTA phase timestamps (None disables)."""
+    lib().hmm_debug_set_timers(None if buf is None else ctypes.c_void_p(buf.data_ptr()))
 
 
 def _check(status: int, what: str):

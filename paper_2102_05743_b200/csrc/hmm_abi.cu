@@ -70,7 +70,7 @@ bool make_plan(int D, int op, int64_t T, int64_t B, Plan& P) {
     P.G = (int)G;
     P.R = R;
     // fused: the whole CTA range stays resident in shared memory
-    hmm::SmemLayout Lf = hmm::small_smem_layout(D, op, (int)std::min<int64_t>(R, 1 << 30), 1);
+    hmm::SmemLayout Lf = hmm::small_smem_layout(D, op, (int)std::min<int64_t>(R, 1 << 30), 1, (int)G);
     if (R <= (1 << 24) && Lf.total <= smax) {
         int S = (int)cdiv(R, NT);
         if ((S & 1) == 0) S += 1;
@@ -86,7 +86,7 @@ bool make_plan(int D, int op, int64_t T, int64_t B, Plan& P) {
             const int chunk = NT * S;
             const int K = (int)cdiv(R, chunk);
             const int KP = pow2_ceil(K);
-            hmm::SmemLayout L = hmm::small_smem_layout(D, op, chunk, KP);
+            hmm::SmemLayout L = hmm::small_smem_layout(D, op, chunk, KP, (int)G);
             if (L.total <= smax && KP <= 1024) {
                 P.S = S; P.chunk = chunk; P.K = K; P.KP = KP; P.smem = L.total;
                 break;
@@ -102,7 +102,7 @@ bool make_plan(int D, int op, int64_t T, int64_t B, Plan& P) {
     P.ws_sync = off;
     off += hmm::align16((size_t)B * 64);
     off = (off + 255) & ~(size_t)255;
-    P.slot_bytes = hmm::align16((size_t)D * D * 4) + 32;
+    P.slot_bytes = hmm::small_slot_bytes(D);
     P.ws_slots = off;
     off += (size_t)B * P.G * P.slot_bytes;
     off = (off + 255) & ~(size_t)255;
@@ -119,6 +119,9 @@ bool make_plan(int D, int op, int64_t T, int64_t B, Plan& P) {
     P.ws_total = off;
     return true;
 }
+
+// Profiling hook (hmm_debug_set_timers): per-thread, not used unless set.
+thread_local unsigned long long* t_timers = nullptr;
 
 bool al4(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 3u) == 0; }
 bool al8(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 7u) == 0; }
@@ -145,7 +148,8 @@ hmm_status_t run(int op, int D, int64_t T, int64_t B, const float* log_pi, const
     kp.ws = static_cast<uint8_t*>(ws);
     kp.ws_sync = P.ws_sync; kp.ws_slots = P.ws_slots; kp.slot_bytes = P.slot_bytes;
     kp.ws_chunk = P.ws_chunk; kp.chunk_slot = P.chunk_slot; kp.ws_bp = P.ws_bp; kp.ws_lmap = P.ws_lmap;
-    kp.L = hmm::small_smem_layout(D, op, P.chunk, P.KP);
+    kp.L = hmm::small_smem_layout(D, op, P.chunk, P.KP, P.G);
+    kp.timers = t_timers;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     cudaError_t e = hmm::launch_small(D, op, (unsigned)P.G, (unsigned)P.B, P.smem, P.coop, kp, s);
     return e == cudaSuccess ? HMM_SUCCESS : HMM_ERR_CUDA;
@@ -167,6 +171,16 @@ const char* hmm_status_string(hmm_status_t status) {
 }
 
 const char* hmm_version(void) { return "hmmscan 0.1 sm_100a"; }
+
+void hmm_debug_set_timers(unsigned long long* device_buf) { t_timers = device_buf; }
+
+int hmm_debug_plan(int op, int D, int64_t T, int64_t B, int64_t* out /*[8]*/) {
+    Plan P;
+    if (!make_plan(D, op, T, B, P)) return 0;
+    out[0] = P.G; out[1] = P.R; out[2] = P.S; out[3] = P.chunk; out[4] = P.K; out[5] = P.fused;
+    out[6] = (int64_t)P.smem; out[7] = P.NT;
+    return 1;
+}
 
 size_t hmm_workspace_size(int op, int D, int64_t T, int64_t B) {
     if ((op != 0 && op != 1) || D < 1 || D > HMM_MAX_D || T < 1 || B < 1) return 0;

@@ -73,27 +73,36 @@ __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
     return v;
 }
 
-// Grid barrier among the G CTAs that share (count, gen).  count returns to 0 after every barrier
-// (the last arriver resets it), gen only grows, so a zero-filled workspace stays valid across calls.
+__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Arrive-and-wait among the G CTAs of a sequence on a monotonic 64-bit counter: every CTA adds 1
+// (release) and thread 0 spins (acquire) until the counter reaches G*epoch.  The counter is never
+// reset, so there is no extra round trip for a generation bump and a zero-filled workspace is valid.
 // All G CTAs must be co-resident (cooperative launch).
-__device__ __forceinline__ void group_barrier(uint32_t* count, uint32_t* gen, uint32_t G) {
+__device__ __forceinline__ void group_arrive_wait(unsigned long long* counter, uint32_t G, uint32_t epoch) {
     __syncthreads();
     if (threadIdx.x == 0 && G > 1) {
-        uint32_t my_gen = ld_acquire_u32(gen);
         __threadfence();
-        uint32_t arrived = atomicAdd(count, 1u);
-        if (arrived == G - 1) {
-            atomicExch(count, 0u);
-            __threadfence();
-            atomicAdd(gen, 1u);
-        } else {
-            while (ld_acquire_u32(gen) == my_gen) {
-                __nanosleep(20);
-            }
+        asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(counter) : "memory");
+        const unsigned long long target = (unsigned long long)G * epoch;
+        while (ld_acquire_u64(counter) < target) {
         }
-        __threadfence();
     }
     __syncthreads();
+}
+
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
 }
 
 // ---------------------------------------------------------------- arithmetic helpers

@@ -18,34 +18,39 @@ __host__ __device__ constexpr int small_nt(int D) { return D <= 4 ? 256 : 128; }
 __host__ __device__ constexpr int small_ne(int D) { return D * D > 2 * D ? D * D : 2 * D; }
 __host__ __device__ constexpr int small_bpb(int D) { return D <= 4 ? 2 : 4; }
 
-// Shared-memory carve-up (byte offsets from the dynamic smem base).  RC = steps resident per chunk.
+// Shared-memory carve-up (byte offsets from the dynamic smem base).  RC = steps resident per chunk,
+// KP = chunks per CTA rounded to a power of two, G = CTAs per sequence (slot staging).
 struct SmemLayout {
-    size_t tile, regB, carr, bp, tree, maps, ends, cmaps, cends, misc, total;
+    size_t tile, regB, carr, bp, tree, maps, ends, cmaps, cends, stage, misc, total;
 };
 
-__host__ __device__ inline SmemLayout small_smem_layout(int D, int op, int RC, int KP) {
+__host__ __device__ inline size_t small_slot_bytes(int D) { return align16((size_t)D * D * 4) + 32; }
+
+__host__ __device__ inline SmemLayout small_smem_layout(int D, int op, int RC, int KP, int G) {
     const int NT = small_nt(D), NE = small_ne(D);
     const int NPM = NT > KP ? NT : KP;
+    const size_t tree_bytes = align16((size_t)2 * NPM * NE * 4);
+    const size_t stage_bytes = align16((size_t)G * small_slot_bytes(D));
     SmemLayout L{};
     size_t off = 0;
     L.tile = off;
     off += align16((size_t)RC * D * 4);
     if (op == 0) {
+        // regB: filtered staging during the sweeps; before them the trees + the CTA-slot staging
         size_t rb = (size_t)RC * D * 4;
-        size_t t1 = (size_t)2 * NT * NE * 4, t2 = (size_t)2 * KP * NE * 4;
-        if (t1 > rb) rb = t1;
-        if (t2 > rb) rb = t2;
+        if (tree_bytes + stage_bytes > rb) rb = tree_bytes + stage_bytes;
         L.regB = off;
+        L.tree = off;
+        L.stage = off + tree_bytes;
         off += align16(rb);
         L.carr = off;
         off += align16((size_t)KP * 2 * D * 4);
-        L.bp = L.tree = L.maps = L.ends = L.cmaps = L.cends = 0;
+        L.bp = L.maps = L.ends = L.cmaps = L.cends = 0;
     } else {
         L.bp = off;
         off += align16((size_t)RC * small_bpb(D));
-        size_t t1 = (size_t)2 * NT * NE * 4, t2 = (size_t)2 * KP * NE * 4;
         L.tree = off;
-        off += align16(t1 > t2 ? t1 : t2);
+        off += tree_bytes;
         L.maps = off;
         off += align16((size_t)2 * NPM * 8);
         L.ends = off;
@@ -56,10 +61,12 @@ __host__ __device__ inline SmemLayout small_smem_layout(int D, int op, int RC, i
         off += align16((size_t)KP * 8);
         L.cends = off;
         off += align16((size_t)KP * 4);
+        L.stage = off;
+        off += stage_bytes;
         L.regB = 0;
     }
-    L.misc = off;
-    off += 512 + (size_t)(NT / 32) * 8;
+    L.misc = off;  // mbarriers (NT/32 + 1), reduction scratch, CTA carries, flags
+    off += 1024 + (size_t)(NT / 32) * 8;
     L.total = align16(off);
     return L;
 }
@@ -113,6 +120,7 @@ struct KParams {
     uint8_t* ws;
     size_t ws_sync, ws_slots, slot_bytes, ws_chunk, chunk_slot, ws_bp, ws_lmap;
     SmemLayout L;
+    unsigned long long* timers;  // optional [B*G*16] %globaltimer stamps per CTA phase (profiling only)
 };
 
 }  // namespace hmm

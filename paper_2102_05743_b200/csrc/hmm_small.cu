@@ -65,7 +65,6 @@ __device__ __forceinline__ void st_row(float* p, const float* v) {
     }
 }
 
-__device__ __forceinline__ bool is_bad(float x) { return !(x <= FLT_MAX); }  // NaN or +inf
 
 // Byte-packed state maps (D <= 8): byte x holds f(x).
 __device__ __forceinline__ uint64_t map_identity(int D) {
@@ -184,14 +183,63 @@ __device__ __forceinline__ void tree_store(float* tree, int NN, int x, const flo
 template <int D, bool MP>
 __device__ void tree_up(float* tree, int NP) {
     const int NN = 2 * NP;
+    const int lane = threadIdx.x & 31;
     for (int n = NP >> 1; n >= 1; n >>= 1) {
-        for (int k = threadIdx.x; k < n; k += blockDim.x) {
-            const int x = n + k;
-            float Lm[D * D], Rm[D * D], C[D * D];
-            tree_load<D>(tree, NN, 2 * x, Lm);
-            tree_load<D>(tree, NN, 2 * x + 1, Rm);
-            mat_op<D, MP>(Lm, Rm, C);
-            tree_store<D>(tree, NN, x, C);
+        // Wide levels: one thread per product (fewest instructions).  Narrow levels (n*D <= threads):
+        // D threads per product, one output row each, so the level latency is one row not a matrix.
+        if ((32 % D) == 0 && n * D <= (int)blockDim.x) {
+            // the group max comes from xor-shuffles inside the D-lane group (warp-uniform loop so every
+            // shuffle has a full mask)
+            const int work = n * D;
+            for (int base = threadIdx.x & ~31; base < work; base += blockDim.x) {
+                const int w = base + lane;
+                const bool act = w < work;
+                const int x = n + (act ? w / D : 0);
+                const int r = w % D;
+                float Lr[D], row[D];
+#pragma unroll
+                for (int k = 0; k < D; k++) Lr[k] = tree[(r * D + k) * NN + 2 * x];
+#pragma unroll
+                for (int j = 0; j < D; j++) {
+                    if constexpr (MP) {
+                        float sc[D];
+#pragma unroll
+                        for (int k = 0; k < D; k++) sc[k] = Lr[k] + tree[(k * D + j) * NN + 2 * x + 1];
+                        row[j] = vmax<D>(sc);
+                    } else {
+                        float acc = Lr[0] * tree[j * NN + 2 * x + 1];
+#pragma unroll
+                        for (int k = 1; k < D; k++) acc = fmaf(Lr[k], tree[(k * D + j) * NN + 2 * x + 1], acc);
+                        row[j] = acc;
+                    }
+                }
+                float m = vmax<D>(row);
+#pragma unroll
+                for (int o = 1; o < D; o <<= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+                if constexpr (MP) {
+                    if (m > neg_inf()) {
+#pragma unroll
+                        for (int j = 0; j < D; j++) row[j] -= m;
+                    }
+                } else {
+                    const float sc = pow2_inv(m);
+#pragma unroll
+                    for (int j = 0; j < D; j++) row[j] *= sc;
+                }
+                if (act) {
+#pragma unroll
+                    for (int j = 0; j < D; j++) tree[(r * D + j) * NN + x] = row[j];
+                }
+            }
+        } else {
+            for (int k = threadIdx.x; k < n; k += blockDim.x) {
+                const int x = n + k;
+                float Lm[D * D], Rm[D * D], C[D * D];
+                tree_load<D>(tree, NN, 2 * x, Lm);
+                tree_load<D>(tree, NN, 2 * x + 1, Rm);
+                mat_op<D, MP>(Lm, Rm, C);
+                tree_store<D>(tree, NN, x, C);
+            }
         }
         __syncthreads();
     }
@@ -202,6 +250,7 @@ __device__ void tree_up(float* tree, int NP) {
 template <int D, bool MP, bool SUF>
 __device__ void tree_down(float* tree, int NP, const float* pre_root, const float* suf_root) {
     const int NN = 2 * NP;
+    const int lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
 #pragma unroll
         for (int d = 0; d < D; d++) {
@@ -211,27 +260,82 @@ __device__ void tree_down(float* tree, int NP, const float* pre_root, const floa
     }
     __syncthreads();
     for (int n = 1; n < NP; n <<= 1) {
-        for (int k = threadIdx.x; k < n; k += blockDim.x) {
-            const int x = n + k;
-            float pre[D], suf[D], Lm[D * D], Rm[D * D], preR[D], sufL[D];
+        if ((32 % D) == 0 && n * D <= (int)blockDim.x) {
+            // D threads per node: thread d produces element d of preR = pre (x) M_left and of
+            // sufL = M_right (x) suf; group max by xor-shuffles for the normalisation.
+            const int work = n * D;
+            for (int base = threadIdx.x & ~31; base < work; base += blockDim.x) {
+                const int w = base + lane;
+                const bool act = w < work;
+                const int x = n + (act ? w / D : 0);
+                const int d = w % D;
+                float pre[D], suf[D];
 #pragma unroll
-            for (int d = 0; d < D; d++) {
-                pre[d] = tree[d * NN + x];
-                if (SUF) suf[d] = tree[(D + d) * NN + x];
-            }
-            tree_load<D>(tree, NN, 2 * x, Lm);
-            vec_mat<D, MP>(pre, Lm, preR);
-            if (SUF) {
-                tree_load<D>(tree, NN, 2 * x + 1, Rm);
-                mat_vec<D>(Rm, suf, sufL);
-            }
+                for (int k = 0; k < D; k++) {
+                    pre[k] = tree[k * NN + x];
+                    if (SUF) suf[k] = tree[(D + k) * NN + x];
+                }
+                float pr, sl = 0.0f;
+                if constexpr (MP) {
+                    float sc[D];
 #pragma unroll
-            for (int d = 0; d < D; d++) {
-                tree[d * NN + 2 * x] = pre[d];
-                tree[d * NN + 2 * x + 1] = preR[d];
+                    for (int k = 0; k < D; k++) sc[k] = pre[k] + tree[(k * D + d) * NN + 2 * x];
+                    pr = vmax<D>(sc);
+                } else {
+                    pr = pre[0] * tree[d * NN + 2 * x];
+#pragma unroll
+                    for (int k = 1; k < D; k++) pr = fmaf(pre[k], tree[(k * D + d) * NN + 2 * x], pr);
+                    if (SUF) {
+                        sl = tree[(d * D) * NN + 2 * x + 1] * suf[0];
+#pragma unroll
+                        for (int j = 1; j < D; j++) sl = fmaf(tree[(d * D + j) * NN + 2 * x + 1], suf[j], sl);
+                    }
+                }
+                float mp = pr, ms = sl;
+#pragma unroll
+                for (int o = 1; o < D; o <<= 1) {
+                    mp = fmaxf(mp, __shfl_xor_sync(0xffffffffu, mp, o));
+                    if (SUF) ms = fmaxf(ms, __shfl_xor_sync(0xffffffffu, ms, o));
+                }
+                if constexpr (MP) {
+                    if (mp > neg_inf()) pr -= mp;
+                } else {
+                    pr *= pow2_inv(mp);
+                    if (SUF) sl *= pow2_inv(ms);
+                }
+                __syncwarp();
+                if (act) {
+                    tree[d * NN + 2 * x] = pre[d];
+                    tree[d * NN + 2 * x + 1] = pr;
+                    if (SUF) {
+                        tree[(D + d) * NN + 2 * x] = sl;
+                        tree[(D + d) * NN + 2 * x + 1] = suf[d];
+                    }
+                }
+            }
+        } else {
+            for (int k = threadIdx.x; k < n; k += blockDim.x) {
+                const int x = n + k;
+                float pre[D], suf[D], Lm[D * D], Rm[D * D], preR[D], sufL[D];
+#pragma unroll
+                for (int d = 0; d < D; d++) {
+                    pre[d] = tree[d * NN + x];
+                    if (SUF) suf[d] = tree[(D + d) * NN + x];
+                }
+                tree_load<D>(tree, NN, 2 * x, Lm);
+                vec_mat<D, MP>(pre, Lm, preR);
                 if (SUF) {
-                    tree[(D + d) * NN + 2 * x] = sufL[d];
-                    tree[(D + d) * NN + 2 * x + 1] = suf[d];
+                    tree_load<D>(tree, NN, 2 * x + 1, Rm);
+                    mat_vec<D>(Rm, suf, sufL);
+                }
+#pragma unroll
+                for (int d = 0; d < D; d++) {
+                    tree[d * NN + 2 * x] = pre[d];
+                    tree[d * NN + 2 * x + 1] = preR[d];
+                    if (SUF) {
+                        tree[(D + d) * NN + 2 * x] = sufL[d];
+                        tree[(D + d) * NN + 2 * x + 1] = suf[d];
+                    }
                 }
             }
         }
@@ -264,31 +368,36 @@ __device__ inline void map_tree_down(const uint64_t* maps, int32_t* ends, int NP
 }
 
 // ---------------------------------------------------------------------------- warp reductions over
-// the G CTA roots of a sequence (global memory, one slot per CTA).  Lane l folds a contiguous group
-// in order, then a fixed shuffle tree; the result (product of slots [lo, hi)) is returned in all lanes.
+// the G CTA roots of a sequence, staged in shared memory (one slot of `sw` words per CTA).  Lane l
+// folds a contiguous group in order, then a fixed shuffle tree; the ordered product of slots
+// [lo, hi) is returned in all lanes.
 template <int D, bool MP>
-__device__ void warp_prod(const uint8_t* slots, size_t slot_bytes, int lo, int hi, float* out) {
+__device__ void warp_prod(const float* stage, int sw, int lo, int hi, float* out) {
     const int lane = threadIdx.x & 31;
     const int n = hi - lo;
     const int q = (n + 31) / 32;
     int a = lo + lane * q, e = a + q;
     if (e > hi) e = hi;
     float M[D * D];
-    mat_identity<D, MP>(M);
-    for (int s = a; s < e; s++) {
-        const float* src = reinterpret_cast<const float*>(slots + (size_t)s * slot_bytes);
-        float X[D * D], C[D * D];
+    if (a < e) {
 #pragma unroll
-        for (int k = 0; k < D * D; k++) X[k] = __ldcg(src + k);
-        mat_op<D, MP>(M, X, C);
+        for (int k = 0; k < D * D; k++) M[k] = stage[(size_t)a * sw + k];
+        for (int s = a + 1; s < e; s++) {
+            float X[D * D], C[D * D];
 #pragma unroll
-        for (int k = 0; k < D * D; k++) M[k] = C[k];
+            for (int k = 0; k < D * D; k++) X[k] = stage[(size_t)s * sw + k];
+            mat_op<D, MP>(M, X, C);
+#pragma unroll
+            for (int k = 0; k < D * D; k++) M[k] = C[k];
+        }
+    } else {
+        mat_identity<D, MP>(M);
     }
     for (int st = 1; st < 32; st <<= 1) {
         float O[D * D];
 #pragma unroll
         for (int k = 0; k < D * D; k++) O[k] = __shfl_down_sync(0xffffffffu, M[k], st);
-        if ((lane & (2 * st - 1)) == 0 && lane + st < 32) {
+        if ((lane & (2 * st - 1)) == 0 && lane + st < 32 && lo + (lane + st) * q < hi) {
             float C[D * D];
             mat_op<D, MP>(M, O, C);
 #pragma unroll
@@ -299,15 +408,14 @@ __device__ void warp_prod(const uint8_t* slots, size_t slot_bytes, int lo, int h
     for (int k = 0; k < D * D; k++) out[k] = __shfl_sync(0xffffffffu, M[k], 0);
 }
 template <int D>
-__device__ uint64_t warp_compose(const uint8_t* slots, size_t slot_bytes, size_t map_off, int lo, int hi) {
+__device__ uint64_t warp_compose(const uint64_t* maps, int lo, int hi) {
     const int lane = threadIdx.x & 31;
     const int n = hi - lo;
     const int q = (n + 31) / 32;
     int a = lo + lane * q, e = a + q;
     if (e > hi) e = hi;
     uint64_t f = map_identity(D);
-    for (int s = a; s < e; s++)
-        f = map_compose<D>(f, __ldcg(reinterpret_cast<const unsigned long long*>(slots + (size_t)s * slot_bytes + map_off)));
+    for (int s = a; s < e; s++) f = map_compose<D>(f, maps[s]);
     for (int st = 1; st < 32; st <<= 1) {
         uint64_t o = __shfl_down_sync(0xffffffffu, f, st);
         if ((lane & (2 * st - 1)) == 0 && lane + st < 32) f = map_compose<D>(f, o);
@@ -330,9 +438,8 @@ __device__ double block_sum(double v, double* scratch) {
 }
 
 // ---------------------------------------------------------------------------- tile movement
-// Loads `n` steps (n*D floats) of log_lik starting at `src` into smem `dst`.  The 16-B aligned body
-// goes through one bulk copy (TMA engine, UBLKCP) completing on `bar`; head/tail bytes and
-// misaligned sources go through ordinary loads.  Returns after the data is visible to all threads.
+// Whole-CTA load of nf floats (used for small side arrays): bulk copy of the 16-B aligned body on
+// `bar`, ordinary loads for the rest.  Returns after the data is visible to all threads.
 __device__ inline void load_floats(float* dst, const float* src, int64_t nf, uint64_t* bar, uint32_t& phase) {
     const uintptr_t a = reinterpret_cast<uintptr_t>(src);
     const bool aligned = (a & 15u) == 0;
@@ -348,23 +455,74 @@ __device__ inline void load_floats(float* dst, const float* src, int64_t nf, uin
     }
     __syncthreads();
 }
-// Stores nf floats (or int32) from smem to global; bulk store for the aligned body.
-// Caller must have issued fence_proxy_async_smem() after writing smem and __syncthreads().
-__device__ inline void store_words(void* dst_, const void* src_, int64_t nw) {
+
+// Chunk tile load split into one piece per warp (warp w's 32 leaves = steps [32Sw, 32S(w+1))), each
+// a bulk copy completing on its own mbarrier, so a warp starts folding its leaves as soon as its own
+// piece has landed (load overlapped with the leaf products of earlier warps).
+struct TileLoad {
+    bool bulk;      // false: cooperative loads were used and the tile is complete
+};
+template <int D>
+__device__ inline TileLoad tile_issue(float* tile, const float* src, int nch, int S, uint64_t* mbars, int nw) {
+    TileLoad tl;
+    tl.bulk = (reinterpret_cast<uintptr_t>(src) & 15u) == 0;
+    if (!tl.bulk) {
+        for (int64_t i = threadIdx.x; i < (int64_t)nch * D; i += blockDim.x) tile[i] = __ldg(src + i);
+        __syncthreads();
+        return tl;
+    }
+    if (threadIdx.x == 0) {
+        for (int w = 0; w < nw; w++) {
+            const int s0 = 32 * S * w;
+            if (s0 >= nch) break;
+            const int s1 = (s0 + 32 * S < nch) ? s0 + 32 * S : nch;
+            const uint32_t body = ((uint32_t)(s1 - s0) * D * 4u) & ~15u;
+            if (body) {
+                mbar_arrive_expect_tx(&mbars[w], body);
+                bulk_g2s(tile + (size_t)s0 * D, src + (size_t)s0 * D, body, &mbars[w]);
+            }
+        }
+    }
+    return tl;
+}
+// Warp w waits for its piece (+ loads the ragged tail of the last piece itself).
+template <int D>
+__device__ inline void tile_wait(const TileLoad& tl, float* tile, const float* src, int nch, int S, uint64_t* mbars,
+                                 uint32_t& wphase) {
+    if (!tl.bulk) return;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int s0 = 32 * S * w;
+    if (s0 >= nch) return;
+    const int s1 = (s0 + 32 * S < nch) ? s0 + 32 * S : nch;
+    const uint32_t nf = (uint32_t)(s1 - s0) * D;
+    const uint32_t body = nf & ~3u;
+    if (body) {
+        mbar_wait(&mbars[w], wphase);
+        wphase ^= 1u;
+    }
+    for (uint32_t i = body + lane; i < nf; i += 32) tile[(size_t)s0 * D + i] = __ldg(src + (size_t)s0 * D + i);
+    __syncwarp();
+}
+// Warp-cooperative store of nw 32-bit words from smem (written by this warp) to global: one bulk
+// store (UBLKCP) for the 16-B aligned body issued by lane 0, ordinary stores for the rest.
+__device__ inline void warp_store(void* dst_, const void* src_, int64_t nw) {
     uint32_t* dst = reinterpret_cast<uint32_t*>(dst_);
     const uint32_t* src = reinterpret_cast<const uint32_t*>(src_);
-    const uintptr_t a = reinterpret_cast<uintptr_t>(dst);
-    const bool aligned = (a & 15u) == 0;
+    const int lane = threadIdx.x & 31;
+    const bool aligned = ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15u) == 0;
     const int64_t body = aligned ? (nw / 4) * 4 : 0;
-    if (body > 0 && threadIdx.x == 0) {
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (body > 0 && lane == 0) {
         bulk_s2g(dst, src, (uint32_t)(body * 4));
         bulk_commit();
     }
-    for (int64_t i = body + threadIdx.x; i < nw; i += blockDim.x) dst[i] = src[i];
+    for (int64_t i = body + lane; i < nw; i += 32) dst[i] = src[i];
 }
-__device__ inline void store_wait() {
-    if (threadIdx.x == 0) bulk_wait_all();
-    __syncthreads();
+// Before shared memory read by this warp's bulk stores is overwritten (or the CTA exits).
+__device__ inline void warp_store_wait() {
+    if ((threadIdx.x & 31) == 0) bulk_wait_all();
+    __syncwarp();
 }
 
 // ---------------------------------------------------------------------------- leaf kernels
@@ -377,14 +535,14 @@ __device__ __forceinline__ void sp_leaf(float* rows, int n, bool t0, const float
     for (int i = 0; i < n; i++) {
         float v[D], l[D];
         ld_row<D>(rows + i * D, v);
-#pragma unroll
-        for (int j = 0; j < D; j++) bad |= is_bad(v[j]);
         const float m = vmax<D>(v);
         if (m > neg_inf()) {
             if (acc_m) msum += (double)m;
 #pragma unroll
-            for (int j = 0; j < D; j++) l[j] = ex2((v[j] - m) * kLog2e);
+            for (int j = 0; j < D; j++) l[j] = ex2((v[j] - m) * kLog2e);  // NaN / +inf propagate to P
         } else {
+            const float sv = vsum<D>(v);  // all -inf (impossible step) or NaN among -inf
+            bad |= (sv != sv);
 #pragma unroll
             for (int j = 0; j < D; j++) l[j] = 0.0f;
         }
@@ -416,6 +574,8 @@ __device__ __forceinline__ void sp_leaf(float* rows, int n, bool t0, const float
     }
 #pragma unroll
     for (int e = 0; e < D * D; e++) P[e] *= s;
+    const float chk = vsum<D * D>(P);  // a NaN or +inf input anywhere in the leaf leaves a NaN here
+    bad |= (chk != chk);
 }
 
 // Max-product leaf (log domain): P = psi~_{t0} (max,+) ... ; values shifted by -m_t per step,
@@ -423,15 +583,15 @@ __device__ __forceinline__ void sp_leaf(float* rows, int n, bool t0, const float
 template <int D>
 __device__ __forceinline__ void mp_leaf(const float* rows, int n, bool t0, const float* LA, const float* LP, float* P,
                                         bool& bad) {
+    float chk = 0.0f;
     for (int i = 0; i < n; i++) {
         float v[D], w[D];
         ld_row<D>(rows + i * D, v);
-#pragma unroll
-        for (int j = 0; j < D; j++) bad |= is_bad(v[j]);
         float m = vmax<D>(v);
         if (!(m > neg_inf())) m = 0.0f;
 #pragma unroll
         for (int j = 0; j < D; j++) w[j] = v[j] - m;
+        chk += vsum<D>(w);  // NaN iff a NaN / +inf input (max-plus itself drops NaNs)
         if (i == 0) {
 #pragma unroll
             for (int r = 0; r < D; r++)
@@ -458,6 +618,7 @@ __device__ __forceinline__ void mp_leaf(const float* rows, int n, bool t0, const
 #pragma unroll
         for (int e = 0; e < D * D; e++) P[e] -= m;
     }
+    bad |= (chk != chk);
 }
 
 // ---------------------------------------------------------------------------- sweeps
@@ -617,10 +778,11 @@ __device__ __forceinline__ void vit_backtrack(const void* bprow, int32_t* out, i
 template <int D, int OP>
 __global__ void __launch_bounds__(small_nt(D)) hmm_small_kernel(const KParams p) {
     constexpr int NT = small_nt(D);
-    constexpr int NE = small_ne(D);
+    constexpr int NW = NT / 32;
     constexpr bool MP = (OP == 1);
     extern __shared__ __align__(128) uint8_t smem[];
     const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
     const int c = blockIdx.x, G = gridDim.x;
     const int64_t b = blockIdx.y;
     const int64_t T = p.T;
@@ -630,29 +792,43 @@ __global__ void __launch_bounds__(small_nt(D)) hmm_small_kernel(const KParams p)
     const int S = p.S;
     const bool fused = p.fused != 0;
 
+    // per-sequence sync block (64 B): [0] u64 arrivals of exchange 1, [2] u64 arrivals of exchange 2,
+    // [4] u64 impossible-step code, [6] epoch, [7] done counter, [8] bad-input flag
     uint32_t* sync = reinterpret_cast<uint32_t*>(p.ws + p.ws_sync + (size_t)b * 64);
+    unsigned long long* arrive1 = reinterpret_cast<unsigned long long*>(sync + 0);
+    unsigned long long* arrive2 = reinterpret_cast<unsigned long long*>(sync + 2);
     unsigned long long* zero_code = reinterpret_cast<unsigned long long*>(sync + 4);
     uint8_t* slots = p.ws + p.ws_slots + (size_t)b * G * p.slot_bytes;
     const size_t map_off = align16((size_t)D * D * 4);
+    const int sw = (int)(p.slot_bytes / 4);  // slot stride in words
     uint8_t* myslot = slots + (size_t)c * p.slot_bytes;
     const float* ll_seq = p.log_lik + (size_t)b * T * D;
 
     float* tile = reinterpret_cast<float*>(smem + p.L.tile);
     float* carr = reinterpret_cast<float*>(smem + p.L.carr);
-    uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + p.L.misc);
-    double* red = reinterpret_cast<double*>(smem + p.L.misc + 16);
-    float* cta_pre = reinterpret_cast<float*>(smem + p.L.misc + 16 + (NT / 32) * 8);
+    float* tree = reinterpret_cast<float*>(smem + p.L.tree);
+    float* stage = reinterpret_cast<float*>(smem + p.L.stage);
+    uint64_t* mbars = reinterpret_cast<uint64_t*>(smem + p.L.misc);  // NW piece barriers + 1 aux
+    uint64_t* mbar_aux = mbars + NW;
+    double* red = reinterpret_cast<double*>(smem + p.L.misc + 8 * (NW + 1));
+    float* cta_pre = reinterpret_cast<float*>(red + NT / 32);
     float* cta_suf = cta_pre + D;
     int* flag = reinterpret_cast<int*>(cta_suf + D);
-    float* tree = reinterpret_cast<float*>(smem + (OP == 0 ? p.L.regB : p.L.tree));
 
+    unsigned long long* tmr = p.timers ? p.timers + ((size_t)b * G + c) * 16 : nullptr;
+#define HMM_STAMP(i) do { if (tmr && tid == 0) tmr[i] = global_ns(); } while (0)
+    HMM_STAMP(0);
+    // call epoch: every CTA of this launch reads the same value; the last CTA bumps it at exit
+    const uint32_t epoch = *reinterpret_cast<volatile uint32_t*>(sync + 6) + 1u;
+    uint32_t* done_ctr = sync + 7;
+    uint32_t* bad_flag = sync + 8;
     if (tid == 0) {
-        mbar_init(mbar, 1);
+        for (int w = 0; w <= NW; w++) mbar_init(&mbars[w], 1);
         fence_mbar_init();
         flag[0] = -1;
     }
     __syncthreads();
-    uint32_t phase = 0;
+    uint32_t wphase = 0, aux_phase = 0;
 
     // model in registers
     float A[D * D], pv[D];
@@ -668,28 +844,41 @@ __global__ void __launch_bounds__(small_nt(D)) hmm_small_kernel(const KParams p)
     }
 
     bool bad = false;
-    double acc = 0.0;          // log Z / log_prob partial of this thread
-    int64_t zero_t = INT64_MAX; // smallest impossible step seen by this thread
+    double acc = 0.0;            // log Z / log_prob partial of this thread
+    int64_t zero_t = INT64_MAX;  // smallest impossible step seen by this thread
 
-    // ===================== pass 1: leaf aggregates -> chunk roots
-    for (int k = 0; k < nchunks; k++) {
-        const int64_t ch0 = cta0 + (int64_t)k * p.chunk;
-        const int nch = (int)(((ch0 + p.chunk < cta1) ? ch0 + p.chunk : cta1) - ch0);
-        load_floats(tile, ll_seq + ch0 * D, (int64_t)nch * D, mbar, phase);
+    // leaf aggregate of this thread for chunk [ch0, ch0+nch): load (pipelined per warp), fold, store leaf
+    auto leaf_pass = [&](int64_t ch0, int nch, bool write_l, bool acc_m, bool& badf) {
+        const float* src = ll_seq + ch0 * D;
+        fence_proxy_async_smem();  // earlier generic-proxy smem writes before the bulk copies overwrite them
+        __syncthreads();
+        const TileLoad tl = tile_issue<D>(tile, src, nch, S, mbars, NW);
+        tile_wait<D>(tl, tile, src, nch, S, mbars, wphase);
+        HMM_STAMP(11);
         const int li = tid * S;
         const int ln = (li < nch) ? ((nch - li < S) ? nch - li : S) : 0;
         float P[D * D];
         if (ln > 0) {
             if constexpr (MP)
-                mp_leaf<D>(tile + li * D, ln, ch0 + li == 0, A, pv, P, bad);
+                mp_leaf<D>(tile + li * D, ln, ch0 + li == 0, A, pv, P, badf);
             else
-                sp_leaf<D>(tile + li * D, ln, ch0 + li == 0, A, pv, P, acc, fused, true, bad);
+                sp_leaf<D>(tile + li * D, ln, ch0 + li == 0, A, pv, P, acc, write_l, acc_m, badf);
         } else {
             mat_identity<D, MP>(P);
         }
+        HMM_STAMP(12);
         tree_store<D>(tree, 2 * NT, NT + tid, P);
         __syncthreads();
+        HMM_STAMP(13);
         tree_up<D, MP>(tree, NT);
+    };
+
+    // ===================== pass 1: leaf aggregates -> chunk roots
+    for (int k = 0; k < nchunks; k++) {
+        const int64_t ch0 = cta0 + (int64_t)k * p.chunk;
+        const int nch = (int)(((ch0 + p.chunk < cta1) ? ch0 + p.chunk : cta1) - ch0);
+        leaf_pass(ch0, nch, fused, true, bad);
+        HMM_STAMP(1);
         if (!fused) {
             float* dst = reinterpret_cast<float*>(p.ws + p.ws_chunk + ((size_t)(b * G + c) * p.K + k) * p.chunk_slot);
             if (tid < D * D) dst[tid] = tree[tid * 2 * NT + 1];
@@ -699,7 +888,6 @@ __global__ void __launch_bounds__(small_nt(D)) hmm_small_kernel(const KParams p)
 
     // ===================== CTA root (fused: the chunk tree root; else a tree over chunk roots)
     if (!fused) {
-        __threadfence_block();
         const int NN = 2 * p.KP;
         for (int x = tid; x < p.KP; x += NT) {
             float M[D * D];
@@ -717,48 +905,51 @@ __global__ void __launch_bounds__(small_nt(D)) hmm_small_kernel(const KParams p)
         tree_up<D, MP>(tree, p.KP);
     }
     const int NNroot = fused ? 2 * NT : 2 * p.KP;
-    // publish the CTA root, exchange, and get this CTA's carries
+
+    // ===================== cross-CTA exchange: publish the root, barrier, stage all roots in SMEM,
+    // warp 0 folds the roots to the left (forward carry), warp 1 the roots to the right (backward).
     if (tid < D * D) reinterpret_cast<float*>(myslot)[tid] = tree[tid * NNroot + 1];
-    group_barrier(sync + 0, sync + 1, (uint32_t)G);
-    {
-        const int warp = tid >> 5;
-        if (warp == 0) {
-            float M[D * D];
-            if (c > 0) warp_prod<D, MP>(slots, p.slot_bytes, 0, c, M);
-            if ((tid & 31) == 0) {
-                float v[D];
-                if (c == 0) {
+    HMM_STAMP(2);
+    if (G > 1) {
+        group_arrive_wait(arrive1, (uint32_t)G, epoch);
+        HMM_STAMP(3);
+        // copy all G roots into SMEM: one round of independent loads
+        for (int i = tid; i < G; i += NT) {
+            const float* src = reinterpret_cast<const float*>(slots + (size_t)i * p.slot_bytes);
+            float v[D * D];
 #pragma unroll
-                    for (int d = 0; d < D; d++) v[d] = MP ? 0.0f : 1.0f;
-                } else {
-                    float u[D];
+            for (int e = 0; e < D * D; e++) v[e] = __ldcg(src + e);
 #pragma unroll
-                    for (int d = 0; d < D; d++) u[d] = MP ? 0.0f : 1.0f;
-                    vec_mat<D, MP>(u, M, v);
-                }
+            for (int e = 0; e < D * D; e++) stage[(size_t)i * sw + e] = v[e];
+        }
+        __syncthreads();
+    }
+    if (warp == 0) {
+        float M[D * D];
+        if (c > 0) warp_prod<D, MP>(stage, sw, 0, c, M);
+        if (lane == 0) {
+            float u[D], v[D];
 #pragma unroll
-                for (int d = 0; d < D; d++) cta_pre[d] = v[d];
-            }
-        } else if (warp == 1 && !MP) {
-            float M[D * D];
-            if (c < G - 1) warp_prod<D, MP>(slots, p.slot_bytes, c + 1, G, M);
-            if ((tid & 31) == 0) {
-                float v[D];
+            for (int d = 0; d < D; d++) u[d] = v[d] = MP ? 0.0f : 1.0f;
+            if (c > 0) vec_mat<D, MP>(u, M, v);
 #pragma unroll
-                for (int d = 0; d < D; d++) v[d] = 1.0f;
-                if (c < G - 1) {
-                    float u[D];
+            for (int d = 0; d < D; d++) cta_pre[d] = v[d];
+        }
+    } else if (warp == 1 && !MP) {
+        float M[D * D];
+        if (c < G - 1) warp_prod<D, MP>(stage, sw, c + 1, G, M);
+        if (lane == 0) {
+            float u[D], v[D];
 #pragma unroll
-                    for (int d = 0; d < D; d++) u[d] = 1.0f;
-                    mat_vec<D>(M, u, v);
-                }
+            for (int d = 0; d < D; d++) u[d] = v[d] = 1.0f;
+            if (c < G - 1) mat_vec<D>(M, u, v);
 #pragma unroll
-                for (int d = 0; d < D; d++) cta_suf[d] = v[d];
-            }
+            for (int d = 0; d < D; d++) cta_suf[d] = v[d];
         }
     }
     __syncthreads();
 
+    HMM_STAMP(4);
     // carries per chunk (non-fused) or per leaf (fused)
     if (!fused) {
         tree_down<D, MP, !MP>(tree, p.KP, cta_pre, cta_suf);
@@ -775,6 +966,14 @@ __global__ void __launch_bounds__(small_nt(D)) hmm_small_kernel(const KParams p)
         tree_down<D, MP, !MP>(tree, NT, cta_pre, cta_suf);
     }
 
+    // this warp's rows of a chunk: [32 S warp, 32 S (warp+1)) clipped to nch
+    auto warp_rows = [&](int nch, int& r0, int& nr) {
+        r0 = 32 * S * warp;
+        int r1 = r0 + 32 * S;
+        if (r1 > nch) r1 = nch;
+        nr = (r1 > r0) ? r1 - r0 : 0;
+    };
+
     if constexpr (OP == 0) {
         // ===================== smoother pass 2 (chunks in reverse order: the tail is still in L2)
         float* filt = reinterpret_cast<float*>(smem + p.L.regB);
@@ -785,17 +984,8 @@ __global__ void __launch_bounds__(small_nt(D)) hmm_small_kernel(const KParams p)
             const int ln = (li < nch) ? ((nch - li < S) ? nch - li : S) : 0;
             const bool t0 = (ch0 + li == 0);
             if (!fused) {
-                load_floats(tile, ll_seq + ch0 * D, (int64_t)nch * D, mbar, phase);
-                float P[D * D];
-                double dummy = 0.0;
                 bool dbad = false;
-                if (ln > 0)
-                    sp_leaf<D>(tile + li * D, ln, t0, A, pv, P, dummy, true, false, dbad);
-                else
-                    mat_identity<D, false>(P);
-                tree_store<D>(tree, 2 * NT, NT + tid, P);
-                __syncthreads();
-                tree_up<D, false>(tree, NT);
+                leaf_pass(ch0, nch, true, false, dbad);
                 tree_down<D, false, true>(tree, NT, carr + k * 2 * D, carr + k * 2 * D + D);
             }
             float alpha[D], beta[D];
@@ -805,27 +995,31 @@ __global__ void __launch_bounds__(small_nt(D)) hmm_small_kernel(const KParams p)
                 beta[d] = tree[(D + d) * 2 * NT + NT + tid];
             }
             {
-                float s = vsum<D>(alpha);
-                float r = (s > 0.0f) ? 1.0f / s : 0.0f;
+                const float s = vsum<D>(alpha);
+                const float r = (s > 0.0f) ? 1.0f / s : 0.0f;
 #pragma unroll
                 for (int d = 0; d < D; d++) alpha[d] *= r;
             }
-            __syncthreads();  // tree (in regB) is dead from here: filt overwrites it
+            __syncthreads();  // the tree (in regB) is dead from here: filtered rows overwrite it
+            HMM_STAMP(5);
+            if (tmr && tid == 0) tmr[14] = clock64();
             if (ln > 0) {
                 const int zi = sp_alpha<D>(tile + li * D, filt + li * D, ln, t0, A, pv, alpha, acc, false);
                 if (zi >= 0 && ch0 + li + zi < zero_t) zero_t = ch0 + li + zi;
             }
-            __syncthreads();
-            if (p.filtered) {
-                fence_proxy_async_smem();
-                __syncthreads();
-                store_words(p.filtered + ((size_t)b * T + ch0) * D, filt, (int64_t)nch * D);
-            }
+            int r0, nr;
+            warp_rows(nch, r0, nr);
+            if (p.filtered && nr > 0)
+                warp_store(p.filtered + ((size_t)b * T + ch0 + r0) * D, filt + (size_t)r0 * D, (int64_t)nr * D);
+            if (tmr && tid == 0) tmr[15] = clock64();
+            HMM_STAMP(6);
             if (ln > 0) sp_beta<D>(tile + li * D, filt + li * D, ln, A, beta);
-            fence_proxy_async_smem();
+            HMM_STAMP(7);
+            if (nr > 0)
+                warp_store(p.smoothed + ((size_t)b * T + ch0 + r0) * D, tile + (size_t)r0 * D, (int64_t)nr * D);
+            warp_store_wait();
             __syncthreads();
-            store_words(p.smoothed + ((size_t)b * T + ch0) * D, tile, (int64_t)nch * D);
-            store_wait();
+            HMM_STAMP(8);
         }
     } else {
         // ===================== Viterbi pass 2: forward sweeps with backpointers, leaf/chunk maps
@@ -843,16 +1037,8 @@ __global__ void __launch_bounds__(small_nt(D)) hmm_small_kernel(const KParams p)
             const int ln = (li < nch) ? ((nch - li < S) ? nch - li : S) : 0;
             const bool t0 = (ch0 + li == 0);
             if (!fused) {
-                load_floats(tile, ll_seq + ch0 * D, (int64_t)nch * D, mbar, phase);
-                float P[D * D];
                 bool dbad = false;
-                if (ln > 0)
-                    mp_leaf<D>(tile + li * D, ln, t0, A, pv, P, dbad);
-                else
-                    mat_identity<D, true>(P);
-                tree_store<D>(tree, 2 * NT, NT + tid, P);
-                __syncthreads();
-                tree_up<D, true>(tree, NT);
+                leaf_pass(ch0, nch, false, false, dbad);
                 tree_down<D, true, false>(tree, NT, carr + k * 2 * D, nullptr);
             }
             float V[D];
@@ -870,46 +1056,57 @@ __global__ void __launch_bounds__(small_nt(D)) hmm_small_kernel(const KParams p)
                     flag[0] = xs;
                 }
             }
+            HMM_STAMP(5);
             maps[NT + tid] = f;
-            __syncthreads();
             if (!fused) {
-                // spill backpointers + leaf maps of this chunk (re-read by pass 3)
-                fence_proxy_async_smem();
-                __syncthreads();
-                store_words(p.ws + p.ws_bp + (cta_chunk_base + k) * (size_t)p.chunk * BPB, bp,
-                            ((int64_t)nch * BPB + 3) / 4);
+                // spill this warp's backpointers + leaf maps (re-read by pass 3)
+                int r0, nr;
+                warp_rows(nch, r0, nr);
+                if (nr > 0)
+                    warp_store(p.ws + p.ws_bp + (cta_chunk_base + k) * (size_t)p.chunk * BPB + (size_t)r0 * BPB,
+                               bp + (size_t)r0 * BPB, ((int64_t)nr * BPB + 3) / 4);
                 reinterpret_cast<uint64_t*>(p.ws + p.ws_lmap)[(cta_chunk_base + k) * NT + tid] = f;
+                warp_store_wait();
             }
+            __syncthreads();
             map_tree_up<D>(maps, NT);
-            if (!fused) {
-                if (tid == 0) cmaps[k] = maps[1];
-                store_wait();
-            }
+            if (!fused && tid == 0) cmaps[k] = maps[1];
         }
         // CTA map
         uint64_t F;
         if (fused) {
             F = maps[1];
         } else {
+            __syncthreads();
             for (int x = tid; x < p.KP; x += NT) maps[p.KP + x] = (x < nchunks) ? cmaps[x] : map_identity(D);
             __syncthreads();
             map_tree_up<D>(maps, p.KP);
             F = maps[1];
         }
-        if (tid == 0) {
-            *reinterpret_cast<uint64_t*>(myslot + map_off) = F;
-            if (c == G - 1) *reinterpret_cast<int32_t*>(myslot + map_off + 16) = flag[0];
-        }
-        group_barrier(sync + 0, sync + 1, (uint32_t)G);
         // end state of this CTA = (F_{c+1} o ... o F_{G-1})(x*)
-        if (tid < 32) {
-            const int xs = __ldcg(reinterpret_cast<const int*>(slots + (size_t)(G - 1) * p.slot_bytes + map_off + 16));
+        uint64_t* smaps = reinterpret_cast<uint64_t*>(stage);
+        int xs = flag[0];
+        if (G > 1) {
+            if (tid == 0) {
+                *reinterpret_cast<uint64_t*>(myslot + map_off) = F;
+                if (c == G - 1) *reinterpret_cast<int32_t*>(myslot + map_off + 16) = flag[0];
+            }
+            group_arrive_wait(arrive2, (uint32_t)G, epoch);
+            for (int i = c + 1 + tid; i < G; i += NT) {
+                smaps[i] = __ldcg(reinterpret_cast<const unsigned long long*>(slots + (size_t)i * p.slot_bytes + map_off));
+                if (i == G - 1) flag[3] = __ldcg(reinterpret_cast<const int*>(slots + (size_t)i * p.slot_bytes + map_off + 16));
+            }
+            __syncthreads();
+            if (c < G - 1) xs = flag[3];
+        }
+        if (warp == 0) {
             uint64_t Fs = map_identity(D);
-            if (c < G - 1) Fs = warp_compose<D>(slots, p.slot_bytes, map_off, c + 1, G);
-            if (tid == 0) flag[1] = map_apply(Fs, xs < 0 ? 0 : xs);
+            if (c < G - 1) Fs = warp_compose<D>(smaps, c + 1, G);
+            if (lane == 0) flag[1] = map_apply(Fs, xs < 0 ? 0 : xs);
         }
         __syncthreads();
         const int cta_end = flag[1];
+        HMM_STAMP(6);
         if (fused) {
             map_tree_down(maps, ends, NT, cta_end);
         } else {
@@ -927,7 +1124,7 @@ __global__ void __launch_bounds__(small_nt(D)) hmm_small_kernel(const KParams p)
             if (!fused) {
                 const uint8_t* src = p.ws + p.ws_bp + (cta_chunk_base + k) * (size_t)p.chunk * BPB;
                 load_floats(reinterpret_cast<float*>(bp), reinterpret_cast<const float*>(src),
-                            ((int64_t)nch * BPB + 3) / 4, mbar, phase);
+                            ((int64_t)nch * BPB + 3) / 4, mbar_aux, aux_phase);
                 maps[NT + tid] = __ldcg(reinterpret_cast<const unsigned long long*>(p.ws + p.ws_lmap) +
                                         (cta_chunk_base + k) * NT + tid);
                 __syncthreads();
@@ -937,37 +1134,47 @@ __global__ void __launch_bounds__(small_nt(D)) hmm_small_kernel(const KParams p)
             const int xe = ends[NT + tid];
             int32_t* out = reinterpret_cast<int32_t*>(tile);
             if (ln > 0) vit_backtrack<D>(bp + (size_t)li * BPB, out + li, ln, xe);
-            fence_proxy_async_smem();
+            int r0, nr;
+            warp_rows(nch, r0, nr);
+            __syncwarp();
+            if (nr > 0) warp_store(p.path + (size_t)b * T + ch0 + r0, out + r0, nr);
+            warp_store_wait();
             __syncthreads();
-            store_words(p.path + (size_t)b * T + ch0, out, nch);
-            store_wait();
         }
     }
 
     // ===================== scalars: log Z / log_prob, info (last CTA of the sequence)
-    if (bad) atomicOr(sync + 3, 1u);
+    HMM_STAMP(9);
+    if (bad) atomicOr(bad_flag, 1u);
     if (zero_t != INT64_MAX) atomicMax(zero_code, (1ull << 62) - (unsigned long long)zero_t);
     const double part = block_sum<NT>(acc, red);
     if (tid == 0) {
         *reinterpret_cast<double*>(myslot + map_off + 8) = part;
         __threadfence();
-        const uint32_t prev = atomicAdd(sync + 2, 1u);
+        const uint32_t prev = atomicAdd(done_ctr, 1u);
         flag[2] = (prev == (uint32_t)G - 1) ? 1 : 0;
     }
     __syncthreads();
-    if (flag[2] && tid == 0) {
+    if (flag[2]) {
+        // last CTA: fixed-order sum of the G partials (one per thread, then the block tree)
         __threadfence();
-        double s = 0.0;
-        for (int x = 0; x < G; x++) s += __ldcg(reinterpret_cast<const double*>(slots + (size_t)x * p.slot_bytes + map_off + 8));
-        p.scalar_out[b] = s;
-        const uint32_t badf = atomicExch(sync + 3, 0u);
-        const unsigned long long zc = atomicExch(zero_code, 0ull);
-        int32_t inf = 0;
-        if (badf) inf = -1;
-        else if (zc) inf = (int32_t)((1ull << 62) - zc + 1ull);
-        p.info[b] = inf;
-        atomicExch(sync + 2, 0u);
+        double v = 0.0;
+        for (int x = tid; x < G; x += NT) v += __ldcg(reinterpret_cast<const double*>(slots + (size_t)x * p.slot_bytes + map_off + 8));
+        const double tot = block_sum<NT>(v, red);
+        if (tid == 0) {
+            p.scalar_out[b] = tot;
+            const uint32_t badf = atomicExch(bad_flag, 0u);
+            const unsigned long long zc = atomicExch(zero_code, 0ull);
+            int32_t inf = 0;
+            if (badf) inf = -1;
+            else if (zc) inf = (int32_t)((1ull << 62) - zc + 1ull);
+            p.info[b] = inf;
+            atomicExch(done_ctr, 0u);
+            atomicAdd(sync + 6, 1u);  // next call's epoch
+        }
     }
+    HMM_STAMP(10);
+#undef HMM_STAMP
 }
 
 // ---------------------------------------------------------------------------- host launch

@@ -196,7 +196,8 @@ def test_deterministic_and_workspace_reuse():
     # the workspace is left zeroed for the next call
     ws = H.workspace(H.HMM_OP_SMOOTH, 4, 1_000_000, 1)
     words = ws[:64].view(torch.int32).cpu().numpy()
-    assert words[0] == 0 and (words[2:] == 0).all()  # only the barrier generation word (1) may be non-zero
+    # arrival counters (words 0-3) and the epoch (6) only grow; info accumulators + done counter are reset
+    assert (words[4:6] == 0).all() and words[7] == 0 and words[8] == 0
 
 
 def test_logz_no_normalisation_drift():
