@@ -47,7 +47,7 @@
 extern "C" {
 #endif
 
-#define HMM_MAX_D 8
+#define HMM_MAX_D 64
 
 typedef enum {
     HMM_SUCCESS = 0,
@@ -72,7 +72,8 @@ size_t hmm_workspace_size(int op, int D, int64_t T, int64_t B);
 /*
  * Parallel sum-product smoother — Algorithm 3.
  *   filtered [T*D] out: p(x_t | y_0..y_t), the normalised forward potential a_{0:t} (Thm 1,
- *                       PAPER.md:304-341; filtering PAPER.md:177).  May be NULL (not written).
+ *                       PAPER.md:304-341; filtering PAPER.md:177).  May be NULL (not written) for
+ *                       D <= 8; required for D > 8 (the large-D path stages alpha there).
  *   smoothed [T*D] out: p(x_t | y_0..y_{T-1}) = a_{0:t} a_{t:T+1} / Z_t (Eq. 14).
  *   log_likelihood [1] out (double): log Z, Z the partition function of Eq. 1
  *                       = log p(y_0..y_{T-1}) when the inputs are normalised probabilities.

@@ -22,7 +22,7 @@ import torch
 from .build import LIB, ROOT
 
 HMM_OP_SMOOTH, HMM_OP_VITERBI = 0, 1
-HMM_MAX_D = 8
+HMM_MAX_D = 64
 STATUS = {0: "HMM_SUCCESS", 1: "HMM_ERR_INVALID_VALUE", 2: "HMM_ERR_WORKSPACE", 3: "HMM_ERR_UNSUPPORTED",
           4: "HMM_ERR_CUDA"}
 
@@ -140,7 +140,7 @@ def smooth(log_pi, log_A, log_lik, want_filtered: bool = True, out=None, ws=None
     batched, B, T, D = _inputs(log_pi, log_A, log_lik)
     dev = log_lik.device
     if out is None:
-        filt = torch.empty_like(log_lik) if want_filtered else None
+        filt = torch.empty_like(log_lik) if (want_filtered or D > 8) else None
         sm = torch.empty_like(log_lik)
         lz = torch.empty(B, dtype=torch.float64, device=dev)
         info = torch.empty(B, dtype=torch.int32, device=dev)

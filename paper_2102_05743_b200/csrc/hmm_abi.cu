@@ -8,11 +8,14 @@
 #include <mutex>
 
 #include "../../include/hmmscan.h"
+#include "hmm_large.h"
 #include "hmm_plan.h"
 
 namespace hmm {
 cudaError_t launch_small(int D, int op, unsigned G, unsigned B, size_t smem, bool coop, const KParams& kp,
                          cudaStream_t s);
+cudaError_t launch_large(int DP, int op, const LgParams& p, cudaStream_t s);
+int large_leaves_per_block(int DP);
 }
 
 using hmm::Plan;
@@ -123,6 +126,45 @@ bool make_plan(int D, int op, int64_t T, int64_t B, Plan& P) {
 // Profiling hook (hmm_debug_set_timers): per-thread, not used unless set.
 thread_local unsigned long long* t_timers = nullptr;
 
+// Large-D plan (9 <= D <= 64): DP = padded state count; leaves of SL steps, NLB leaves per CTA.
+struct LgPlan {
+    int DP = 0;
+    int64_t SL = 0, NL = 0, NB = 0;
+    size_t o_sync, o_leaf, o_groot, o_bpre, o_bsuf, o_part, o_bp, o_lmap, o_bmap, o_bend, o_xstar, total;
+};
+
+bool make_large_plan(int D, int op, int64_t T, int64_t B, LgPlan& P) {
+    DevInfo di;
+    if (!dev_info(di)) return false;
+    P.DP = D <= 16 ? 16 : (D <= 32 ? 32 : 64);
+    const int NLB = hmm::large_leaves_per_block(P.DP);
+    // enough leaves for ~2 waves of 8-warp CTAs, leaves between 16 and 512 steps
+    const int64_t target = (int64_t)di.sms * 2 * NLB;
+    int64_t SL = cdiv(T * B, target);
+    if (SL < 16) SL = 16;
+    if (SL > 512) SL = 512;
+    if (SL > T) SL = T;
+    P.SL = SL;
+    P.NL = cdiv(T, SL);
+    P.NB = cdiv(P.NL, NLB);
+    const size_t DP2 = (size_t)P.DP * P.DP;
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t o = off; off = (off + bytes + 255) & ~(size_t)255; return o; };
+    P.o_sync = take((size_t)B * 64);
+    P.o_leaf = take((size_t)B * P.NL * DP2 * 4);
+    P.o_groot = take((size_t)B * P.NB * DP2 * 4);
+    P.o_bpre = take((size_t)B * P.NB * P.DP * 4);
+    P.o_bsuf = take((size_t)B * P.NB * P.DP * 4);
+    P.o_part = take((size_t)B * P.NL * 8);
+    P.o_bp = take(op == 1 ? (size_t)B * T * P.DP : 0);
+    P.o_lmap = take(op == 1 ? (size_t)B * P.NL * P.DP : 0);
+    P.o_bmap = take(op == 1 ? (size_t)B * P.NB * P.DP : 0);
+    P.o_bend = take(op == 1 ? (size_t)B * P.NB * 4 : 0);
+    P.o_xstar = take((size_t)B * 4);
+    P.total = off;
+    return true;
+}
+
 bool al4(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 3u) == 0; }
 bool al8(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 7u) == 0; }
 
@@ -131,6 +173,35 @@ hmm_status_t run(int op, int D, int64_t T, int64_t B, const float* log_pi, const
                  size_t ws_bytes, void* stream) {
     if (D < 1 || T < 1 || B < 1 || B > 65535) return HMM_ERR_INVALID_VALUE;
     if (D > HMM_MAX_D) return HMM_ERR_UNSUPPORTED;
+    if (D > 8) {
+        if (!log_pi || !log_A || !log_lik || !scalar || !info) return HMM_ERR_INVALID_VALUE;
+        if (op == 0 && !smoothed) return HMM_ERR_INVALID_VALUE;
+        if (op == 1 && !path) return HMM_ERR_INVALID_VALUE;
+        if (op == 0 && !filtered) return HMM_ERR_UNSUPPORTED;  // large-D smoother stages alpha in `filtered`
+        if (!al4(log_pi) || !al4(log_A) || !al4(log_lik) || !al8(scalar) || !al4(info)) return HMM_ERR_INVALID_VALUE;
+        LgPlan G;
+        if (!make_large_plan(D, op, T, B, G)) return HMM_ERR_UNSUPPORTED;
+        if (!ws || ws_bytes < G.total || (reinterpret_cast<uintptr_t>(ws) & 255u)) return HMM_ERR_WORKSPACE;
+        uint8_t* w = static_cast<uint8_t*>(ws);
+        hmm::LgParams lp;
+        std::memset(&lp, 0, sizeof(lp));
+        lp.T = T; lp.B = B; lp.D = D; lp.SL = G.SL; lp.NL = G.NL; lp.NB = G.NB;
+        lp.log_pi = log_pi; lp.log_A = log_A; lp.log_lik = log_lik;
+        lp.filtered = filtered; lp.smoothed = smoothed; lp.path = path; lp.scalar_out = scalar; lp.info = info;
+        lp.ws_sync = w + G.o_sync;
+        lp.leafagg = reinterpret_cast<float*>(w + G.o_leaf);
+        lp.groot = reinterpret_cast<float*>(w + G.o_groot);
+        lp.bpre = reinterpret_cast<float*>(w + G.o_bpre);
+        lp.bsuf = reinterpret_cast<float*>(w + G.o_bsuf);
+        lp.partial = reinterpret_cast<double*>(w + G.o_part);
+        lp.bp = w + G.o_bp;
+        lp.lmap = w + G.o_lmap;
+        lp.bmap = w + G.o_bmap;
+        lp.bend = reinterpret_cast<int32_t*>(w + G.o_bend);
+        lp.xstar = reinterpret_cast<int32_t*>(w + G.o_xstar);
+        cudaError_t e = hmm::launch_large(G.DP, op, lp, static_cast<cudaStream_t>(stream));
+        return e == cudaSuccess ? HMM_SUCCESS : HMM_ERR_CUDA;
+    }
     if (!log_pi || !log_A || !log_lik || !scalar || !info) return HMM_ERR_INVALID_VALUE;
     if (op == 0 && !smoothed) return HMM_ERR_INVALID_VALUE;
     if (op == 1 && !path) return HMM_ERR_INVALID_VALUE;
@@ -184,6 +255,11 @@ int hmm_debug_plan(int op, int D, int64_t T, int64_t B, int64_t* out /*[8]*/) {
 
 size_t hmm_workspace_size(int op, int D, int64_t T, int64_t B) {
     if ((op != 0 && op != 1) || D < 1 || D > HMM_MAX_D || T < 1 || B < 1) return 0;
+    if (D > 8) {
+        LgPlan G;
+        if (!make_large_plan(D, op, T, B, G)) return 0;
+        return G.total;
+    }
     Plan P;
     if (!make_plan(D, op, T, B, P)) return 0;
     return P.ws_total;

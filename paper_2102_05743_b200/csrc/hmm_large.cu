@@ -1,0 +1,819 @@
+// hmm_large.cu — parallel-scan HMM smoother and Viterbi for 9 <= D <= 64 (padded to DP in {16,32,64}),
+// sm_100a, FP32 CUDA cores.
+//
+// Same method as hmm_small.cu (block-wise elements of PAPER.md:759-760 scanned with the operators of
+// Def. 3 / Def. 5), organised for large D where one element product is a
+// DP x DP x DP contraction:
+//
+//   K1 lg_leaf   one warp per leaf (two half-warp leaves when DP = 16).  Lane owns CPL = DP/32 columns
+//                of A in registers; the leaf product P lives in SMEM and is read row by row as warp
+//                broadcasts (row r of P.A depends only on row r of P, so rows are updated in place).
+//                Per-step exact pow2 (or max-subtract) normalisation.  The block's leaves are then
+//                combined by an SMEM tree into the block root.
+//   K2 lg_carry  one CTA per sequence: forward (and backward) vector chains through the block roots
+//                (D^2 per root, the carries of Thms 1-2 / Props 2-3 at block granularity).
+//   K3 lg_sweep  per block: vector chains through its leaves, then per-leaf sequential sweeps
+//                (Alg. 1 / Alg. 4 restricted to the leaf) writing filtered/smoothed or backpointers.
+//   K4/K5        Viterbi: block end states by composing block backpointer maps, then backtrack.
+//   finalize     fixed-order fp64 sum of per-leaf partials -> log Z / log_prob; info.
+#include <cfloat>
+#include <cstdint>
+#include <cstring>
+
+#include "hmm_device.cuh"
+#include "hmm_large.h"
+
+namespace hmm {
+
+template <int DP>
+struct LG {
+    static constexpr int CPL = DP >= 32 ? DP / 32 : 1;  // columns (or rows) per lane
+    static constexpr int LPL = DP / CPL;                // lanes per leaf
+    static constexpr int LPW = 32 / LPL;                // leaves per warp
+    static constexpr int NW = 8;                        // warps per CTA
+    static constexpr int NLB = NW * LPW;                // leaves per CTA ("block")
+};
+
+template <int LPL>
+__device__ __forceinline__ float grp_max(float v) {
+#pragma unroll
+    for (int o = 1; o < LPL; o <<= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+template <int LPL>
+__device__ __forceinline__ float grp_sum(float v) {
+#pragma unroll
+    for (int o = 1; o < LPL; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ float lg_pad(bool mp) { return mp ? neg_inf() : 0.0f; }
+
+__device__ __forceinline__ int og_global_lookup(const LgParams& p, int64_t b, int64_t L, int x, int DP) {
+    return p.lmap[((size_t)b * p.NL + L) * DP + x];
+}
+
+// A(k, j) for the padded model (exp for sum-product, log for max-product).
+__device__ __forceinline__ float lg_A(const LgParams& p, int k, int j, bool mp) {
+    if (k >= p.D || j >= p.D) return lg_pad(mp);
+    const float la = __ldg(p.log_A + k * p.D + j);
+    return mp ? la : ex2(la * kLog2e);
+}
+__device__ __forceinline__ float lg_pi(const LgParams& p, int j, bool mp) {
+    if (j >= p.D) return lg_pad(mp);
+    const float lp = __ldg(p.log_pi + j);
+    return mp ? lp : ex2(lp * kLog2e);
+}
+
+// Row-wise in-place product of two DP x DP SMEM matrices by one (sub-)leaf group of lanes:
+// X <- X (op) Y, where the lanes hold Y's columns in registers (Ycol).  Normalised (pow2 / max).
+template <int DP, bool MP>
+__device__ void lg_rows_times(float* X, const float (&Ycol)[LG<DP>::CPL][DP], int cl, bool act) {
+    constexpr int CPL = LG<DP>::CPL, LPL = LG<DP>::LPL;
+    float mx = MP ? neg_inf() : 0.0f;
+    for (int r = 0; r < DP; r++) {
+        float acc[CPL];
+#pragma unroll
+        for (int c = 0; c < CPL; c++) acc[c] = MP ? neg_inf() : 0.0f;
+#pragma unroll
+        for (int k4 = 0; k4 < DP; k4 += 4) {
+            const float4 x = *reinterpret_cast<const float4*>(X + r * DP + k4);
+#pragma unroll
+            for (int c = 0; c < CPL; c++) {
+                if constexpr (MP) {
+                    acc[c] = fmaxf(acc[c], max3(x.x + Ycol[c][k4], x.y + Ycol[c][k4 + 1],
+                                                fmaxf(x.z + Ycol[c][k4 + 2], x.w + Ycol[c][k4 + 3])));
+                } else {
+                    acc[c] = fmaf(x.x, Ycol[c][k4], acc[c]);
+                    acc[c] = fmaf(x.y, Ycol[c][k4 + 1], acc[c]);
+                    acc[c] = fmaf(x.z, Ycol[c][k4 + 2], acc[c]);
+                    acc[c] = fmaf(x.w, Ycol[c][k4 + 3], acc[c]);
+                }
+            }
+        }
+        __syncwarp();
+        if (act) {
+#pragma unroll
+            for (int c = 0; c < CPL; c++) {
+                X[r * DP + cl * CPL + c] = acc[c];
+                mx = fmaxf(mx, acc[c]);
+            }
+        }
+        __syncwarp();
+    }
+    mx = grp_max<LPL>(mx);
+    if (act) {
+        for (int r = 0; r < DP; r++) {
+#pragma unroll
+            for (int c = 0; c < CPL; c++) {
+                float& v = X[r * DP + cl * CPL + c];
+                if constexpr (MP) {
+                    if (mx > neg_inf()) v -= mx;
+                } else {
+                    v *= pow2_inv(mx);
+                }
+            }
+        }
+    }
+    __syncwarp();
+}
+
+// ------------------------------------------------------------------------------------------- K1
+template <int DP, int OP>
+__global__ void __launch_bounds__(256) lg_leaf_kernel(const LgParams p) {
+    using C = LG<DP>;
+    constexpr int CPL = C::CPL, LPL = C::LPL, LPW = C::LPW, NLB = C::NLB;
+    constexpr bool MP = (OP == 1);
+    extern __shared__ __align__(128) uint8_t smem[];
+    float* sm = reinterpret_cast<float*>(smem);
+    const int64_t b = blockIdx.y;
+    const int blk = blockIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int sub = lane / LPL, cl = lane % LPL;
+    const int lidx = warp * LPW + sub;                    // leaf index inside the block
+    const int64_t L = (int64_t)blk * NLB + lidx;          // leaf index inside the sequence
+    float* Pm = sm + (size_t)lidx * DP * DP;
+    const int64_t T = p.T;
+    const int64_t t0 = L * p.SL;
+    auto leaf_len = [&](int64_t LL) -> int {
+        const int64_t a = LL * p.SL;
+        if (LL >= p.NL || a >= T) return 0;
+        return (int)((T - a < p.SL) ? T - a : p.SL);
+    };
+    const int n = leaf_len(L);
+    int nmax = n;
+#pragma unroll
+    for (int o = LPL; o < 32; o <<= 1) nmax = max(nmax, __shfl_xor_sync(0xffffffffu, nmax, o));
+
+    float Acol[CPL][DP], pv[CPL];
+#pragma unroll
+    for (int c = 0; c < CPL; c++) {
+        const int j = cl * CPL + c;
+#pragma unroll
+        for (int k = 0; k < DP; k++) Acol[c][k] = lg_A(p, k, j, MP);
+        pv[c] = lg_pi(p, j, MP);
+    }
+    const float* ll = p.log_lik + (size_t)b * T * p.D;
+    bool bad = false;
+    float s = MP ? 0.0f : 1.0f;  // pending normalisation (scale / offset) from the previous step
+    float chk = 0.0f;
+    for (int i = 0; i < nmax; i++) {
+        const bool act = i < n;
+        const int64_t t = t0 + i;
+        float v[CPL], l[CPL];
+#pragma unroll
+        for (int c = 0; c < CPL; c++) {
+            const int j = cl * CPL + c;
+            v[c] = (act && j < p.D) ? __ldg(ll + t * p.D + j) : neg_inf();
+        }
+        float m = v[0];
+#pragma unroll
+        for (int c = 1; c < CPL; c++) m = fmaxf(m, v[c]);
+        m = grp_max<LPL>(m);
+        if (!(m > neg_inf())) m = 0.0f;
+#pragma unroll
+        for (int c = 0; c < CPL; c++) {
+            if constexpr (MP) {
+                l[c] = v[c] - m;
+                chk += l[c];
+            } else {
+                l[c] = ex2((v[c] - m) * kLog2e);
+            }
+        }
+        if (i == 0) {
+            if (act) {
+#pragma unroll
+                for (int r = 0; r < DP; r++)
+#pragma unroll
+                    for (int c = 0; c < CPL; c++) {
+                        const float a = (t == 0) ? pv[c] : Acol[c][r];
+                        Pm[r * DP + cl * CPL + c] = MP ? a + l[c] : a * l[c];
+                    }
+            }
+            __syncwarp();
+        } else {
+            float mx = MP ? neg_inf() : 0.0f;
+            for (int r = 0; r < DP; r++) {
+                float acc[CPL];
+#pragma unroll
+                for (int c = 0; c < CPL; c++) acc[c] = MP ? neg_inf() : 0.0f;
+#pragma unroll
+                for (int k4 = 0; k4 < DP; k4 += 4) {
+                    const float4 x = *reinterpret_cast<const float4*>(Pm + r * DP + k4);
+#pragma unroll
+                    for (int c = 0; c < CPL; c++) {
+                        if constexpr (MP) {
+                            acc[c] = fmaxf(acc[c], max3(x.x + Acol[c][k4], x.y + Acol[c][k4 + 1],
+                                                        fmaxf(x.z + Acol[c][k4 + 2], x.w + Acol[c][k4 + 3])));
+                        } else {
+                            acc[c] = fmaf(x.x, Acol[c][k4], acc[c]);
+                            acc[c] = fmaf(x.y, Acol[c][k4 + 1], acc[c]);
+                            acc[c] = fmaf(x.z, Acol[c][k4 + 2], acc[c]);
+                            acc[c] = fmaf(x.w, Acol[c][k4 + 3], acc[c]);
+                        }
+                    }
+                }
+                __syncwarp();
+                if (act) {
+#pragma unroll
+                    for (int c = 0; c < CPL; c++) {
+                        const float val = MP ? acc[c] + (l[c] - s) : acc[c] * (l[c] * s);
+                        Pm[r * DP + cl * CPL + c] = val;
+                        mx = fmaxf(mx, val);
+                    }
+                }
+                __syncwarp();
+            }
+            mx = grp_max<LPL>(mx);
+            if constexpr (MP) {
+                s = (mx > neg_inf()) ? mx : 0.0f;
+            } else {
+                s = pow2_inv(mx);
+            }
+        }
+    }
+    // final normalisation and NaN check, then write the leaf aggregate (reductions warp-uniform: the
+    // two half-warp leaves of DP = 16 may differ in length)
+    float mx = MP ? neg_inf() : 0.0f;
+    float sum = 0.0f;
+    if (n > 0) {
+        for (int r = 0; r < DP; r++)
+#pragma unroll
+            for (int c = 0; c < CPL; c++) {
+                mx = fmaxf(mx, Pm[r * DP + cl * CPL + c]);
+                sum += Pm[r * DP + cl * CPL + c];
+            }
+    }
+    mx = grp_max<LPL>(mx);
+    if (n > 0) {
+        if constexpr (!MP) bad |= (sum != sum);
+        float* dst = p.leafagg + ((size_t)b * p.NL + L) * DP * DP;
+        for (int r = 0; r < DP; r++)
+#pragma unroll
+            for (int c = 0; c < CPL; c++) {
+                float& x = Pm[r * DP + cl * CPL + c];
+                if constexpr (MP) {
+                    if (mx > neg_inf()) x -= mx;
+                } else {
+                    x *= pow2_inv(mx);
+                }
+                dst[r * DP + cl * CPL + c] = x;
+            }
+    } else {
+        for (int r = 0; r < DP; r++)
+#pragma unroll
+            for (int c = 0; c < CPL; c++) {
+                const int j = cl * CPL + c;
+                Pm[r * DP + j] = (r == j) ? (MP ? 0.0f : 1.0f) : lg_pad(MP);
+            }
+    }
+    if constexpr (MP) bad |= (chk != chk);
+    if (bad) atomicOr(reinterpret_cast<uint32_t*>(p.ws_sync + b * 64) + 8, 1u);
+    __syncthreads();
+
+    // block root: ordered tree over the NLB leaf buffers (products by leaf lane-groups)
+    for (int stride = 1; stride < NLB; stride <<= 1) {
+        const bool lead = (lidx % (2 * stride)) == 0 && lidx + stride < NLB;
+        const bool any = __any_sync(0xffffffffu, lead);
+        if (any) {
+            float Ycol[CPL][DP];
+            const float* Y = sm + (size_t)(lead ? lidx + stride : lidx) * DP * DP;
+#pragma unroll
+            for (int c = 0; c < CPL; c++)
+#pragma unroll
+                for (int k = 0; k < DP; k++) Ycol[c][k] = Y[k * DP + cl * CPL + c];
+            __syncwarp();
+            lg_rows_times<DP, MP>(Pm, Ycol, cl, lead);
+        }
+        __syncthreads();
+    }
+    if (lidx == 0) {
+        float* dst = p.groot + ((size_t)b * p.NB + blk) * DP * DP;
+        for (int r = 0; r < DP; r++)
+#pragma unroll
+            for (int c = 0; c < CPL; c++) dst[r * DP + cl * CPL + c] = Pm[r * DP + cl * CPL + c];
+    }
+}
+
+// ------------------------------------------------------------------------------------------- K2
+// Vector chains through NB block roots (one warp each).  Lane owns output columns / rows.
+template <int DP, bool MP>
+__device__ void lg_chain_fwd(const float* mats, int64_t nm, const float* v0, float* out /*[nm][DP]*/, float* vs) {
+    constexpr int Q = DP >= 32 ? DP / 32 : 1;
+    const int lane = threadIdx.x & 31;
+    const bool act = lane * Q < DP;
+    if (act)
+        for (int q = 0; q < Q; q++) vs[lane * Q + q] = v0[lane * Q + q];
+    __syncwarp();
+    for (int64_t i = 0; i < nm; i++) {
+        if (act)
+            for (int q = 0; q < Q; q++) out[i * DP + lane * Q + q] = vs[lane * Q + q];
+        const float* M = mats + (size_t)i * DP * DP;
+        float y[Q];
+#pragma unroll
+        for (int q = 0; q < Q; q++) y[q] = MP ? neg_inf() : 0.0f;
+        if (act) {
+            for (int k = 0; k < DP; k++) {
+                const float vk = vs[k];
+#pragma unroll
+                for (int q = 0; q < Q; q++) {
+                    const float mkj = __ldcg(M + (size_t)k * DP + lane * Q + q);
+                    y[q] = MP ? fmaxf(y[q], vk + mkj) : fmaf(vk, mkj, y[q]);
+                }
+            }
+        }
+        float m = y[0];
+#pragma unroll
+        for (int q = 1; q < Q; q++) m = fmaxf(m, y[q]);
+        m = grp_max<32>(act ? m : (MP ? neg_inf() : 0.0f));
+        __syncwarp();
+        if (act)
+            for (int q = 0; q < Q; q++) vs[lane * Q + q] = MP ? ((m > neg_inf()) ? y[q] - m : y[q]) : y[q] * pow2_inv(m);
+        __syncwarp();
+    }
+}
+template <int DP>
+__device__ void lg_chain_bwd(const float* mats, int64_t nm, const float* w0, float* out, float* ws) {
+    constexpr int Q = DP >= 32 ? DP / 32 : 1;
+    const int lane = threadIdx.x & 31;
+    const bool act = lane * Q < DP;
+    if (act)
+        for (int q = 0; q < Q; q++) ws[lane * Q + q] = w0[lane * Q + q];
+    __syncwarp();
+    for (int64_t i = nm - 1; i >= 0; i--) {
+        if (act)
+            for (int q = 0; q < Q; q++) out[i * DP + lane * Q + q] = ws[lane * Q + q];
+        const float* M = mats + (size_t)i * DP * DP;
+        float y[Q];
+#pragma unroll
+        for (int q = 0; q < Q; q++) y[q] = 0.0f;
+        if (act) {
+#pragma unroll
+            for (int q = 0; q < Q; q++) {
+                const float* row = M + (size_t)(lane * Q + q) * DP;
+                for (int j = 0; j < DP; j++) y[q] = fmaf(__ldcg(row + j), ws[j], y[q]);
+            }
+        }
+        float m = y[0];
+#pragma unroll
+        for (int q = 1; q < Q; q++) m = fmaxf(m, y[q]);
+        m = grp_max<32>(act ? m : 0.0f);
+        __syncwarp();
+        if (act)
+            for (int q = 0; q < Q; q++) ws[lane * Q + q] = y[q] * pow2_inv(m);
+        __syncwarp();
+    }
+}
+
+template <int DP, int OP>
+__global__ void __launch_bounds__(64) lg_carry_kernel(const LgParams p) {
+    constexpr bool MP = (OP == 1);
+    __shared__ float v0[DP], vs[2][DP];
+    const int64_t b = blockIdx.x;
+    const int warp = threadIdx.x >> 5;
+    const float* roots = p.groot + (size_t)b * p.NB * DP * DP;
+    for (int j = threadIdx.x; j < DP; j += blockDim.x) v0[j] = (MP ? 0.0f : 1.0f);
+    __syncthreads();
+    if (warp == 0) {
+        lg_chain_fwd<DP, MP>(roots, p.NB, v0, p.bpre + (size_t)b * p.NB * DP, vs[0]);
+    } else if (!MP) {
+        lg_chain_bwd<DP>(roots, p.NB, v0, p.bsuf + (size_t)b * p.NB * DP, vs[1]);
+    }
+}
+
+// ------------------------------------------------------------------------------------------- K3
+template <int DP, int OP>
+__global__ void __launch_bounds__(256) lg_sweep_kernel(const LgParams p) {
+    using C = LG<DP>;
+    constexpr int CPL = C::CPL, LPL = C::LPL, LPW = C::LPW, NLB = C::NLB;
+    constexpr bool MP = (OP == 1);
+    extern __shared__ __align__(128) uint8_t smem[];
+    float* lpre = reinterpret_cast<float*>(smem);          // [NLB][DP]
+    float* lsuf = lpre + NLB * DP;                          // [NLB][DP]
+    float* vec = lsuf + NLB * DP;                           // [NLB][DP] per-leaf broadcast vector
+    float* cw = vec + NLB * DP;                             // [2][DP] chain scratch
+    uint8_t* orig = reinterpret_cast<uint8_t*>(cw + 2 * DP);  // [NLB][DP] Viterbi origin maps
+    const int64_t b = blockIdx.y;
+    const int blk = blockIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int sub = lane / LPL, cl = lane % LPL;
+    const int lidx = warp * LPW + sub;
+    const int64_t L = (int64_t)blk * NLB + lidx;
+    const int64_t T = p.T;
+    const int D = p.D;
+    const float* leafs = p.leafagg + ((size_t)b * p.NL + (size_t)blk * NLB) * DP * DP;
+    int nleaf = NLB;  // leaves of this block that exist
+    if ((int64_t)blk * NLB + nleaf > p.NL) nleaf = (int)(p.NL - (int64_t)blk * NLB);
+    // leaf carries: chains through this block's leaves, from the block carries
+    if (warp == 0) {
+        lg_chain_fwd<DP, MP>(leafs, nleaf, p.bpre + ((size_t)b * p.NB + blk) * DP, lpre, cw);
+    } else if (warp == 1 && !MP) {
+        lg_chain_bwd<DP>(leafs, nleaf, p.bsuf + ((size_t)b * p.NB + blk) * DP, lsuf, cw + DP);
+    }
+    __syncthreads();
+    int n = 0;
+    if (L < p.NL) {
+        const int64_t a = L * p.SL;
+        n = (a < T) ? (int)((T - a < p.SL) ? T - a : p.SL) : 0;
+    }
+    int nmax = n;
+#pragma unroll
+    for (int o = LPL; o < 32; o <<= 1) nmax = max(nmax, __shfl_xor_sync(0xffffffffu, nmax, o));
+    const int64_t t0 = L * p.SL;
+    const float* ll = p.log_lik + (size_t)b * T * D;
+    float* vv = vec + lidx * DP;
+    uint32_t* sync = reinterpret_cast<uint32_t*>(p.ws_sync + b * 64);
+    unsigned long long* zero_code = reinterpret_cast<unsigned long long*>(sync + 4);
+    double part = 0.0;
+    int64_t zero_t = INT64_MAX;
+
+    if constexpr (!MP) {
+        // ---------------- forward filter over the leaf (lane owns CPL columns; A columns in regs)
+        float Acol[CPL][DP], pv[CPL];
+#pragma unroll
+        for (int c = 0; c < CPL; c++) {
+#pragma unroll
+            for (int k = 0; k < DP; k++) Acol[c][k] = lg_A(p, k, cl * CPL + c, false);
+            pv[c] = lg_pi(p, cl * CPL + c, false);
+        }
+        float a_own[CPL];
+        {
+            float s = 0.0f;
+#pragma unroll
+            for (int c = 0; c < CPL; c++) s += lpre[lidx * DP + cl * CPL + c];
+            s = grp_sum<LPL>(s);
+            const float r = (s > 0.0f) ? 1.0f / s : 0.0f;
+#pragma unroll
+            for (int c = 0; c < CPL; c++) {
+                a_own[c] = lpre[lidx * DP + cl * CPL + c] * r;
+                vv[cl * CPL + c] = a_own[c];
+            }
+        }
+        __syncwarp();
+        float rprod = 1.0f;
+        int rexp = 0;
+        double msum = 0.0;
+        float* filt = p.filtered;
+        for (int i = 0; i < nmax; i++) {
+            const bool act = i < n;
+            const int64_t t = t0 + i;
+            float v[CPL], l[CPL], ah[CPL];
+#pragma unroll
+            for (int c = 0; c < CPL; c++) {
+                const int j = cl * CPL + c;
+                v[c] = (act && j < D) ? __ldg(ll + t * D + j) : neg_inf();
+            }
+            float m = v[0];
+#pragma unroll
+            for (int c = 1; c < CPL; c++) m = fmaxf(m, v[c]);
+            m = grp_max<LPL>(m);
+            if (m > neg_inf()) msum += (cl == 0 && act) ? (double)m : 0.0;
+            else m = 0.0f;
+#pragma unroll
+            for (int c = 0; c < CPL; c++) {
+                l[c] = ex2((v[c] - m) * kLog2e);
+                ah[c] = 0.0f;
+            }
+            if (t == 0) {
+#pragma unroll
+                for (int c = 0; c < CPL; c++) ah[c] = pv[c] * l[c];
+            } else {
+#pragma unroll
+                for (int k4 = 0; k4 < DP; k4 += 4) {
+                    const float4 x = *reinterpret_cast<const float4*>(vv + k4);
+#pragma unroll
+                    for (int c = 0; c < CPL; c++) {
+                        ah[c] = fmaf(x.x, Acol[c][k4], ah[c]);
+                        ah[c] = fmaf(x.y, Acol[c][k4 + 1], ah[c]);
+                        ah[c] = fmaf(x.z, Acol[c][k4 + 2], ah[c]);
+                        ah[c] = fmaf(x.w, Acol[c][k4 + 3], ah[c]);
+                    }
+                }
+#pragma unroll
+                for (int c = 0; c < CPL; c++) ah[c] *= l[c];
+            }
+            float cs = 0.0f;
+#pragma unroll
+            for (int c = 0; c < CPL; c++) cs += ah[c];
+            cs = grp_sum<LPL>(cs);
+            if (act && !(cs > 0.0f) && t < zero_t) zero_t = t;
+            const float r = rcp(cs);
+            __syncwarp();
+            if (act) {  // a shorter half-warp leaf keeps its final state while its partner runs on
+#pragma unroll
+                for (int c = 0; c < CPL; c++) {
+                    a_own[c] = ah[c] * r;
+                    vv[cl * CPL + c] = a_own[c];
+                    const int j = cl * CPL + c;
+                    if (j < D) filt[((size_t)b * T + t) * D + j] = a_own[c];
+                }
+            }
+            __syncwarp();
+            if (act) {
+                rprod *= r;
+                const uint32_t bits = __float_as_uint(rprod);
+                rexp += (int)((bits >> 23) & 0xffu) - 127;
+                rprod = __uint_as_float((bits & 0x807fffffu) | 0x3f800000u);
+            }
+        }
+        if (n > 0 && cl == 0) {
+            float s = 0.0f;
+            for (int j = 0; j < DP; j++) s += vv[j];
+            part = log((double)s) - log((double)rprod) - (double)rexp * (double)kLn2 + msum;
+        }
+        __syncwarp();
+        // ---------------- backward pass + Eq. 14 (lane owns CPL rows; A rows in regs)
+        float Arow[CPL][DP];
+#pragma unroll
+        for (int c = 0; c < CPL; c++)
+#pragma unroll
+            for (int j = 0; j < DP; j++) Arow[c][j] = lg_A(p, cl * CPL + c, j, false);
+        float bt[CPL];
+#pragma unroll
+        for (int c = 0; c < CPL; c++) bt[c] = lsuf[lidx * DP + cl * CPL + c];
+        for (int i = nmax - 1; i >= 0; i--) {
+            const bool act = i < n;
+            const int64_t t = t0 + i;
+            float g[CPL];
+            float z = 0.0f;
+#pragma unroll
+            for (int c = 0; c < CPL; c++) {
+                const int j = cl * CPL + c;
+                const float a = (act && j < D) ? filt[((size_t)b * T + t) * D + j] : 0.0f;
+                g[c] = a * bt[c];
+                z += g[c];
+            }
+            z = grp_sum<LPL>(z);
+            const float rz = rcp(z);
+#pragma unroll
+            for (int c = 0; c < CPL; c++) {
+                const int j = cl * CPL + c;
+                if (act && j < D) p.smoothed[((size_t)b * T + t) * D + j] = g[c] * rz;
+            }
+            if (i > 0) {
+                float v[CPL];
+#pragma unroll
+                for (int c = 0; c < CPL; c++) {
+                    const int j = cl * CPL + c;
+                    v[c] = (act && j < D) ? __ldg(ll + t * D + j) : neg_inf();
+                }
+                float m = v[0];
+#pragma unroll
+                for (int c = 1; c < CPL; c++) m = fmaxf(m, v[c]);
+                m = grp_max<LPL>(m);
+                if (!(m > neg_inf())) m = 0.0f;
+                __syncwarp();
+                if (act) {
+#pragma unroll
+                    for (int c = 0; c < CPL; c++) vv[cl * CPL + c] = ex2((v[c] - m) * kLog2e) * bt[c];
+                }
+                __syncwarp();
+                float y[CPL];
+#pragma unroll
+                for (int c = 0; c < CPL; c++) y[c] = 0.0f;
+#pragma unroll
+                for (int k4 = 0; k4 < DP; k4 += 4) {
+                    const float4 x = *reinterpret_cast<const float4*>(vv + k4);
+#pragma unroll
+                    for (int c = 0; c < CPL; c++) {
+                        y[c] = fmaf(Arow[c][k4], x.x, y[c]);
+                        y[c] = fmaf(Arow[c][k4 + 1], x.y, y[c]);
+                        y[c] = fmaf(Arow[c][k4 + 2], x.z, y[c]);
+                        y[c] = fmaf(Arow[c][k4 + 3], x.w, y[c]);
+                    }
+                }
+                float mx = y[0];
+#pragma unroll
+                for (int c = 1; c < CPL; c++) mx = fmaxf(mx, y[c]);
+                mx = grp_max<LPL>(mx);
+                const float sc = pow2_inv(mx);
+                if (act) {
+#pragma unroll
+                    for (int c = 0; c < CPL; c++) bt[c] = y[c] * sc;
+                }
+            }
+        }
+    } else {
+        // ---------------- Viterbi forward sweep with backpointers (lane owns CPL columns)
+        float LAc[CPL][DP], lpv[CPL];
+#pragma unroll
+        for (int c = 0; c < CPL; c++) {
+#pragma unroll
+            for (int k = 0; k < DP; k++) LAc[c][k] = lg_A(p, k, cl * CPL + c, true);
+            lpv[c] = lg_pi(p, cl * CPL + c, true);
+        }
+        uint8_t* og = orig + lidx * DP;
+#pragma unroll
+        for (int c = 0; c < CPL; c++) {
+            vv[cl * CPL + c] = lpre[lidx * DP + cl * CPL + c];
+            og[cl * CPL + c] = (uint8_t)(cl * CPL + c);
+        }
+        __syncwarp();
+        double acc = 0.0;
+        float V[CPL];
+#pragma unroll
+        for (int c = 0; c < CPL; c++) V[c] = vv[cl * CPL + c];
+        for (int i = 0; i < nmax; i++) {
+            const bool act = i < n;
+            const int64_t t = t0 + i;
+            float v[CPL];
+#pragma unroll
+            for (int c = 0; c < CPL; c++) {
+                const int j = cl * CPL + c;
+                v[c] = (act && j < D) ? __ldg(ll + t * D + j) : neg_inf();
+            }
+            float m = v[0];
+#pragma unroll
+            for (int c = 1; c < CPL; c++) m = fmaxf(m, v[c]);
+            m = grp_max<LPL>(m);
+            if (!(m > neg_inf())) m = 0.0f;
+            float best[CPL];
+            int arg[CPL];
+#pragma unroll
+            for (int c = 0; c < CPL; c++) {
+                best[c] = neg_inf();
+                arg[c] = 0;
+            }
+#pragma unroll
+            for (int k = 0; k < DP; k++) {
+                const float vk = vv[k];
+#pragma unroll
+                for (int c = 0; c < CPL; c++) {
+                    const float sc = vk + ((t == 0) ? lpv[c] : LAc[c][k]);
+                    if (sc > best[c]) {
+                        best[c] = sc;
+                        arg[c] = k;
+                    }
+                }
+            }
+            float o = neg_inf(), Vn[CPL];
+#pragma unroll
+            for (int c = 0; c < CPL; c++) {
+                Vn[c] = best[c] + (v[c] - m);
+                o = fmaxf(o, Vn[c]);
+            }
+            o = grp_max<LPL>(o);
+            if (!(o > neg_inf())) {
+                if (act && t < zero_t) zero_t = t;
+                o = 0.0f;
+            }
+            if (act && cl == 0) acc += (double)(o + m);
+            uint8_t on[CPL];
+#pragma unroll
+            for (int c = 0; c < CPL; c++) on[c] = og[arg[c]];
+            __syncwarp();
+            if (act) {  // inactive half-warp leaves keep their final V / origin map
+#pragma unroll
+                for (int c = 0; c < CPL; c++) {
+                    const int j = cl * CPL + c;
+                    V[c] = Vn[c] - o;
+                    vv[j] = V[c];
+                    og[j] = on[c];
+                    p.bp[((size_t)b * T + t) * DP + j] = (uint8_t)arg[c];
+                }
+            }
+            __syncwarp();
+        }
+        part = acc;
+        {
+            // x*_{T-1} = smallest argmax of V (reduction warp-uniform, used by the leaf ending at T)
+            int xs = DP;
+#pragma unroll
+            for (int c = CPL - 1; c >= 0; c--)
+                if (V[c] == 0.0f && cl * CPL + c < D) xs = cl * CPL + c;
+#pragma unroll
+            for (int o = 1; o < LPL; o <<= 1) xs = min(xs, __shfl_xor_sync(0xffffffffu, xs, o));
+            if (n > 0) {
+                // leaf map f(x_end) = state before the leaf
+#pragma unroll
+                for (int c = 0; c < CPL; c++)
+                    p.lmap[((size_t)b * p.NL + L) * DP + cl * CPL + c] = og[cl * CPL + c];
+                if (t0 + n == T && cl == 0) p.xstar[b] = xs;
+            }
+        }
+        __syncthreads();
+        // block map = f_first o ... o f_last over this block's leaves (thread x < DP computes entry x)
+        if (threadIdx.x < DP) {
+            int x = threadIdx.x;
+            for (int q = nleaf - 1; q >= 0; q--) x = og_global_lookup(p, b, (int64_t)blk * NLB + q, x, DP);
+            p.bmap[((size_t)b * p.NB + blk) * DP + threadIdx.x] = (uint8_t)x;
+        }
+    }
+    // per-leaf partial sums (fixed order later) and info
+    if (L < p.NL && cl == 0) p.partial[(size_t)b * p.NL + L] = part;
+    if (zero_t != INT64_MAX) atomicMax(zero_code, (1ull << 62) - (unsigned long long)zero_t);
+}
+
+// ------------------------------------------------------------------------------------------- K4/K5
+__global__ void lg_resolve_kernel(const LgParams p, int DP) {
+    // one CTA per sequence: end state of every block = (F_{blk+1} o ... o F_{NB-1})(x*)
+    const int64_t b = blockIdx.x;
+    if (threadIdx.x != 0) return;
+    int x = p.xstar[b];
+    if (x < 0 || x >= DP) x = 0;
+    for (int64_t blk = p.NB - 1; blk >= 0; blk--) {
+        p.bend[b * p.NB + blk] = x;
+        x = p.bmap[((size_t)b * p.NB + blk) * DP + x];
+    }
+}
+
+template <int DP>
+__global__ void __launch_bounds__(256) lg_backtrack_kernel(const LgParams p) {
+    using C = LG<DP>;
+    constexpr int NLB = C::NLB;
+    __shared__ int ends[NLB];
+    const int64_t b = blockIdx.y;
+    const int blk = blockIdx.x;
+    const int64_t T = p.T;
+    int nleaf = NLB;
+    if ((int64_t)blk * NLB + nleaf > p.NL) nleaf = (int)(p.NL - (int64_t)blk * NLB);
+    if (threadIdx.x == 0) {
+        int x = p.bend[b * p.NB + blk];
+        for (int q = nleaf - 1; q >= 0; q--) {
+            ends[q] = x;
+            x = p.lmap[((size_t)b * p.NL + (int64_t)blk * NLB + q) * DP + x];
+        }
+    }
+    __syncthreads();
+    // one thread per leaf backtracks through its backpointers
+    const int q = threadIdx.x;
+    if (q < nleaf) {
+        const int64_t L = (int64_t)blk * NLB + q;
+        const int64_t a = L * p.SL;
+        const int n = (int)((T - a < p.SL) ? T - a : p.SL);
+        int x = ends[q];
+        for (int i = n - 1; i >= 0; i--) {
+            const int64_t t = a + i;
+            p.path[(size_t)b * T + t] = x;
+            x = p.bp[((size_t)b * T + t) * DP + x];
+        }
+    }
+}
+
+__global__ void lg_finalize_kernel(const LgParams p) {
+    // one CTA (256 threads) per sequence: fixed-order sum of the NL partials, info, reset sync words
+    __shared__ double red[8];
+    const int64_t b = blockIdx.x;
+    const int64_t per = (p.NL + 255) / 256;
+    double v = 0.0;
+    for (int64_t i = threadIdx.x * per; i < (threadIdx.x + 1) * per && i < p.NL; i++) v += p.partial[b * p.NL + i];
+#pragma unroll
+    for (int st = 16; st >= 1; st >>= 1) v += __shfl_down_sync(0xffffffffu, v, st);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int w = 0; w < 8; w++) s += red[w];
+        p.scalar_out[b] = s;
+        uint32_t* sync = reinterpret_cast<uint32_t*>(p.ws_sync + b * 64);
+        unsigned long long* zero_code = reinterpret_cast<unsigned long long*>(sync + 4);
+        const uint32_t badf = atomicExch(sync + 8, 0u);
+        const unsigned long long zc = atomicExch(zero_code, 0ull);
+        int32_t inf = 0;
+        if (badf) inf = -1;
+        else if (zc) inf = (int32_t)((1ull << 62) - zc + 1ull);
+        p.info[b] = inf;
+    }
+}
+
+// ------------------------------------------------------------------------------------------- host
+template <int DP, int OP>
+static cudaError_t lg_launch(const LgParams& p, cudaStream_t s) {
+    using C = LG<DP>;
+    const size_t sm1 = (size_t)C::NLB * DP * DP * 4;
+    static size_t cfg1 = 0, cfg3 = 0;
+    if (cfg1 < sm1) {
+        cudaError_t e = cudaFuncSetAttribute(lg_leaf_kernel<DP, OP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
+        if (e != cudaSuccess) return e;
+        cfg1 = sm1;
+    }
+    const size_t sm3 = (size_t)(3 * C::NLB + 2) * DP * 4 + (size_t)C::NLB * DP + 64;
+    if (cfg3 < sm3) {
+        cudaError_t e = cudaFuncSetAttribute(lg_sweep_kernel<DP, OP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm3);
+        if (e != cudaSuccess) return e;
+        cfg3 = sm3;
+    }
+    const dim3 grid((unsigned)p.NB, (unsigned)p.B);
+    lg_leaf_kernel<DP, OP><<<grid, 256, sm1, s>>>(p);
+    lg_carry_kernel<DP, OP><<<(unsigned)p.B, 64, 0, s>>>(p);
+    lg_sweep_kernel<DP, OP><<<grid, 256, sm3, s>>>(p);
+    if (OP == 1) {
+        lg_resolve_kernel<<<(unsigned)p.B, 32, 0, s>>>(p, DP);
+        lg_backtrack_kernel<DP><<<grid, 256, 0, s>>>(p);
+    }
+    lg_finalize_kernel<<<(unsigned)p.B, 256, 0, s>>>(p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_large(int DP, int op, const LgParams& p, cudaStream_t s) {
+    switch (DP) {
+        case 16: return op == 0 ? lg_launch<16, 0>(p, s) : lg_launch<16, 1>(p, s);
+        case 32: return op == 0 ? lg_launch<32, 0>(p, s) : lg_launch<32, 1>(p, s);
+        case 64: return op == 0 ? lg_launch<64, 0>(p, s) : lg_launch<64, 1>(p, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+int large_leaves_per_block(int DP) { return DP == 16 ? LG<16>::NLB : (DP == 32 ? LG<32>::NLB : LG<64>::NLB); }
+
+}  // namespace hmm

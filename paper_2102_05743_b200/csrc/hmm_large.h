@@ -1,0 +1,36 @@
+// hmm_large.h — parameter block of the large-D kernels (hmm_large.cu), filled by hmm_abi.cu.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+
+namespace hmm {
+
+struct LgParams {
+    int64_t T, B;
+    int D;
+    int64_t SL;  // steps per leaf
+    int64_t NL;  // leaves per sequence
+    int64_t NB;  // blocks (CTAs of K1/K3) per sequence
+    const float* log_pi;
+    const float* log_A;
+    const float* log_lik;
+    float* filtered;
+    float* smoothed;
+    int32_t* path;
+    double* scalar_out;
+    int32_t* info;
+    // workspace views
+    uint8_t* ws_sync;   // [B][64 B]
+    float* leafagg;     // [B][NL][DP*DP]
+    float* groot;       // [B][NB][DP*DP]
+    float* bpre;        // [B][NB][DP]
+    float* bsuf;        // [B][NB][DP]
+    double* partial;    // [B][NL]
+    uint8_t* bp;        // [B][T][DP]   Viterbi backpointers
+    uint8_t* lmap;      // [B][NL][DP]  Viterbi leaf maps
+    uint8_t* bmap;      // [B][NB][DP]  Viterbi block maps
+    int32_t* bend;      // [B][NB]      Viterbi block end states
+    int32_t* xstar;     // [B]
+};
+
+}  // namespace hmm

@@ -35,7 +35,9 @@ def test_invalid_arguments_rejected_on_host(L):
     assert L.hmm_viterbi(4, -5, p, p, p, p, p, p, p, 1 << 20, None) == 1
     assert L.hmm_smooth_batched(4, 10, 0, p, p, p, p, p, p, p, p, 1 << 20, None) == 1
     # D beyond this build's range
-    assert L.hmm_smooth(HMM_D := H.HMM_MAX_D + 1, 10, p, p, p, p, p, p, p, p, 1 << 20, None) == 3
+    assert L.hmm_smooth(H.HMM_MAX_D + 1, 10, p, p, p, p, p, p, p, p, 1 << 20, None) == 3
+    # large-D smoother needs the filtered buffer (alpha staging)
+    assert L.hmm_smooth(16, 10, p, p, p, None, p, p, p, p, 1 << 20, None) == 3
     # NULL required pointers
     assert L.hmm_smooth(4, 10, None, p, p, p, p, p, p, p, 1 << 20, None) == 1
     assert L.hmm_smooth(4, 10, p, p, p, p, None, p, p, p, 1 << 20, None) == 1   # smoothed NULL

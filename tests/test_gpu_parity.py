@@ -214,3 +214,54 @@ def test_logz_no_normalisation_drift():
     _, _, lz, info = gpu_smooth(wl)
     per_state = lp.astype(np.float64) + ll.astype(np.float64).sum(0)
     assert abs(lz[0] - np.logaddexp.reduce(per_state)) < 1.5e-8 * T
+
+
+# ---------------------------------------------------------------- large D (9..64): BASELINE configs ③ ④
+@pytest.mark.parametrize("D,T", [(9, 1000), (16, 777), (16, 20_000), (24, 5000), (32, 4097), (33, 3000), (48, 2000),
+                                 (64, 1), (64, 17), (64, 10_000)])
+def test_large_D_smoother(D, T):
+    wl = W.dense(D, T, seed=100 + D)
+    check_smooth(wl, *gpu_smooth(wl))
+
+
+@pytest.mark.parametrize("D,T", [(9, 1000), (16, 20_000), (24, 5000), (32, 4097), (48, 2000), (64, 1), (64, 10_000)])
+def test_large_D_viterbi(D, T):
+    wl = W.dense(D, T, seed=200 + D)
+    check_viterbi(wl, *gpu_viterbi(wl))
+    wp = W.planted(D, min(T, 3000), seed=D)
+    path, lp, info = gpu_viterbi(wp)
+    assert np.array_equal(path, wp.states)
+
+
+def test_config3_dense_D64_T1e5():
+    """BASELINE config ③: dense D=64, T=1e5 (Dirichlet(1) rows, Gaussian emissions)."""
+    wl = W.dense(64, 100_000, seed=3)
+    check_smooth(wl, *gpu_smooth(wl))
+    check_viterbi(wl, *gpu_viterbi(wl))
+
+
+def test_config4_batched_B1024_D16_T4096():
+    """BASELINE config ④: B=1024 sequences, D=16, T=4096, shared model; sampled sequences vs oracle."""
+    wl = W.dense_batch(1024, 16, 4096)
+    f, s, lz, info = gpu_smooth(wl)
+    assert (info == 0).all()
+    for b in (0, 1, 511, 1023):
+        check_smooth(wl, f, s, lz, info, b=b)
+    path, lp, vinfo = gpu_viterbi(wl)
+    assert (vinfo == 0).all()
+    for b in (0, 7, 900, 1023):
+        check_viterbi(wl, path, lp, vinfo, b=b)
+    # every sequence: log Z finite and rows of smoothed sum to 1
+    assert np.isfinite(lz).all()
+    np.testing.assert_allclose(s.sum(-1), 1.0, atol=1e-5)
+
+
+def test_large_D_info():
+    wl = W.dense(20, 5000, seed=1)
+    wl.log_lik[3333, :] = -np.inf
+    assert int(gpu_smooth(wl)[3][0]) == 3334
+    assert int(gpu_viterbi(wl)[2][0]) == 3334
+    wl = W.dense(20, 5000, seed=1)
+    wl.log_lik[100, 5] = np.nan
+    assert int(gpu_smooth(wl)[3][0]) == -1
+    assert int(gpu_viterbi(wl)[2][0]) == -1
