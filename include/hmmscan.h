@@ -110,6 +110,52 @@ hmm_status_t hmm_viterbi_batched(int D, int64_t T, int64_t B, const float* log_p
                                  void* workspace, size_t workspace_bytes, void* stream);
 
 /*
+ * Split-phase distributed execution (one sequence partitioned along T across `world` ranks, one
+ * process per GPU).  Rank r owns the contiguous global steps
+ * [t_base, t_base + T_local) and passes its slice of log_lik.  The library never calls NCCL: between
+ * the phases the CALLER all-gathers small fixed-size blobs (e.g. torch.distributed
+ * all_gather_into_tensor over NCCL/NVLink) into rank order.  All phases of one rank must use the same
+ * workspace (hmm_dist_workspace_size bytes, zero-filled once), on the same stream, in order.
+ * Supported for 1 <= D <= 8 and a single sequence.
+ *
+ * Smoother (Algorithm 3 across ranks; the rank aggregate is the ordered product of the rank's
+ * elements, Def. 3 / PAPER.md:281-290):
+ *   1. hmm_smooth_dist_reduce  -> agg_out (hmm_dist_agg_bytes(D) bytes, 16-B aligned device memory)
+ *   2. caller: all-gather the world aggregates -> agg_all[world] (rank order)
+ *   3. hmm_smooth_dist_finish  -> filtered/smoothed of the local slice, log_z_partial[1] (double).
+ *      log Z = sum over ranks of log_z_partial, in rank order (caller: all-gather + sum).
+ * Viterbi (Def. 5 aggregates; rank backpointer maps compose right to left):
+ *   1. hmm_viterbi_dist_reduce  -> agg_out
+ *   2. caller: all-gather -> agg_all
+ *   3. hmm_viterbi_dist_forward -> record_out (hmm_dist_record_bytes() = 16 bytes: u64 map, i32 x*),
+ *      log_prob_partial[1]; log_prob = sum of partials over ranks.
+ *   4. caller: all-gather the records -> records_all[world]
+ *   5. hmm_viterbi_dist_finish  -> path of the local slice.
+ * info: reduce reports bad inputs (-1); finish/forward report the first impossible GLOBAL step + 1.
+ */
+size_t hmm_dist_agg_bytes(int D);
+size_t hmm_dist_record_bytes(void);
+size_t hmm_dist_workspace_size(int op, int D, int64_t T_local);
+hmm_status_t hmm_smooth_dist_reduce(int D, int64_t T_local, int64_t t_base, const float* log_pi, const float* log_A,
+                                    const float* log_lik, void* agg_out, int32_t* info, void* workspace,
+                                    size_t workspace_bytes, void* stream);
+hmm_status_t hmm_smooth_dist_finish(int D, int64_t T_local, int64_t t_base, const float* log_pi, const float* log_A,
+                                    const float* log_lik, const void* agg_all, int rank, int world, float* filtered,
+                                    float* smoothed, double* log_z_partial, int32_t* info, void* workspace,
+                                    size_t workspace_bytes, void* stream);
+hmm_status_t hmm_viterbi_dist_reduce(int D, int64_t T_local, int64_t t_base, const float* log_pi, const float* log_A,
+                                     const float* log_lik, void* agg_out, int32_t* info, void* workspace,
+                                     size_t workspace_bytes, void* stream);
+hmm_status_t hmm_viterbi_dist_forward(int D, int64_t T_local, int64_t t_base, const float* log_pi,
+                                      const float* log_A, const float* log_lik, const void* agg_all, int rank,
+                                      int world, void* record_out, double* log_prob_partial, int32_t* info,
+                                      void* workspace, size_t workspace_bytes, void* stream);
+hmm_status_t hmm_viterbi_dist_finish(int D, int64_t T_local, int64_t t_base, const float* log_pi, const float* log_A,
+                                     const float* log_lik, const void* records_all, int rank, int world,
+                                     int32_t* path, int32_t* info, void* workspace, size_t workspace_bytes,
+                                     void* stream);
+
+/*
  * Profiling / introspection (not part of the compute path).
  *   hmm_debug_set_timers: for calls made later from the calling host thread, CTA phase timestamps
  *     (%globaltimer, ns) are written to device_buf[(b*G + c)*16 + i] (NULL disables).

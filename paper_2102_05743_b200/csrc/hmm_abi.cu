@@ -51,7 +51,7 @@ int pow2_ceil(int x) {
 }
 
 // Work decomposition for the small-D kernels (see hmm_plan.h and DESIGN.md §"Decomposition").
-bool make_plan(int D, int op, int64_t T, int64_t B, Plan& P) {
+bool make_plan(int D, int op, int64_t T, int64_t B, Plan& P, bool chunked = false) {
     DevInfo di;
     if (!dev_info(di)) return false;
     P = Plan{};
@@ -74,7 +74,7 @@ bool make_plan(int D, int op, int64_t T, int64_t B, Plan& P) {
     P.R = R;
     // fused: the whole CTA range stays resident in shared memory
     hmm::SmemLayout Lf = hmm::small_smem_layout(D, op, (int)std::min<int64_t>(R, 1 << 30), 1, (int)G);
-    if (R <= (1 << 24) && Lf.total <= smax) {
+    if (!chunked && R <= (1 << 24) && Lf.total <= smax) {
         int S = (int)cdiv(R, NT);
         if ((S & 1) == 0) S += 1;
         P.S = S;
@@ -90,6 +90,10 @@ bool make_plan(int D, int op, int64_t T, int64_t B, Plan& P) {
             const int K = (int)cdiv(R, chunk);
             const int KP = pow2_ceil(K);
             hmm::SmemLayout L = hmm::small_smem_layout(D, op, chunk, KP, (int)G);
+            if (chunked && (int64_t)chunk > R && S > 3) {  // split-phase: keep chunks no longer than the range
+                S -= 2;
+                continue;
+            }
             if (L.total <= smax && KP <= 1024) {
                 P.S = S; P.chunk = chunk; P.K = K; P.KP = KP; P.smem = L.total;
                 break;
@@ -118,6 +122,9 @@ bool make_plan(int D, int op, int64_t T, int64_t B, Plan& P) {
     off = (off + 255) & ~(size_t)255;
     P.ws_lmap = off;
     if (op == 1 && !P.fused) off += (size_t)B * P.G * P.K * (size_t)NT * 8;
+    off = (off + 255) & ~(size_t)255;
+    P.ws_cmap = off;
+    if (op == 1 && !P.fused) off += (size_t)B * P.G * P.K * 8;
     off = (off + 255) & ~(size_t)255;
     P.ws_total = off;
     return true;
@@ -168,11 +175,21 @@ bool make_large_plan(int D, int op, int64_t T, int64_t B, LgPlan& P) {
 bool al4(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 3u) == 0; }
 bool al8(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 7u) == 0; }
 
+struct DistArgs {
+    int mode = 0, rank = 0, world = 1;
+    int64_t t_base = 0;
+    const float* agg_all = nullptr;
+    float* agg_out = nullptr;
+    const uint8_t* rec_all = nullptr;
+    uint8_t* rec_out = nullptr;
+};
+
 hmm_status_t run(int op, int D, int64_t T, int64_t B, const float* log_pi, const float* log_A, const float* log_lik,
                  float* filtered, float* smoothed, int32_t* path, double* scalar, int32_t* info, void* ws,
-                 size_t ws_bytes, void* stream) {
+                 size_t ws_bytes, void* stream, const DistArgs& da = DistArgs()) {
     if (D < 1 || T < 1 || B < 1 || B > 65535) return HMM_ERR_INVALID_VALUE;
     if (D > HMM_MAX_D) return HMM_ERR_UNSUPPORTED;
+    if (D > 8 && da.mode != hmm::HMM_MODE_FULL) return HMM_ERR_UNSUPPORTED;  // split phase: D <= 8
     if (D > 8) {
         if (!log_pi || !log_A || !log_lik || !scalar || !info) return HMM_ERR_INVALID_VALUE;
         if (op == 0 && !smoothed) return HMM_ERR_INVALID_VALUE;
@@ -202,14 +219,21 @@ hmm_status_t run(int op, int D, int64_t T, int64_t B, const float* log_pi, const
         cudaError_t e = hmm::launch_large(G.DP, op, lp, static_cast<cudaStream_t>(stream));
         return e == cudaSuccess ? HMM_SUCCESS : HMM_ERR_CUDA;
     }
-    if (!log_pi || !log_A || !log_lik || !scalar || !info) return HMM_ERR_INVALID_VALUE;
-    if (op == 0 && !smoothed) return HMM_ERR_INVALID_VALUE;
-    if (op == 1 && !path) return HMM_ERR_INVALID_VALUE;
-    if (!al4(log_pi) || !al4(log_A) || !al4(log_lik) || !al8(scalar) || !al4(info)) return HMM_ERR_INVALID_VALUE;
+    const bool dist = da.mode != hmm::HMM_MODE_FULL;
+    const bool need_scalar = !dist || da.mode == hmm::HMM_MODE_SFINISH || da.mode == hmm::HMM_MODE_VFORWARD;
+    if (!log_pi || !log_A || !log_lik || !info || (need_scalar && !scalar)) return HMM_ERR_INVALID_VALUE;
+    if (op == 0 && (da.mode == hmm::HMM_MODE_FULL || da.mode == hmm::HMM_MODE_SFINISH) && !smoothed)
+        return HMM_ERR_INVALID_VALUE;
+    if (op == 1 && (da.mode == hmm::HMM_MODE_FULL || da.mode == hmm::HMM_MODE_VFINISH) && !path)
+        return HMM_ERR_INVALID_VALUE;
+    if (!al4(log_pi) || !al4(log_A) || !al4(log_lik) || (scalar && !al8(scalar)) || !al4(info))
+        return HMM_ERR_INVALID_VALUE;
     if ((filtered && !al4(filtered)) || (smoothed && !al4(smoothed)) || (path && !al4(path)))
         return HMM_ERR_INVALID_VALUE;
+    if (dist && (D > 8 || B != 1 || da.world < 1 || da.rank < 0 || da.rank >= da.world || da.t_base < 0))
+        return D > 8 ? HMM_ERR_UNSUPPORTED : HMM_ERR_INVALID_VALUE;
     Plan P;
-    if (!make_plan(D, op, T, B, P)) return HMM_ERR_UNSUPPORTED;
+    if (!make_plan(D, op, T, B, P, dist)) return HMM_ERR_UNSUPPORTED;
     if (!ws || ws_bytes < P.ws_total || (reinterpret_cast<uintptr_t>(ws) & 255u)) return HMM_ERR_WORKSPACE;
     hmm::KParams kp;
     std::memset(&kp, 0, sizeof(kp));
@@ -221,6 +245,10 @@ hmm_status_t run(int op, int D, int64_t T, int64_t B, const float* log_pi, const
     kp.ws_chunk = P.ws_chunk; kp.chunk_slot = P.chunk_slot; kp.ws_bp = P.ws_bp; kp.ws_lmap = P.ws_lmap;
     kp.L = hmm::small_smem_layout(D, op, P.chunk, P.KP, P.G);
     kp.timers = t_timers;
+    kp.ws_cmap = P.ws_cmap;
+    kp.mode = da.mode; kp.rank = da.rank; kp.world = da.world; kp.t_base = da.t_base;
+    kp.agg_all = da.agg_all; kp.agg_stride = (int)(hmm::align16((size_t)D * D * 4) / 4);
+    kp.agg_out = da.agg_out; kp.rec_all = da.rec_all; kp.rec_out = da.rec_out;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     cudaError_t e = hmm::launch_small(D, op, (unsigned)P.G, (unsigned)P.B, P.smem, P.coop, kp, s);
     return e == cudaSuccess ? HMM_SUCCESS : HMM_ERR_CUDA;
@@ -277,6 +305,68 @@ hmm_status_t hmm_viterbi(int D, int64_t T, const float* log_pi, const float* log
                          void* stream) {
     return run(1, D, T, 1, log_pi, log_A, log_lik, nullptr, nullptr, path, log_prob, info, workspace,
                workspace_bytes, stream);
+}
+
+size_t hmm_dist_agg_bytes(int D) { return (D < 1 || D > 8) ? 0 : hmm::align16((size_t)D * D * 4); }
+
+size_t hmm_dist_record_bytes(void) { return 16; }
+
+size_t hmm_dist_workspace_size(int op, int D, int64_t T_local) {
+    if ((op != 0 && op != 1) || D < 1 || D > 8 || T_local < 1) return 0;
+    Plan P;
+    if (!make_plan(D, op, T_local, 1, P, true)) return 0;
+    return P.ws_total;
+}
+
+hmm_status_t hmm_smooth_dist_reduce(int D, int64_t T_local, int64_t t_base, const float* log_pi, const float* log_A,
+                                    const float* log_lik, void* agg_out, int32_t* info, void* workspace,
+                                    size_t workspace_bytes, void* stream) {
+    if (!agg_out || (reinterpret_cast<uintptr_t>(agg_out) & 15u)) return HMM_ERR_INVALID_VALUE;
+    DistArgs da; da.mode = hmm::HMM_MODE_REDUCE; da.t_base = t_base; da.agg_out = static_cast<float*>(agg_out);
+    return run(0, D, T_local, 1, log_pi, log_A, log_lik, nullptr, nullptr, nullptr, nullptr, info, workspace,
+               workspace_bytes, stream, da);
+}
+
+hmm_status_t hmm_smooth_dist_finish(int D, int64_t T_local, int64_t t_base, const float* log_pi, const float* log_A,
+                                    const float* log_lik, const void* agg_all, int rank, int world, float* filtered,
+                                    float* smoothed, double* log_z_partial, int32_t* info, void* workspace,
+                                    size_t workspace_bytes, void* stream) {
+    if (!agg_all) return HMM_ERR_INVALID_VALUE;
+    DistArgs da; da.mode = hmm::HMM_MODE_SFINISH; da.t_base = t_base; da.rank = rank; da.world = world;
+    da.agg_all = static_cast<const float*>(agg_all);
+    return run(0, D, T_local, 1, log_pi, log_A, log_lik, filtered, smoothed, nullptr, log_z_partial, info, workspace,
+               workspace_bytes, stream, da);
+}
+
+hmm_status_t hmm_viterbi_dist_reduce(int D, int64_t T_local, int64_t t_base, const float* log_pi, const float* log_A,
+                                     const float* log_lik, void* agg_out, int32_t* info, void* workspace,
+                                     size_t workspace_bytes, void* stream) {
+    if (!agg_out || (reinterpret_cast<uintptr_t>(agg_out) & 15u)) return HMM_ERR_INVALID_VALUE;
+    DistArgs da; da.mode = hmm::HMM_MODE_REDUCE; da.t_base = t_base; da.agg_out = static_cast<float*>(agg_out);
+    return run(1, D, T_local, 1, log_pi, log_A, log_lik, nullptr, nullptr, nullptr, nullptr, info, workspace,
+               workspace_bytes, stream, da);
+}
+
+hmm_status_t hmm_viterbi_dist_forward(int D, int64_t T_local, int64_t t_base, const float* log_pi,
+                                      const float* log_A, const float* log_lik, const void* agg_all, int rank,
+                                      int world, void* record_out, double* log_prob_partial, int32_t* info,
+                                      void* workspace, size_t workspace_bytes, void* stream) {
+    if (!agg_all || !record_out || (reinterpret_cast<uintptr_t>(record_out) & 15u)) return HMM_ERR_INVALID_VALUE;
+    DistArgs da; da.mode = hmm::HMM_MODE_VFORWARD; da.t_base = t_base; da.rank = rank; da.world = world;
+    da.agg_all = static_cast<const float*>(agg_all); da.rec_out = static_cast<uint8_t*>(record_out);
+    return run(1, D, T_local, 1, log_pi, log_A, log_lik, nullptr, nullptr, nullptr, log_prob_partial, info,
+               workspace, workspace_bytes, stream, da);
+}
+
+hmm_status_t hmm_viterbi_dist_finish(int D, int64_t T_local, int64_t t_base, const float* log_pi, const float* log_A,
+                                     const float* log_lik, const void* records_all, int rank, int world,
+                                     int32_t* path, int32_t* info, void* workspace, size_t workspace_bytes,
+                                     void* stream) {
+    if (!records_all) return HMM_ERR_INVALID_VALUE;
+    DistArgs da; da.mode = hmm::HMM_MODE_VFINISH; da.t_base = t_base; da.rank = rank; da.world = world;
+    da.rec_all = static_cast<const uint8_t*>(records_all);
+    return run(1, D, T_local, 1, log_pi, log_A, log_lik, nullptr, nullptr, path, nullptr, info, workspace,
+               workspace_bytes, stream, da);
 }
 
 hmm_status_t hmm_smooth_batched(int D, int64_t T, int64_t B, const float* log_pi, const float* log_A,

@@ -83,17 +83,16 @@ __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long
     return v;
 }
 
-// Arrive-and-wait among the G CTAs of a sequence on a monotonic 64-bit counter: every CTA adds 1
-// (release) and thread 0 spins (acquire) until the counter reaches G*epoch.  The counter is never
-// reset, so there is no extra round trip for a generation bump and a zero-filled workspace is valid.
+// Arrive-and-wait among the G CTAs of a sequence: every CTA adds 1 (release) and thread 0 spins
+// (acquire) until the counter reaches G.  The counters are reset to 0 by the last CTA of the launch
+// (after every CTA has passed every wait), so a zero-filled workspace stays valid across calls.
 // All G CTAs must be co-resident (cooperative launch).
-__device__ __forceinline__ void group_arrive_wait(unsigned long long* counter, uint32_t G, uint32_t epoch) {
+__device__ __forceinline__ void group_arrive_wait(unsigned long long* counter, uint32_t G) {
     __syncthreads();
     if (threadIdx.x == 0 && G > 1) {
         __threadfence();
         asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(counter) : "memory");
-        const unsigned long long target = (unsigned long long)G * epoch;
-        while (ld_acquire_u64(counter) < target) {
+        while (ld_acquire_u64(counter) < (unsigned long long)G) {
         }
     }
     __syncthreads();

@@ -98,6 +98,7 @@ struct Plan {
     size_t chunk_slot = 0;
     size_t ws_bp = 0;        // Viterbi non-fused: backpointers, B*G*K*chunk*bpb bytes
     size_t ws_lmap = 0;      // Viterbi non-fused: leaf maps, B*G*K*NT*8 bytes
+    size_t ws_cmap = 0;      // Viterbi non-fused: chunk maps, B*G*K*8 bytes
     size_t ws_total = 0;
 };
 
@@ -121,6 +122,18 @@ struct KParams {
     size_t ws_sync, ws_slots, slot_bytes, ws_chunk, chunk_slot, ws_bp, ws_lmap;
     SmemLayout L;
     unsigned long long* timers;  // optional [B*G*16] %globaltimer stamps per CTA phase (profiling only)
+    // split-phase distributed execution; mode 0 = whole sequence in one call
+    int mode;             // 0 full, 1 reduce, 2 smoother finish, 3 Viterbi forward, 4 Viterbi finish
+    int rank, world;
+    int64_t t_base;       // global index of local step 0
+    const float* agg_all; // [world][agg_stride] rank aggregates (modes 2, 3)
+    int agg_stride;       // floats between aggregates
+    float* agg_out;       // this rank's aggregate (mode 1)
+    const uint8_t* rec_all;  // [world][16] Viterbi rank records {u64 map, i32 x*} (mode 4)
+    uint8_t* rec_out;        // this rank's record (mode 3)
+    size_t ws_cmap;          // per-chunk Viterbi maps persisted between modes 3 and 4
 };
+
+enum { HMM_MODE_FULL = 0, HMM_MODE_REDUCE = 1, HMM_MODE_SFINISH = 2, HMM_MODE_VFORWARD = 3, HMM_MODE_VFINISH = 4 };
 
 }  // namespace hmm

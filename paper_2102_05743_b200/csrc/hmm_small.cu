@@ -791,6 +791,9 @@ __global__ void __launch_bounds__(small_nt(D)) hmm_small_kernel(const KParams p)
     const int nchunks = (int)((cta1 - cta0 + p.chunk - 1) / p.chunk);
     const int S = p.S;
     const bool fused = p.fused != 0;
+    const int mode = p.mode;
+    const bool do_pass1 = (mode == HMM_MODE_FULL || mode == HMM_MODE_REDUCE);
+    const int64_t tb = p.t_base;  // global index of local step 0 (split-phase ranks)
 
     // per-sequence sync block (64 B): [0] u64 arrivals of exchange 1, [2] u64 arrivals of exchange 2,
     // [4] u64 impossible-step code, [6] epoch, [7] done counter, [8] bad-input flag
@@ -818,8 +821,6 @@ __global__ void __launch_bounds__(small_nt(D)) hmm_small_kernel(const KParams p)
     unsigned long long* tmr = p.timers ? p.timers + ((size_t)b * G + c) * 16 : nullptr;
 #define HMM_STAMP(i) do { if (tmr && tid == 0) tmr[i] = global_ns(); } while (0)
     HMM_STAMP(0);
-    // call epoch: every CTA of this launch reads the same value; the last CTA bumps it at exit
-    const uint32_t epoch = *reinterpret_cast<volatile uint32_t*>(sync + 6) + 1u;
     uint32_t* done_ctr = sync + 7;
     uint32_t* bad_flag = sync + 8;
     if (tid == 0) {
@@ -860,9 +861,9 @@ __global__ void __launch_bounds__(small_nt(D)) hmm_small_kernel(const KParams p)
         float P[D * D];
         if (ln > 0) {
             if constexpr (MP)
-                mp_leaf<D>(tile + li * D, ln, ch0 + li == 0, A, pv, P, badf);
+                mp_leaf<D>(tile + li * D, ln, tb + ch0 + li == 0, A, pv, P, badf);
             else
-                sp_leaf<D>(tile + li * D, ln, ch0 + li == 0, A, pv, P, acc, write_l, acc_m, badf);
+                sp_leaf<D>(tile + li * D, ln, tb + ch0 + li == 0, A, pv, P, acc, write_l, acc_m, badf);
         } else {
             mat_identity<D, MP>(P);
         }
@@ -873,8 +874,9 @@ __global__ void __launch_bounds__(small_nt(D)) hmm_small_kernel(const KParams p)
         tree_up<D, MP>(tree, NT);
     };
 
-    // ===================== pass 1: leaf aggregates -> chunk roots
-    for (int k = 0; k < nchunks; k++) {
+    // ===================== pass 1: leaf aggregates -> chunk roots (split-phase finish calls reuse the
+    // chunk roots the reduce call left in the workspace)
+    for (int k = 0; do_pass1 && k < nchunks; k++) {
         const int64_t ch0 = cta0 + (int64_t)k * p.chunk;
         const int nch = (int)(((ch0 + p.chunk < cta1) ? ch0 + p.chunk : cta1) - ch0);
         leaf_pass(ch0, nch, fused, true, bad);
@@ -887,7 +889,7 @@ __global__ void __launch_bounds__(small_nt(D)) hmm_small_kernel(const KParams p)
     }
 
     // ===================== CTA root (fused: the chunk tree root; else a tree over chunk roots)
-    if (!fused) {
+    if (!fused && mode != HMM_MODE_VFINISH) {
         const int NN = 2 * p.KP;
         for (int x = tid; x < p.KP; x += NT) {
             float M[D * D];
@@ -908,50 +910,78 @@ __global__ void __launch_bounds__(small_nt(D)) hmm_small_kernel(const KParams p)
 
     // ===================== cross-CTA exchange: publish the root, barrier, stage all roots in SMEM,
     // warp 0 folds the roots to the left (forward carry), warp 1 the roots to the right (backward).
-    if (tid < D * D) reinterpret_cast<float*>(myslot)[tid] = tree[tid * NNroot + 1];
-    HMM_STAMP(2);
-    if (G > 1) {
-        group_arrive_wait(arrive1, (uint32_t)G, epoch);
-        HMM_STAMP(3);
-        // copy all G roots into SMEM: one round of independent loads
-        for (int i = tid; i < G; i += NT) {
-            const float* src = reinterpret_cast<const float*>(slots + (size_t)i * p.slot_bytes);
-            float v[D * D];
+    // Finish calls of the split-phase path find the roots already published by their reduce call.
+    if (mode != HMM_MODE_VFINISH) {
+        if (do_pass1 && tid < D * D) reinterpret_cast<float*>(myslot)[tid] = tree[tid * NNroot + 1];
+        HMM_STAMP(2);
+        if (G > 1 || !do_pass1 || mode == HMM_MODE_REDUCE) {
+            if (do_pass1) group_arrive_wait(arrive1, (uint32_t)G);  // (G == 1: just a CTA barrier)
+            HMM_STAMP(3);
+            // copy all G roots into SMEM: one round of independent loads
+            for (int i = tid; i < G; i += NT) {
+                const float* src = reinterpret_cast<const float*>(slots + (size_t)i * p.slot_bytes);
+                float v[D * D];
 #pragma unroll
-            for (int e = 0; e < D * D; e++) v[e] = __ldcg(src + e);
+                for (int e = 0; e < D * D; e++) v[e] = __ldcg(src + e);
 #pragma unroll
-            for (int e = 0; e < D * D; e++) stage[(size_t)i * sw + e] = v[e];
+                for (int e = 0; e < D * D; e++) stage[(size_t)i * sw + e] = v[e];
+            }
+            __syncthreads();
+        }
+        if (mode == HMM_MODE_REDUCE) {
+            // the rank aggregate = ordered product of all G CTA roots
+            if (c == 0 && warp == 0) {
+                float M[D * D];
+                warp_prod<D, MP>(stage, sw, 0, G, M);
+                if (lane < D * D) p.agg_out[lane] = M[lane];
+            }
+        } else if (warp == 0) {
+            float M[D * D];
+            if (c > 0) warp_prod<D, MP>(stage, sw, 0, c, M);
+            if (lane == 0) {
+                float u[D], v[D];
+#pragma unroll
+                for (int d = 0; d < D; d++) u[d] = v[d] = MP ? 0.0f : 1.0f;
+                // rank carry (split phase): fold the aggregates of the ranks to the left
+                for (int q = 0; q < p.rank; q++) {
+                    float X[D * D];
+#pragma unroll
+                    for (int e = 0; e < D * D; e++) X[e] = __ldg(p.agg_all + (size_t)q * p.agg_stride + e);
+                    vec_mat<D, MP>(u, X, v);
+#pragma unroll
+                    for (int d = 0; d < D; d++) u[d] = v[d];
+                }
+                if (c > 0) vec_mat<D, MP>(u, M, v);
+#pragma unroll
+                for (int d = 0; d < D; d++) cta_pre[d] = v[d];
+            }
+        } else if (warp == 1 && !MP) {
+            float M[D * D];
+            if (c < G - 1) warp_prod<D, MP>(stage, sw, c + 1, G, M);
+            if (lane == 0) {
+                float u[D], v[D];
+#pragma unroll
+                for (int d = 0; d < D; d++) u[d] = v[d] = 1.0f;
+                for (int q = p.world - 1; q > p.rank; q--) {
+                    float X[D * D];
+#pragma unroll
+                    for (int e = 0; e < D * D; e++) X[e] = __ldg(p.agg_all + (size_t)q * p.agg_stride + e);
+                    mat_vec<D>(X, u, v);
+#pragma unroll
+                    for (int d = 0; d < D; d++) u[d] = v[d];
+                }
+                if (c < G - 1) mat_vec<D>(M, u, v);
+#pragma unroll
+                for (int d = 0; d < D; d++) cta_suf[d] = v[d];
+            }
         }
         __syncthreads();
     }
-    if (warp == 0) {
-        float M[D * D];
-        if (c > 0) warp_prod<D, MP>(stage, sw, 0, c, M);
-        if (lane == 0) {
-            float u[D], v[D];
-#pragma unroll
-            for (int d = 0; d < D; d++) u[d] = v[d] = MP ? 0.0f : 1.0f;
-            if (c > 0) vec_mat<D, MP>(u, M, v);
-#pragma unroll
-            for (int d = 0; d < D; d++) cta_pre[d] = v[d];
-        }
-    } else if (warp == 1 && !MP) {
-        float M[D * D];
-        if (c < G - 1) warp_prod<D, MP>(stage, sw, c + 1, G, M);
-        if (lane == 0) {
-            float u[D], v[D];
-#pragma unroll
-            for (int d = 0; d < D; d++) u[d] = v[d] = 1.0f;
-            if (c < G - 1) mat_vec<D>(M, u, v);
-#pragma unroll
-            for (int d = 0; d < D; d++) cta_suf[d] = v[d];
-        }
-    }
-    __syncthreads();
-
     HMM_STAMP(4);
+    const bool do_sweep = (mode == HMM_MODE_FULL || mode == HMM_MODE_SFINISH || mode == HMM_MODE_VFORWARD);
     // carries per chunk (non-fused) or per leaf (fused)
-    if (!fused) {
+    if (!do_sweep) {
+    } else if (!fused) {
         tree_down<D, MP, !MP>(tree, p.KP, cta_pre, cta_suf);
         const int NN = 2 * p.KP;
         for (int x = tid; x < nchunks; x += NT) {
@@ -977,15 +1007,16 @@ __global__ void __launch_bounds__(small_nt(D)) hmm_small_kernel(const KParams p)
     if constexpr (OP == 0) {
         // ===================== smoother pass 2 (chunks in reverse order: the tail is still in L2)
         float* filt = reinterpret_cast<float*>(smem + p.L.regB);
-        for (int k = nchunks - 1; k >= 0; k--) {
+        for (int k = nchunks - 1; do_sweep && k >= 0; k--) {
             const int64_t ch0 = cta0 + (int64_t)k * p.chunk;
             const int nch = (int)(((ch0 + p.chunk < cta1) ? ch0 + p.chunk : cta1) - ch0);
             const int li = tid * S;
             const int ln = (li < nch) ? ((nch - li < S) ? nch - li : S) : 0;
-            const bool t0 = (ch0 + li == 0);
+            const bool t0 = (tb + ch0 + li == 0);
             if (!fused) {
                 bool dbad = false;
-                leaf_pass(ch0, nch, true, false, dbad);
+                // (a split-phase finish skipped pass 1, so it accumulates sum m_t here)
+                leaf_pass(ch0, nch, true, mode == HMM_MODE_SFINISH, dbad);
                 tree_down<D, false, true>(tree, NT, carr + k * 2 * D, carr + k * 2 * D + D);
             }
             float alpha[D], beta[D];
@@ -1005,7 +1036,7 @@ __global__ void __launch_bounds__(small_nt(D)) hmm_small_kernel(const KParams p)
             if (tmr && tid == 0) tmr[14] = clock64();
             if (ln > 0) {
                 const int zi = sp_alpha<D>(tile + li * D, filt + li * D, ln, t0, A, pv, alpha, acc, false);
-                if (zi >= 0 && ch0 + li + zi < zero_t) zero_t = ch0 + li + zi;
+                if (zi >= 0 && tb + ch0 + li + zi < zero_t) zero_t = tb + ch0 + li + zi;
             }
             int r0, nr;
             warp_rows(nch, r0, nr);
@@ -1030,12 +1061,13 @@ __global__ void __launch_bounds__(small_nt(D)) hmm_small_kernel(const KParams p)
         int32_t* cends = reinterpret_cast<int32_t*>(smem + p.L.cends);
         constexpr int BPB = small_bpb(D);
         const size_t cta_chunk_base = (size_t)(b * G + c) * p.K;
-        for (int k = 0; k < nchunks; k++) {
+        uint64_t* cmap_ws = reinterpret_cast<uint64_t*>(p.ws + p.ws_cmap) + cta_chunk_base;
+        for (int k = 0; do_sweep && k < nchunks; k++) {
             const int64_t ch0 = cta0 + (int64_t)k * p.chunk;
             const int nch = (int)(((ch0 + p.chunk < cta1) ? ch0 + p.chunk : cta1) - ch0);
             const int li = tid * S;
             const int ln = (li < nch) ? ((nch - li < S) ? nch - li : S) : 0;
-            const bool t0 = (ch0 + li == 0);
+            const bool t0 = (tb + ch0 + li == 0);
             if (!fused) {
                 bool dbad = false;
                 leaf_pass(ch0, nch, false, false, dbad);
@@ -1048,7 +1080,7 @@ __global__ void __launch_bounds__(small_nt(D)) hmm_small_kernel(const KParams p)
             if (ln > 0) {
                 int zi;
                 f = vit_sweep<D>(tile + li * D, bp + (size_t)li * BPB, ln, t0, A, pv, V, acc, zi);
-                if (zi >= 0 && ch0 + li + zi < zero_t) zero_t = ch0 + li + zi;
+                if (zi >= 0 && tb + ch0 + li + zi < zero_t) zero_t = tb + ch0 + li + zi;
                 if (ch0 + li + ln == T) {  // this leaf ends the sequence: x*_{T-1} = argmax V (smallest)
                     int xs = 0;
                     for (int d = D - 1; d >= 0; d--)
@@ -1070,44 +1102,78 @@ __global__ void __launch_bounds__(small_nt(D)) hmm_small_kernel(const KParams p)
             }
             __syncthreads();
             map_tree_up<D>(maps, NT);
-            if (!fused && tid == 0) cmaps[k] = maps[1];
+            if (!fused && tid == 0) {
+                cmaps[k] = maps[1];
+                cmap_ws[k] = maps[1];  // persisted for a split-phase finish call
+            }
+        }
+        if (mode == HMM_MODE_VFINISH) {  // chunk maps from the forward call
+            for (int x = tid; x < nchunks; x += NT) cmaps[x] = cmap_ws[x];
         }
         // CTA map
-        uint64_t F;
-        if (fused) {
-            F = maps[1];
-        } else {
-            __syncthreads();
-            for (int x = tid; x < p.KP; x += NT) maps[p.KP + x] = (x < nchunks) ? cmaps[x] : map_identity(D);
-            __syncthreads();
-            map_tree_up<D>(maps, p.KP);
-            F = maps[1];
+        uint64_t F = 0;
+        if (mode == HMM_MODE_FULL || mode == HMM_MODE_VFORWARD || mode == HMM_MODE_VFINISH) {
+            if (fused) {
+                F = maps[1];
+            } else {
+                __syncthreads();
+                for (int x = tid; x < p.KP; x += NT) maps[p.KP + x] = (x < nchunks) ? cmaps[x] : map_identity(D);
+                __syncthreads();
+                map_tree_up<D>(maps, p.KP);
+                F = maps[1];
+            }
         }
-        // end state of this CTA = (F_{c+1} o ... o F_{G-1})(x*)
+        // end state of this CTA = (F_{c+1} o ... o F_{G-1})(x_end), x_end = x*_{T-1} (whole sequence) or the
+        // end state of this rank (split phase: resolved from the gathered rank records)
         uint64_t* smaps = reinterpret_cast<uint64_t*>(stage);
         int xs = flag[0];
-        if (G > 1) {
+        if (mode == HMM_MODE_FULL || mode == HMM_MODE_VFORWARD) {
             if (tid == 0) {
                 *reinterpret_cast<uint64_t*>(myslot + map_off) = F;
                 if (c == G - 1) *reinterpret_cast<int32_t*>(myslot + map_off + 16) = flag[0];
             }
-            group_arrive_wait(arrive2, (uint32_t)G, epoch);
-            for (int i = c + 1 + tid; i < G; i += NT) {
+            if (G > 1) group_arrive_wait(arrive2, (uint32_t)G);
+            else __syncthreads();
+        }
+        if (mode == HMM_MODE_VFORWARD) {
+            // rank record: {map of the whole rank slice, x* of its last step}
+            for (int i = tid; i < G; i += NT)
                 smaps[i] = __ldcg(reinterpret_cast<const unsigned long long*>(slots + (size_t)i * p.slot_bytes + map_off));
-                if (i == G - 1) flag[3] = __ldcg(reinterpret_cast<const int*>(slots + (size_t)i * p.slot_bytes + map_off + 16));
+            __syncthreads();
+            if (c == 0 && warp == 0) {
+                const uint64_t Fr = warp_compose<D>(smaps, 0, G);
+                if (lane == 0) *reinterpret_cast<uint64_t*>(p.rec_out) = Fr;
+            }
+            if (c == G - 1 && tid == 0) *reinterpret_cast<int32_t*>(p.rec_out + 8) = flag[0];
+        }
+        if (mode == HMM_MODE_FULL || mode == HMM_MODE_VFINISH) {
+            if (G > 1 || mode == HMM_MODE_VFINISH) {
+                for (int i = c + 1 + tid; i < G; i += NT) {
+                    smaps[i] = __ldcg(reinterpret_cast<const unsigned long long*>(slots + (size_t)i * p.slot_bytes + map_off));
+                    if (i == G - 1) flag[3] = __ldcg(reinterpret_cast<const int*>(slots + (size_t)i * p.slot_bytes + map_off + 16));
+                }
+                if (mode == HMM_MODE_VFINISH && tid == 0) {
+                    // x* of the whole sequence (last rank), mapped back through the ranks to our right
+                    int x = *reinterpret_cast<const int32_t*>(p.rec_all + (size_t)(p.world - 1) * 16 + 8);
+                    for (int q = p.world - 1; q > p.rank; q--)
+                        x = map_apply(*reinterpret_cast<const unsigned long long*>(p.rec_all + (size_t)q * 16), x < 0 ? 0 : x);
+                    flag[0] = x;
+                }
+                __syncthreads();
+                xs = (mode == HMM_MODE_VFINISH) ? flag[0] : ((c < G - 1) ? flag[3] : flag[0]);
+            }
+            if (warp == 0) {
+                uint64_t Fs = map_identity(D);
+                if (c < G - 1) Fs = warp_compose<D>(smaps, c + 1, G);
+                if (lane == 0) flag[1] = map_apply(Fs, xs < 0 ? 0 : xs);
             }
             __syncthreads();
-            if (c < G - 1) xs = flag[3];
         }
-        if (warp == 0) {
-            uint64_t Fs = map_identity(D);
-            if (c < G - 1) Fs = warp_compose<D>(smaps, c + 1, G);
-            if (lane == 0) flag[1] = map_apply(Fs, xs < 0 ? 0 : xs);
-        }
-        __syncthreads();
+        const bool do_path = (mode == HMM_MODE_FULL || mode == HMM_MODE_VFINISH);
         const int cta_end = flag[1];
         HMM_STAMP(6);
-        if (fused) {
+        if (!do_path) {
+        } else if (fused) {
             map_tree_down(maps, ends, NT, cta_end);
         } else {
             // chunk maps are still the leaves of the map tree (KP level)
@@ -1116,7 +1182,7 @@ __global__ void __launch_bounds__(small_nt(D)) hmm_small_kernel(const KParams p)
             __syncthreads();
         }
         // ===================== pass 3: backtrack and write the path
-        for (int k = nchunks - 1; k >= 0; k--) {
+        for (int k = nchunks - 1; do_path && k >= 0; k--) {
             const int64_t ch0 = cta0 + (int64_t)k * p.chunk;
             const int nch = (int)(((ch0 + p.chunk < cta1) ? ch0 + p.chunk : cta1) - ch0);
             const int li = tid * S;
@@ -1162,15 +1228,17 @@ __global__ void __launch_bounds__(small_nt(D)) hmm_small_kernel(const KParams p)
         for (int x = tid; x < G; x += NT) v += __ldcg(reinterpret_cast<const double*>(slots + (size_t)x * p.slot_bytes + map_off + 8));
         const double tot = block_sum<NT>(v, red);
         if (tid == 0) {
-            p.scalar_out[b] = tot;
+            if (p.scalar_out) p.scalar_out[b] = tot;
             const uint32_t badf = atomicExch(bad_flag, 0u);
             const unsigned long long zc = atomicExch(zero_code, 0ull);
             int32_t inf = 0;
             if (badf) inf = -1;
             else if (zc) inf = (int32_t)((1ull << 62) - zc + 1ull);
-            p.info[b] = inf;
+            if (p.info) p.info[b] = inf;
+            // every CTA has passed every wait of this launch: reset the arrival counters
+            atomicExch(arrive1, 0ull);
+            atomicExch(arrive2, 0ull);
             atomicExch(done_ctr, 0u);
-            atomicAdd(sync + 6, 1u);  // next call's epoch
         }
     }
     HMM_STAMP(10);

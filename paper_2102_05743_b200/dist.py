@@ -1,0 +1,189 @@
+"""Split-phase multi-GPU path: one HMM sequence partitioned along T across the ranks of a process group.
+
+Rank r owns the contiguous global steps [t_base, t_base + T_local) (``partition``).  The exchange is
+the only collective of the method: every rank reduces its slice to one D x D
+aggregate (the ordered product of its elements, Def. 3 / Def. 5 of the paper), the W aggregates are
+all-gathered (NCCL over NVLink on B200s; ~W*80 bytes at D=4), and every rank runs a local finish
+pass with carries folded from the gathered aggregates in rank order.  log Z / log_prob are the
+fixed-order sums of per-rank partials (a second tiny all-gather), so every rank holds bitwise-identical
+scalars.  Viterbi adds one more tiny all-gather of the rank backpointer maps (D bytes + x*).
+
+The compute is done by ``LibBackend`` (the C ABI of libhmmscan.so).  The orchestration takes the
+backend as a parameter so its host logic can be exercised on CPU with gloo (tests/test_dist_gloo.py).
+"""
+from __future__ import annotations
+
+import ctypes
+
+import torch
+import torch.distributed as dist
+
+from . import HmmError, _check, _ptr, _stream, lib
+
+RECORD_BYTES = 16
+
+
+def partition(T: int, world: int, rank: int, align: int = 8) -> tuple[int, int]:
+    """Contiguous slices with boundaries on multiples of `align` (16-B aligned slices for the bulk
+    copies); if that would leave a rank empty, an unaligned equal split.  Returns (t_base, T_local)."""
+    if T < world:
+        raise HmmError("need T >= world")
+    per = -(-T // world)
+    per = -(-per // align) * align
+    if per * (world - 1) >= T:  # some rank would be empty: equal split for everyone
+        return rank * T // world, (rank + 1) * T // world - rank * T // world
+    t0 = rank * per
+    return t0, min(per, T - t0)
+
+
+class LibBackend:
+    """Device compute of the phases through the C ABI (hmmscan.h split-phase entry points)."""
+
+    def __init__(self):
+        L = lib()
+        i32, i64, p, sz = ctypes.c_int, ctypes.c_int64, ctypes.c_void_p, ctypes.c_size_t
+        L.hmm_dist_agg_bytes.restype = sz
+        L.hmm_dist_agg_bytes.argtypes = [i32]
+        L.hmm_dist_workspace_size.restype = sz
+        L.hmm_dist_workspace_size.argtypes = [i32, i32, i64]
+        L.hmm_smooth_dist_reduce.argtypes = [i32, i64, i64, p, p, p, p, p, p, sz, p]
+        L.hmm_smooth_dist_finish.argtypes = [i32, i64, i64, p, p, p, p, i32, i32, p, p, p, p, p, sz, p]
+        L.hmm_viterbi_dist_reduce.argtypes = [i32, i64, i64, p, p, p, p, p, p, sz, p]
+        L.hmm_viterbi_dist_forward.argtypes = [i32, i64, i64, p, p, p, p, i32, i32, p, p, p, p, sz, p]
+        L.hmm_viterbi_dist_finish.argtypes = [i32, i64, i64, p, p, p, p, i32, i32, p, p, p, sz, p]
+        for f in ("hmm_smooth_dist_reduce", "hmm_smooth_dist_finish", "hmm_viterbi_dist_reduce",
+                  "hmm_viterbi_dist_forward", "hmm_viterbi_dist_finish"):
+            getattr(L, f).restype = i32
+        self.L = L
+        self._ws = {}
+
+    def agg_bytes(self, D):
+        return int(self.L.hmm_dist_agg_bytes(D))
+
+    def ws(self, op, D, T_local, device):
+        key = (op, D, T_local, device)
+        if key not in self._ws:
+            n = int(self.L.hmm_dist_workspace_size(op, D, T_local))
+            if n == 0:
+                raise HmmError(f"split phase unsupported for D={D}")
+            self._ws[key] = torch.zeros(n, dtype=torch.uint8, device=device)
+        return self._ws[key]
+
+    def smooth_reduce(self, lp, la, ll, t_base):
+        T, D = ll.shape
+        ws = self.ws(0, D, T, ll.device)
+        agg = torch.empty(self.agg_bytes(D), dtype=torch.uint8, device=ll.device)
+        info = torch.empty(1, dtype=torch.int32, device=ll.device)
+        _check(self.L.hmm_smooth_dist_reduce(D, T, t_base, _ptr(lp), _ptr(la), _ptr(ll), _ptr(agg), _ptr(info),
+                                             _ptr(ws), ws.numel(), _stream(None)), "hmm_smooth_dist_reduce")
+        return agg, info
+
+    def smooth_finish(self, lp, la, ll, t_base, agg_all, rank, world):
+        T, D = ll.shape
+        ws = self.ws(0, D, T, ll.device)
+        filt, sm = torch.empty_like(ll), torch.empty_like(ll)
+        lzp = torch.empty(1, dtype=torch.float64, device=ll.device)
+        info = torch.empty(1, dtype=torch.int32, device=ll.device)
+        _check(self.L.hmm_smooth_dist_finish(D, T, t_base, _ptr(lp), _ptr(la), _ptr(ll), _ptr(agg_all), rank, world,
+                                             _ptr(filt), _ptr(sm), _ptr(lzp), _ptr(info), _ptr(ws), ws.numel(),
+                                             _stream(None)), "hmm_smooth_dist_finish")
+        return filt, sm, lzp, info
+
+    def viterbi_reduce(self, lp, la, ll, t_base):
+        T, D = ll.shape
+        ws = self.ws(1, D, T, ll.device)
+        agg = torch.empty(self.agg_bytes(D), dtype=torch.uint8, device=ll.device)
+        info = torch.empty(1, dtype=torch.int32, device=ll.device)
+        _check(self.L.hmm_viterbi_dist_reduce(D, T, t_base, _ptr(lp), _ptr(la), _ptr(ll), _ptr(agg), _ptr(info),
+                                              _ptr(ws), ws.numel(), _stream(None)), "hmm_viterbi_dist_reduce")
+        return agg, info
+
+    def viterbi_forward(self, lp, la, ll, t_base, agg_all, rank, world):
+        T, D = ll.shape
+        ws = self.ws(1, D, T, ll.device)
+        rec = torch.zeros(RECORD_BYTES, dtype=torch.uint8, device=ll.device)
+        lpp = torch.empty(1, dtype=torch.float64, device=ll.device)
+        info = torch.empty(1, dtype=torch.int32, device=ll.device)
+        _check(self.L.hmm_viterbi_dist_forward(D, T, t_base, _ptr(lp), _ptr(la), _ptr(ll), _ptr(agg_all), rank, world,
+                                               _ptr(rec), _ptr(lpp), _ptr(info), _ptr(ws), ws.numel(),
+                                               _stream(None)), "hmm_viterbi_dist_forward")
+        return rec, lpp, info
+
+    def viterbi_finish(self, lp, la, ll, t_base, rec_all, rank, world):
+        T, D = ll.shape
+        ws = self.ws(1, D, T, ll.device)
+        path = torch.empty(T, dtype=torch.int32, device=ll.device)
+        info = torch.empty(1, dtype=torch.int32, device=ll.device)
+        _check(self.L.hmm_viterbi_dist_finish(D, T, t_base, _ptr(lp), _ptr(la), _ptr(ll), _ptr(rec_all), rank, world,
+                                              _ptr(path), _ptr(info), _ptr(ws), ws.numel(), _stream(None)),
+               "hmm_viterbi_dist_finish")
+        return path, info
+
+
+_default = None
+
+
+def _backend(backend):
+    global _default
+    if backend is not None:
+        return backend
+    if _default is None:
+        _default = LibBackend()
+    return _default
+
+
+def _all_gather(x: torch.Tensor, group=None) -> torch.Tensor:
+    """Rank-ordered concatenation of a small per-rank tensor (NCCL: all_gather_into_tensor)."""
+    world = dist.get_world_size(group)
+    if x.is_cuda:
+        out = torch.empty(world * x.numel(), dtype=x.dtype, device=x.device)
+        dist.all_gather_into_tensor(out, x.contiguous().view(-1), group=group)
+        return out
+    parts = [torch.empty_like(x) for _ in range(world)]
+    dist.all_gather(parts, x.contiguous(), group=group)
+    return torch.cat([q.view(-1) for q in parts])
+
+
+def _combine_info(infos: torch.Tensor) -> torch.Tensor:
+    """Global info from per-rank codes: -1 if any rank saw a bad input, else the smallest positive."""
+    bad = (infos == -1).any()
+    pos = torch.where(infos > 0, infos, torch.full_like(infos, torch.iinfo(torch.int32).max))
+    m = pos.min()
+    first = torch.where(m == torch.iinfo(torch.int32).max, torch.zeros_like(m), m)
+    return torch.where(bad, torch.full_like(first, -1), first).view(1)
+
+
+def smooth_dist(log_pi, log_A, log_lik_local, t_base: int, group=None, backend=None):
+    """Parallel smoother over a T-partitioned sequence.  Returns (filtered, smoothed, log_z [1], info [1])
+    for the local slice; log_z and info are global and identical on every rank."""
+    be = _backend(backend)
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    agg, info1 = be.smooth_reduce(log_pi, log_A, log_lik_local, t_base)
+    agg_all = _all_gather(agg, group)                       # the method's one exchange step
+    filt, sm, lzp, info2 = be.smooth_finish(log_pi, log_A, log_lik_local, t_base, agg_all, rank, world)
+    parts = _all_gather(torch.cat([lzp, torch.stack([info1.double().view(()), info2.double().view(())])]), group)
+    parts = parts.view(world, 3)
+    log_z = torch.zeros(1, dtype=torch.float64, device=parts.device)
+    for r in range(world):  # fixed rank order
+        log_z += parts[r, 0]
+    info = _combine_info(parts[:, 1:].reshape(-1).to(torch.int32))
+    return filt, sm, log_z, info
+
+
+def viterbi_dist(log_pi, log_A, log_lik_local, t_base: int, group=None, backend=None):
+    """Parallel MAP path over a T-partitioned sequence.  Returns (path of the local slice, log_prob [1],
+    info [1]); log_prob and info are global."""
+    be = _backend(backend)
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    agg, info1 = be.viterbi_reduce(log_pi, log_A, log_lik_local, t_base)
+    agg_all = _all_gather(agg, group)
+    rec, lpp, info2 = be.viterbi_forward(log_pi, log_A, log_lik_local, t_base, agg_all, rank, world)
+    rec_all = _all_gather(rec, group)                      # rank backpointer maps + x*
+    path, info3 = be.viterbi_finish(log_pi, log_A, log_lik_local, t_base, rec_all, rank, world)
+    parts = _all_gather(torch.cat([lpp, torch.stack([info1.double().view(()), info2.double().view(()),
+                                                     info3.double().view(())])]), group).view(world, 4)
+    log_prob = torch.zeros(1, dtype=torch.float64, device=parts.device)
+    for r in range(world):
+        log_prob += parts[r, 0]
+    info = _combine_info(parts[:, 1:].reshape(-1).to(torch.int32))
+    return path, log_prob, info

@@ -1,0 +1,104 @@
+"""Split-phase (multi-GPU) kernels emulated on one GPU: W ranks' reduce / finish phases run in
+sequence through the C ABI with per-rank workspaces, the all-gathers are host-side concatenations in
+rank order (what NCCL's all_gather_into_tensor produces).  Results must match the fp64 oracle on the
+unpartitioned sequence and the single-call path (rank-count invariance)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import workloads as W
+from parity import TAU, TOL_MARG, TOL_REL, rel
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(autouse=True, scope="module")
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+
+
+def _slices(T, world):
+    from paper_2102_05743_b200.dist import partition
+    return [partition(T, world, r) for r in range(world)]
+
+
+def emulate_smooth(wl, world):
+    from paper_2102_05743_b200.dist import LibBackend
+    dev = torch.device("cuda")
+    lp, la = torch.from_numpy(wl.log_pi).to(dev), torch.from_numpy(wl.log_A).to(dev)
+    ll = torch.from_numpy(wl.log_lik).to(dev)
+    bes = [LibBackend() for _ in range(world)]
+    sl = _slices(wl.T, world)
+    aggs, infos = [], []
+    for r, (t0, n) in enumerate(sl):
+        a, i = bes[r].smooth_reduce(lp, la, ll[t0:t0 + n], t0)
+        aggs.append(a); infos.append(i)
+    agg_all = torch.cat(aggs)
+    outs = [bes[r].smooth_finish(lp, la, ll[t0:t0 + n], t0, agg_all, r, world) for r, (t0, n) in enumerate(sl)]
+    torch.cuda.synchronize()
+    filt = torch.cat([o[0] for o in outs]).cpu().numpy()
+    sm = torch.cat([o[1] for o in outs]).cpu().numpy()
+    lz = sum(float(o[2].item()) for o in outs)
+    info = [int(i.item()) for i in infos] + [int(o[3].item()) for o in outs]
+    return filt, sm, lz, info
+
+
+def emulate_viterbi(wl, world):
+    from paper_2102_05743_b200.dist import LibBackend
+    dev = torch.device("cuda")
+    lp, la = torch.from_numpy(wl.log_pi).to(dev), torch.from_numpy(wl.log_A).to(dev)
+    ll = torch.from_numpy(wl.log_lik).to(dev)
+    bes = [LibBackend() for _ in range(world)]
+    sl = _slices(wl.T, world)
+    agg_all = torch.cat([bes[r].viterbi_reduce(lp, la, ll[t0:t0 + n], t0)[0] for r, (t0, n) in enumerate(sl)])
+    fw = [bes[r].viterbi_forward(lp, la, ll[t0:t0 + n], t0, agg_all, r, world) for r, (t0, n) in enumerate(sl)]
+    rec_all = torch.cat([f[0] for f in fw])
+    fin = [bes[r].viterbi_finish(lp, la, ll[t0:t0 + n], t0, rec_all, r, world) for r, (t0, n) in enumerate(sl)]
+    torch.cuda.synchronize()
+    path = torch.cat([f[0] for f in fin]).cpu().numpy()
+    lpr = sum(float(f[1].item()) for f in fw)
+    info = [int(f[2].item()) for f in fw] + [int(f[1].item()) for f in fin]
+    return path, lpr, info
+
+
+@pytest.mark.parametrize("world,T", [(1, 100_000), (2, 1_000_000), (4, 1_000_003), (8, 2_000_000), (3, 5000),
+                                     (8, 64), (8, 8)])
+def test_dist_smoother_rank_invariance(world, T):
+    wl = W.ge(T, seed=5)
+    filt, sm, lz, info = emulate_smooth(wl, world)
+    assert all(i == 0 for i in info)
+    o = oracle.smooth(wl.log_pi, wl.log_A, wl.log_lik)
+    assert float(np.abs(sm - o["smoothed"]).max()) <= TOL_MARG
+    assert float(np.abs(filt - o["filtered"]).max()) <= TOL_MARG
+    assert rel(lz, o["log_z"]) <= TOL_REL
+
+
+@pytest.mark.parametrize("world,T", [(1, 50_000), (2, 1_000_000), (4, 999_999), (8, 2_000_000), (3, 5000), (8, 64)])
+def test_dist_viterbi_rank_invariance(world, T):
+    wl = W.ge(T, seed=6, jitter=0.1)
+    path, lpr, info = emulate_viterbi(wl, world)
+    assert all(i == 0 for i in info)
+    v = oracle.viterbi(wl.log_pi, wl.log_A, wl.log_lik)
+    assert rel(lpr, v["log_prob"]) <= TOL_REL
+    _, gap = oracle.max_marginals(wl.log_pi, wl.log_A, wl.log_lik)
+    safe = gap >= TAU
+    assert int(((path != v["path"]) & safe).sum()) == 0
+    jw = oracle.joint_weight(wl.log_pi, wl.log_A, wl.log_lik, path)
+    assert rel(jw, v["log_prob"]) <= TOL_REL
+
+
+def test_dist_planted_path_exact():
+    wl = W.planted(5, 300_000, seed=4)
+    path, lpr, info = emulate_viterbi(wl, 4)
+    assert np.array_equal(path, wl.states)
+
+
+def test_dist_info_global_step():
+    wl = W.ge(400_000, seed=9)
+    wl.log_lik[250_123, :] = -np.inf
+    _, _, _, info = emulate_smooth(wl, 4)
+    assert min(i for i in info if i > 0) == 250_124
+    _, _, vinfo = emulate_viterbi(wl, 4)
+    assert min(i for i in vinfo if i > 0) == 250_124
