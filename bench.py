@@ -169,6 +169,103 @@ def run_reference(args):
     }), flush=True)
 
 
+def run_multi(args, world, rank, local):
+    """N > 1: one GE sequence of world*T steps partitioned along T (rank r owns T steps); every step
+    runs the split-phase smoother and Viterbi with their NCCL all-gathers (the method's exchange step).
+    Weak scaling: per-GPU work fixed, value = world*T / max-over-ranks step time."""
+    import torch
+    import torch.distributed as dist
+    import workloads as W
+    from paper_2102_05743_b200 import dist as HD
+
+    ndev = torch.cuda.device_count()
+    dev = torch.device("cuda", local % max(ndev, 1))
+    torch.cuda.set_device(dev)
+    if args.dist_backend == "nccl":
+        dist.init_process_group("nccl", device_id=dev)
+    else:
+        dist.init_process_group("gloo")
+    Tg = world * args.T
+    wl = W.ge(Tg, seed=5)  # counter-based RNG: every rank simulates the same global chain
+    t0, n = HD.partition(Tg, world, rank)
+    D = wl.D
+    lp = torch.from_numpy(wl.log_pi).to(dev)
+    la = torch.from_numpy(wl.log_A).to(dev)
+    ll = torch.from_numpy(np.ascontiguousarray(wl.log_lik[t0:t0 + n])).to(dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        f, s, lz, info = HD.smooth_dist(lp, la, ll, t0)
+        path, lpr, vinfo = HD.viterbi_dist(lp, la, ll, t0)
+        return lz, info, lpr, vinfo
+
+    for _ in range(args.warmup):
+        out = step()
+    torch.cuda.synchronize()
+    assert int(out[1].item()) == 0 and int(out[3].item()) == 0
+    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev.index) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    dist.barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if args.dist_backend == "nccl":
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    else:
+        tc = t.cpu(); dist.all_reduce(tc, op=dist.ReduceOp.MAX); t = tc
+    ms = float(t.item())
+    # e2e: H2D of the local slice from pinned memory + the step + D2H of the scalars
+    h_ll = torch.from_numpy(np.ascontiguousarray(wl.log_lik[t0:t0 + n])).pin_memory()
+    h_out = torch.empty(2, dtype=torch.float64).pin_memory()
+
+    def e2e_step():
+        ll.copy_(h_ll, non_blocking=True)
+        lz, info, lpr, vinfo = step()
+        h_out.copy_(torch.cat([lz, lpr]), non_blocking=True)
+
+    for _ in range(args.warmup):
+        e2e_step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0.record(stream)
+    for _ in range(args.steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    te = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device=dev)
+    if args.dist_backend == "nccl":
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    else:
+        tc = te.cpu(); dist.all_reduce(tc, op=dist.ReduceOp.MAX); te = tc
+    ms_e2e = float(te.item())
+    peaks = load_peaks()
+    ach = SMOOTH_BYTES_PER_STEP(D) * n / (ms * 1e-3) / 1e9  # per GPU, whole step (smoother + Viterbi)
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": Tg / (ms * 1e-3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"GE D=4, one sequence of {world}x{args.T:g} steps T-partitioned across ranks "
+                                   f"(split-phase smoother+viterbi, NCCL all-gather of rank aggregates)",
+                       "D": D, "T_global": Tg, "T_per_rank": n, "B": 1, "collective": args.dist_backend,
+                       "l2": "inputs resident; per-rank slice 16 MB"},
+            "roofline": {"kernel": "whole split-phase step per GPU (smoother+viterbi)", "bound": "hbm",
+                         "achieved": ach, "peak": peaks["hbm"], "unit": "GB/s", "frac": ach / peaks["hbm"],
+                         "traffic": None},
+            "cpu_baseline": None,
+            "e2e": {"value": Tg / (ms_e2e * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h_ll.numel() * 4),
+                    "d2h_bytes_per_step": 16, "ms_per_step": ms_e2e},
+            "gpu_launches": 5 * args.steps, "clocks": clk.summary(),
+        }), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -182,6 +279,8 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=100_000)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo only for single-GPU multi-process smoke runs")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -196,10 +295,11 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        run_multi(args, world, rank, local)
+        return
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
 
     wl, desc = make_workload(args, rank)
     D, T = wl.D, wl.T
@@ -221,7 +321,7 @@ def main():
         # write a buffer 4x the L2 (the contract), then read another 2x-L2 buffer so the dirty lines are
         # written back here rather than inside the next timed kernel: L2 is cold AND clean.
         flush_w.zero_()
-        torch.sum(flush_r, out=flush_acc)
+        flush_acc.copy_(flush_r.sum())
 
     def step():
         H.smooth(lp, la, ll, out=out_s, ws=ws_s)

@@ -135,13 +135,14 @@ def _backend(backend):
 def _all_gather(x: torch.Tensor, group=None) -> torch.Tensor:
     """Rank-ordered concatenation of a small per-rank tensor (NCCL: all_gather_into_tensor)."""
     world = dist.get_world_size(group)
-    if x.is_cuda:
+    if x.is_cuda and dist.get_backend(group) == "nccl":
         out = torch.empty(world * x.numel(), dtype=x.dtype, device=x.device)
         dist.all_gather_into_tensor(out, x.contiguous().view(-1), group=group)
         return out
-    parts = [torch.empty_like(x) for _ in range(world)]
-    dist.all_gather(parts, x.contiguous(), group=group)
-    return torch.cat([q.view(-1) for q in parts])
+    xc = x.detach().cpu().contiguous()  # gloo (CPU tests / single-GPU multi-process smoke runs)
+    parts = [torch.empty_like(xc) for _ in range(world)]
+    dist.all_gather(parts, xc, group=group)
+    return torch.cat([q.view(-1) for q in parts]).to(x.device)
 
 
 def _combine_info(infos: torch.Tensor) -> torch.Tensor:
