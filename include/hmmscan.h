@@ -160,11 +160,17 @@ hmm_status_t hmm_viterbi_dist_finish(int D, int64_t T_local, int64_t t_base, con
  *   hmm_debug_set_timers: for calls made later from the calling host thread, CTA phase timestamps
  *     (%globaltimer, ns) are written to device_buf[(b*G + c)*16 + i] (NULL disables).
  *   hmm_debug_plan: the launch plan for (op, D, T, B): out[0..7] = G (CTAs per sequence), R (steps per
- *     CTA), S (steps per leaf), chunk, K (chunks per CTA), fused, dynamic smem bytes, threads per CTA.
- *     Returns 0 if unsupported.
+ *     CTA; lane-streaming plan: steps per lane), S (steps per leaf / slice), chunk, K (chunks per CTA /
+ *     slices per lane), kind (1 fused, 0 chunked, 2 lane-streaming), dynamic smem bytes, threads per
+ *     CTA.  Returns 0 if unsupported.
+ *   hmm_debug_force_path: for calls made later from the calling host thread with 1 <= D <= 8 and
+ *     B == 1, select the decomposition: 0 automatic (default), 1 lane-streaming (16-B aligned
+ *     buffers required, else automatic), 2 resident/chunked.  Test and profiling use only; the
+ *     results agree within the stated tolerances whichever path runs.
  */
 void hmm_debug_set_timers(unsigned long long* device_buf);
 int hmm_debug_plan(int op, int D, int64_t T, int64_t B, int64_t* out);
+void hmm_debug_force_path(int path);
 
 #ifdef __cplusplus
 }

@@ -54,6 +54,8 @@ def lib() -> ctypes.CDLL:
         L.hmm_debug_set_timers.argtypes = [p]
         L.hmm_debug_set_timers.restype = None
         L.hmm_debug_plan.argtypes = [i32, i32, i64, i64, p]
+        L.hmm_debug_force_path.argtypes = [i32]
+        L.hmm_debug_force_path.restype = None
         L.hmm_debug_plan.restype = i32
         for f in ("hmm_smooth", "hmm_viterbi", "hmm_smooth_batched", "hmm_viterbi_batched"):
             getattr(L, f).restype = i32
@@ -76,6 +78,11 @@ def plan(op: int, D: int, T: int, B: int = 1) -> dict:
         raise HmmError("unsupported shape")
     keys = ["G", "R", "S", "chunk", "K", "fused", "smem", "NT"]
     return dict(zip(keys, list(out)))
+
+
+def force_path(path: int):
+    """Testing/profiling: 0 automatic, 1 lane-streaming, 2 resident/chunked (calling thread only)."""
+    lib().hmm_debug_force_path(int(path))
 
 
 def set_timers(buf):

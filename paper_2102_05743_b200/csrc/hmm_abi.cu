@@ -15,6 +15,7 @@ namespace hmm {
 cudaError_t launch_small(int D, int op, unsigned G, unsigned B, size_t smem, bool coop, const KParams& kp,
                          cudaStream_t s);
 cudaError_t launch_large(int DP, int op, const LgParams& p, cudaStream_t s);
+cudaError_t launch_stream(int D, int op, unsigned G, const SParams& sp, cudaStream_t s);
 int large_leaves_per_block(int DP);
 }
 
@@ -130,6 +131,61 @@ bool make_plan(int D, int op, int64_t T, int64_t B, Plan& P, bool chunked = fals
     return true;
 }
 
+// Lane-streaming plan (hmm_stream.cu): G CTAs of NT lanes, n steps per lane (a multiple of the slice
+// length S), K = n / S slices per lane.
+struct StPlan {
+    int G = 1;
+    int64_t n = 0;
+    int K = 0;
+    size_t smem = 0;
+    size_t ws_sync, ws_slots, slot_bytes, ws_q, ws_lagg, ws_bp, ws_lmap, ws_total;
+};
+
+bool make_stream_plan(int D, int op, int64_t T, StPlan& P) {
+    DevInfo di;
+    if (!dev_info(di) || D < 1 || D > 8) return false;
+    P = StPlan{};
+    const int NT = hmm::stream_nt(D), S = hmm::stream_s(D);
+    int64_t G = cdiv(T, (int64_t)NT * S);
+    if (G > di.sms) G = di.sms;
+    int64_t n = round_up(cdiv(T, G * NT), S);
+    G = cdiv(T, n * NT);
+    if (G < 1) G = 1;
+    P.G = (int)G;
+    P.n = n;
+    P.K = (int)(n / S);
+    hmm::StreamLayout L = hmm::stream_smem_layout(D, P.G);
+    if (L.total > (size_t)di.smem_optin) return false;
+    P.smem = L.total;
+    const size_t lanes = (size_t)P.G * NT, QB = hmm::stream_qb(D);
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t o = off; off = (off + bytes + 255) & ~(size_t)255; return o; };
+    P.ws_sync = take(64);
+    P.slot_bytes = hmm::small_slot_bytes(D);
+    P.ws_slots = take((size_t)P.G * P.slot_bytes);
+    P.ws_q = take(op == 0 ? lanes * P.K * QB : 0);
+    P.ws_lagg = take(lanes * QB);
+    P.ws_bp = take(op == 1 ? (size_t)(T + S) * hmm::small_bpb(D) + 16 : 0);
+    P.ws_lmap = take(op == 1 ? lanes * 8 : 0);
+    P.ws_total = off;
+    return true;
+}
+
+// Long single sequences whose CTA ranges do not fit in shared memory take the streaming kernel
+// (as do all split-phase calls); it needs 16-B aligned sequence buffers for its bulk copies.
+thread_local int t_force_path = 0;  // hmm_debug_force_path
+
+bool use_stream(int D, int64_t T, int64_t B, bool dist) {
+    if (D > 8 || B != 1) return false;
+    if (t_force_path == 1) return true;
+    if (t_force_path == 2) return false;
+    if (dist) return true;
+    Plan P;
+    if (!make_plan(D, 0, T, B, P)) return true;
+    return !P.fused;
+}
+bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
 // Profiling hook (hmm_debug_set_timers): per-thread, not used unless set.
 thread_local unsigned long long* t_timers = nullptr;
 
@@ -232,6 +288,27 @@ hmm_status_t run(int op, int D, int64_t T, int64_t B, const float* log_pi, const
         return HMM_ERR_INVALID_VALUE;
     if (dist && (D > 8 || B != 1 || da.world < 1 || da.rank < 0 || da.rank >= da.world || da.t_base < 0))
         return D > 8 ? HMM_ERR_UNSUPPORTED : HMM_ERR_INVALID_VALUE;
+    if (use_stream(D, T, B, dist) && al16(log_lik) && (!filtered || al16(filtered)) && (!smoothed || al16(smoothed)) &&
+        (!path || al16(path))) {
+        StPlan SP;
+        if (!make_stream_plan(D, op, T, SP)) return HMM_ERR_UNSUPPORTED;
+        if (!ws || ws_bytes < SP.ws_total || (reinterpret_cast<uintptr_t>(ws) & 255u)) return HMM_ERR_WORKSPACE;
+        hmm::SParams sp;
+        std::memset(&sp, 0, sizeof(sp));
+        sp.T = T; sp.n = SP.n; sp.K = SP.K;
+        sp.log_pi = log_pi; sp.log_A = log_A; sp.log_lik = log_lik;
+        sp.filtered = filtered; sp.smoothed = smoothed; sp.path = path; sp.scalar_out = scalar; sp.info = info;
+        sp.ws = static_cast<uint8_t*>(ws);
+        sp.ws_sync = SP.ws_sync; sp.ws_slots = SP.ws_slots; sp.slot_bytes = SP.slot_bytes; sp.ws_q = SP.ws_q;
+        sp.ws_lagg = SP.ws_lagg; sp.ws_bp = SP.ws_bp; sp.ws_lmap = SP.ws_lmap;
+        sp.L = hmm::stream_smem_layout(D, SP.G);
+        sp.timers = t_timers;
+        sp.mode = da.mode; sp.rank = da.rank; sp.world = da.world; sp.t_base = da.t_base;
+        sp.agg_all = da.agg_all; sp.agg_stride = (int)(hmm::align16((size_t)D * D * 4) / 4);
+        sp.agg_out = da.agg_out; sp.rec_all = da.rec_all; sp.rec_out = da.rec_out;
+        cudaError_t e = hmm::launch_stream(D, op, (unsigned)SP.G, sp, static_cast<cudaStream_t>(stream));
+        return e == cudaSuccess ? HMM_SUCCESS : HMM_ERR_CUDA;
+    }
     Plan P;
     if (!make_plan(D, op, T, B, P, dist)) return HMM_ERR_UNSUPPORTED;
     if (!ws || ws_bytes < P.ws_total || (reinterpret_cast<uintptr_t>(ws) & 255u)) return HMM_ERR_WORKSPACE;
@@ -273,7 +350,15 @@ const char* hmm_version(void) { return "hmmscan 0.1 sm_100a"; }
 
 void hmm_debug_set_timers(unsigned long long* device_buf) { t_timers = device_buf; }
 
+void hmm_debug_force_path(int path) { t_force_path = (path >= 0 && path <= 2) ? path : 0; }
+
 int hmm_debug_plan(int op, int D, int64_t T, int64_t B, int64_t* out /*[8]*/) {
+    StPlan SP;
+    if (use_stream(D, T, B, false) && make_stream_plan(D, op, T, SP)) {
+        out[0] = SP.G; out[1] = SP.n; out[2] = hmm::stream_s(D); out[3] = hmm::stream_s(D); out[4] = SP.K;
+        out[5] = 2; out[6] = (int64_t)SP.smem; out[7] = hmm::stream_nt(D);
+        return 1;
+    }
     Plan P;
     if (!make_plan(D, op, T, B, P)) return 0;
     out[0] = P.G; out[1] = P.R; out[2] = P.S; out[3] = P.chunk; out[4] = P.K; out[5] = P.fused;
@@ -290,7 +375,10 @@ size_t hmm_workspace_size(int op, int D, int64_t T, int64_t B) {
     }
     Plan P;
     if (!make_plan(D, op, T, B, P)) return 0;
-    return P.ws_total;
+    size_t w = P.ws_total;
+    StPlan SP;
+    if (B == 1 && D <= 8 && make_stream_plan(D, op, T, SP) && SP.ws_total > w) w = SP.ws_total;
+    return w;
 }
 
 hmm_status_t hmm_smooth(int D, int64_t T, const float* log_pi, const float* log_A, const float* log_lik,
@@ -315,7 +403,10 @@ size_t hmm_dist_workspace_size(int op, int D, int64_t T_local) {
     if ((op != 0 && op != 1) || D < 1 || D > 8 || T_local < 1) return 0;
     Plan P;
     if (!make_plan(D, op, T_local, 1, P, true)) return 0;
-    return P.ws_total;
+    size_t w = P.ws_total;
+    StPlan SP;
+    if (make_stream_plan(D, op, T_local, SP) && SP.ws_total > w) w = SP.ws_total;
+    return w;
 }
 
 hmm_status_t hmm_smooth_dist_reduce(int D, int64_t T_local, int64_t t_base, const float* log_pi, const float* log_A,

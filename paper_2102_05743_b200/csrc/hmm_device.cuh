@@ -61,6 +61,24 @@ __device__ __forceinline__ void bulk_wait_read_all() {
     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// Per-thread asynchronous global -> shared copies (cp.async, SASS LDGSTS): a normal per-thread
+// instruction, unlike UBLKCP whose operands live in uniform registers (per-lane addresses serialise).
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
+}
+// zero-filling variant: copies src_bytes (0..16) and fills the rest of the 16 B with zeros
+__device__ __forceinline__ void cp_async16_zfill(void* sdst, const void* gsrc, uint32_t src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(sdst)), "l"(gsrc), "r"(src_bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* sdst, const void* gsrc) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 // Make generic-proxy shared-memory writes visible to the async proxy (before a bulk store reads them).
 __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -119,6 +137,33 @@ __device__ __forceinline__ float max3(float a, float b, float c) {
     float r;
     asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
     return r;
+}
+// Exponent offset d = 127 - E(m) (E = biased exponent), as an exact float: m * 2^d lies in [1,2) for a
+// positive normal m.  Used as an additive term of an ex2 argument, so applying the power-of-two
+// renormalisation costs no multiplies.  Built with the 2^23 magic constant (no I2F).
+__device__ __forceinline__ float exp_offset(float m) {
+    const float biased = __uint_as_float((__float_as_uint(m) >> 23) | 0x4B000000u);  // 2^23 + E (m >= 0)
+    return 8388735.0f - biased;                                                      // (2^23 + 127) - (2^23 + E)
+}
+// Max of N values by a 3-ary tree (depth ~log3 N instead of a serial chain).
+template <int N>
+__device__ __forceinline__ float vmax_tree(const float* v) {
+    if constexpr (N <= 3) {
+        if constexpr (N == 1) return v[0];
+        else if constexpr (N == 2) return fmaxf(v[0], v[1]);
+        else return max3(v[0], v[1], v[2]);
+    } else {
+        constexpr int G = (N + 2) / 3;
+        float w[G];
+#pragma unroll
+        for (int g = 0; g < G; g++) {
+            const int a = 3 * g;
+            if (a + 2 < N) w[g] = max3(v[a], v[a + 1], v[a + 2]);
+            else if (a + 1 < N) w[g] = fmaxf(v[a], v[a + 1]);
+            else w[g] = v[a];
+        }
+        return vmax_tree<G>(w);
+    }
 }
 // Exact power-of-two factor s with m*s in [1,2) for a positive normal m; 1 for 0 / denormal / huge.
 __device__ __forceinline__ float pow2_inv(float m) {

@@ -134,6 +134,68 @@ struct KParams {
     size_t ws_cmap;          // per-chunk Viterbi maps persisted between modes 3 and 4
 };
 
+
+// ---------------------------------------------------------------------------- lane streaming
+// Long single sequences (DESIGN.md §"Streaming"): lane g = c*NT + tid of the G CTAs owns the
+// contiguous steps [g*n, min((g+1)*n, T)), walked in slices of S steps staged by per-lane bulk copies.
+__host__ __device__ constexpr int stream_nt(int D) { return D <= 4 ? 256 : 128; }
+__host__ __device__ constexpr int stream_s(int D) {
+    return D == 1 ? 64 : D == 2 ? 32 : D == 3 ? 20 : D == 4 ? 16 : D == 5 ? 12 : 8;
+}
+// per-lane SMEM slot: S rows + 16 B (the pad staggers lanes across banks for LDS.128)
+__host__ __device__ constexpr int stream_pitch(int D) { return stream_s(D) * D * 4 + 16; }
+// bytes of one stored D x D matrix (16-B aligned slot)
+__host__ __device__ constexpr int stream_qb(int D) { return (D * D * 4 + 15) & ~15; }
+
+struct StreamLayout {
+    size_t ring, qbuf, tree, maps, ends, stage, misc, total;
+};
+__host__ __device__ inline StreamLayout stream_smem_layout(int D, int G) {
+    const int NT = stream_nt(D), NE = small_ne(D);
+    StreamLayout L{};
+    const size_t ring = (size_t)3 * NT * stream_pitch(D);
+    L.ring = 0;
+    L.tree = 0;  // the trees and the CTA-root staging reuse the ring between the passes
+    L.maps = align16((size_t)2 * NT * NE * 4);
+    L.ends = L.maps + align16((size_t)2 * NT * 8);
+    L.stage = L.ends + align16((size_t)2 * NT * 4);
+    size_t u = L.stage + align16((size_t)G * small_slot_bytes(D));
+    if (u < ring) u = ring;
+    L.qbuf = align16(u);
+    L.misc = L.qbuf + (size_t)NT * stream_qb(D);
+    L.total = align16(L.misc + 512);
+    return L;
+}
+
+struct SParams {
+    int64_t T;       // steps (local slice in split-phase modes)
+    int64_t n;       // steps per lane (multiple of S)
+    int K;           // slices per lane = n / S
+    const float* log_pi;
+    const float* log_A;
+    const float* log_lik;
+    float* filtered;
+    float* smoothed;
+    int32_t* path;
+    double* scalar_out;
+    int32_t* info;
+    uint8_t* ws;
+    size_t ws_sync, ws_slots, slot_bytes;
+    size_t ws_q;     // smoother: [G][K][NT] suffix products of each lane's later slices (QB bytes each)
+    size_t ws_lagg;  // [G][NT] lane aggregates (split phase: reduce -> finish / forward)
+    size_t ws_bp;    // Viterbi: backpointers by local step (bpb bytes each)
+    size_t ws_lmap;  // Viterbi: [G][NT] lane maps (split phase: forward -> finish)
+    StreamLayout L;
+    unsigned long long* timers;
+    int mode, rank, world;
+    int64_t t_base;
+    const float* agg_all;
+    int agg_stride;
+    float* agg_out;
+    const uint8_t* rec_all;
+    uint8_t* rec_out;
+};
+
 enum { HMM_MODE_FULL = 0, HMM_MODE_REDUCE = 1, HMM_MODE_SFINISH = 2, HMM_MODE_VFORWARD = 3, HMM_MODE_VFINISH = 4 };
 
 }  // namespace hmm

@@ -1,0 +1,930 @@
+// hmm_stream.cu — lane-streaming parallel scan for long single sequences, 1 <= D <= 8, sm_100a.
+//
+// Same method as hmm_small.cu (Algorithm 3 / Algorithm 5 with block-wise elements, PAPER.md:408-426,
+// 722-740, 759-760), decomposed for sequences too long to stay resident in shared memory:
+//
+//   lane   thread g = c*NT + tid of CTA c owns the contiguous steps [g*n, min((g+1)*n, T)) and walks
+//          them in slices of S steps staged in a private SMEM slot of a 3-deep ring; a warp moves its
+//          32 lane slices cooperatively (cp.async 16 B per thread, coalesced), so loads run two
+//          slices ahead of the math without any CTA-wide synchronisation inside the passes.
+//   pass 1 each lane folds its range right-to-left into one D x D aggregate (Def. 3 matrix product /
+//          Def. 5 max-plus product).  The smoother also stores, per slice k, the product Q_k of the
+//          lane's slices right of k (the suffix that turns the lane's backward carry into the
+//          backward potential at the end of slice k, Thm. 2), so pass 2 needs no second fold.
+//   scan   lane aggregates -> CTA tree (SMEM) -> grid exchange of the G CTA roots (global memory,
+//          arrival counter, cooperative launch) -> lane carries: forward potential a_{0:k} (Thm. 1),
+//          backward potential (Thm. 2), or the max-product forward carry (Alg. 5).
+//   pass 2 smoother: per slice, the forward filter continues the lane's running alpha (Alg. 1 forward,
+//          normalised; log Z by telescoping the applied multipliers over the whole lane), the
+//          backward pass starts from Q_k times the lane's backward carry, Eq. 14 gives the smoothed
+//          marginals; both outputs leave by warp-cooperative streaming stores.  Viterbi: forward sweep with
+//          backpointers (Alg. 4 lines 3-6) written to the workspace, lane backpointer map composed.
+//   pass 3 Viterbi: lane end states from the map tree / exchange, backtrack slice by slice.
+//
+// Pass 1 runs right-to-left so that the slices it loads last (the first slice of every lane) are the
+// first pass 2 reads: up to ~L2-size of the re-read is served from the 126 MB L2.
+#include <cstdint>
+#include <cstring>
+
+#include "hmm_device.cuh"
+#include "hmm_plan.h"
+#include "hmm_small_ops.cuh"
+
+namespace hmm {
+
+// ---------------------------------------------------------------------------- slice folds
+// Sum-product, right to left over one slice: P <- psi_t P for t = nr-1 .. 0 (psi_t = A diag(l_t),
+// psi_0 = 1 (pi o l_0)^T when the slice starts the sequence).  Renormalisation is exact and free: the
+// power-of-two factor 2^d that brings max(P) into [1,2) is added to the next step's ex2 argument,
+// l_t = 2^(log2e (ll_t - m_t) + d), so a step costs D^3 FMA + D^2 FMUL (A diag(l)) + D FFMA + D MUFU +
+// the max tree.  `d` carries the pending offset between slices.  An impossible step (all -inf) gives
+// l = 0; NaN / +inf inputs turn into NaN through ll - m and are caught by the caller's final check.
+template <int D>
+__device__ __forceinline__ void sp_back_step(const float* row, bool t0, const float* A, const float* pi, float* P,
+                                             float& d) {
+    float v[D], l[D];
+    ld_row<D>(row, v);
+    const float m = fmaxf(vmax<D>(v), -1e30f);  // all -inf (impossible step): l = 0, -m*log2e stays finite
+    const float c = fmaf(-m, kLog2e, d);
+#pragma unroll
+    for (int j = 0; j < D; j++) l[j] = ex2(fmaf(v[j], kLog2e, c));
+    float Pn[D * D];
+    if (t0) {
+        float r[D];
+#pragma unroll
+        for (int j = 0; j < D; j++) {
+            float acc = (pi[0] * l[0]) * P[j];
+#pragma unroll
+            for (int k = 1; k < D; k++) acc = fmaf(pi[k] * l[k], P[k * D + j], acc);
+            r[j] = acc;
+        }
+#pragma unroll
+        for (int i = 0; i < D; i++)
+#pragma unroll
+            for (int j = 0; j < D; j++) Pn[i * D + j] = r[j];
+    } else {
+#pragma unroll
+        for (int i = 0; i < D; i++) {
+            float a[D];
+#pragma unroll
+            for (int k = 0; k < D; k++) a[k] = A[i * D + k] * l[k];
+#pragma unroll
+            for (int j = 0; j < D; j++) {
+                float acc = a[0] * P[j];
+#pragma unroll
+                for (int k = 1; k < D; k++) acc = fmaf(a[k], P[k * D + j], acc);
+                Pn[i * D + j] = acc;
+            }
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < D * D; e++) P[e] = Pn[e];
+    d = exp_offset(vmax_tree<D * D>(P));
+}
+template <int D, int S>
+__device__ __forceinline__ void sp_fold_back(const float* rows, int nr, bool t0, const float* A, const float* pi,
+                                             float* P, float& d) {
+    if (nr == S) {
+#pragma unroll 4
+        for (int ii = S - 1; ii >= 1; ii--) sp_back_step<D>(rows + ii * D, false, A, pi, P, d);
+    } else {
+#pragma unroll 1
+        for (int ii = nr - 1; ii >= 1; ii--) sp_back_step<D>(rows + ii * D, false, A, pi, P, d);
+    }
+    sp_back_step<D>(rows, t0, A, pi, P, d);
+}
+
+// Max-product (log domain), right to left: P(i,j) <- max_k (LA(i,k) + w_t(k) + P(k,j)), w_t = ll_t - m_t
+// (row-independent LP(k) + w_0(k) for the sequence's first step).  `chk` collects NaN evidence.
+template <int D, int S>
+__device__ __forceinline__ void mp_fold_back(const float* rows, int nr, bool t0, const float* LA, const float* LP,
+                                             float* P, float& chk) {
+#pragma unroll
+    for (int ii = S - 1; ii >= 0; ii--) {
+        if (ii < nr) {
+            float v[D], W[D * D];
+            ld_row<D>(rows + ii * D, v);
+            float m = vmax<D>(v);
+            if (!(m > neg_inf())) m = 0.0f;
+            float w[D];
+#pragma unroll
+            for (int k = 0; k < D; k++) w[k] = v[k] - m;
+            chk += vsum<D>(w);
+#pragma unroll
+            for (int k = 0; k < D; k++)
+#pragma unroll
+                for (int j = 0; j < D; j++) W[k * D + j] = w[k] + P[k * D + j];
+            float Pn[D * D];
+#pragma unroll
+            for (int i = 0; i < D; i++) {
+#pragma unroll
+                for (int j = 0; j < D; j++) {
+                    float sc[D];
+#pragma unroll
+                    for (int k = 0; k < D; k++) sc[k] = ((ii == 0 && t0) ? LP[k] : LA[i * D + k]) + W[k * D + j];
+                    Pn[i * D + j] = vmax<D>(sc);
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < D * D; e++) P[e] = Pn[e];
+        }
+    }
+}
+
+// Forward filter over one slice, continuing the lane's alpha.  The log-Z bookkeeping (running
+// product of the applied multipliers with its exponent split off, sum of m_t) persists across the
+// lane's slices and is closed once per lane (see sp_alpha in hmm_small_ops.cuh); m_t is summed in
+// fp32 within the slice (<= 64 terms) and added to the fp64 total once per slice.  Rows are turned
+// into l_t in place; filtered rows go to `frows`.  Returns the first zero-mass row, or -1.
+template <int D>
+__device__ __forceinline__ bool sp_alpha_step(float* row, float* frow, bool t0, const float* A, const float* pi,
+                                              float* alpha, float& rprod, int& rexp, float& msl) {
+    float l[D];
+    ld_row<D>(row, l);
+    const float m = vmax<D>(l);
+    const bool ok = m > -FLT_MAX;  // false: impossible step (all -inf), l = 0
+    msl += ok ? m : 0.0f;
+    const float c0 = ok ? -m * kLog2e : 0.0f;
+#pragma unroll
+    for (int j = 0; j < D; j++) l[j] = ex2(fmaf(l[j], kLog2e, c0));
+    st_row<D>(row, l);
+    float ah[D];
+    if (t0) {
+#pragma unroll
+        for (int j = 0; j < D; j++) ah[j] = pi[j] * l[j];
+    } else {
+#pragma unroll
+        for (int j = 0; j < D; j++) {
+            float acc = alpha[0] * A[j];
+#pragma unroll
+            for (int k = 1; k < D; k++) acc = fmaf(alpha[k], A[k * D + j], acc);
+            ah[j] = acc * l[j];
+        }
+    }
+    const float c = vsum<D>(ah);
+    const float r = rcp(c);
+#pragma unroll
+    for (int j = 0; j < D; j++) alpha[j] = ah[j] * r;
+    st_row<D>(frow, alpha);
+    rprod *= r;
+    const uint32_t bits = __float_as_uint(rprod);
+    rexp += (int)((bits >> 23) & 0xffu) - 127;
+    rprod = __uint_as_float((bits & 0x807fffffu) | 0x3f800000u);
+    return c > 0.0f;
+}
+template <int D, int S>
+__device__ __forceinline__ int sp_alpha_slice(float* rows, float* frows, int nr, bool t0, const float* A,
+                                              const float* pi, float* alpha, float& rprod, int& rexp,
+                                              double& msum) {
+    int zero_i = -1;
+    float msl = 0.0f;
+    if (!sp_alpha_step<D>(rows, frows, t0, A, pi, alpha, rprod, rexp, msl)) zero_i = 0;
+    if (nr == S) {
+#pragma unroll 4
+        for (int i = 1; i < S; i++)
+            if (!sp_alpha_step<D>(rows + i * D, frows + i * D, false, A, pi, alpha, rprod, rexp, msl) && zero_i < 0)
+                zero_i = i;
+    } else {
+#pragma unroll 1
+        for (int i = 1; i < nr; i++)
+            if (!sp_alpha_step<D>(rows + i * D, frows + i * D, false, A, pi, alpha, rprod, rexp, msl) && zero_i < 0)
+                zero_i = i;
+    }
+    msum += (double)msl;
+    return zero_i;
+}
+
+// Backward pass over one slice from the backward potential at its last step, combined with Eq. 14
+// (smoothed_t = alpha_t beta_t / Z_t, written over the l rows).
+template <int D>
+__device__ __forceinline__ void sp_beta_step(float* lrow, const float* frow, const float* A, float* beta) {
+    float l[D], a[D], g[D];
+    ld_row<D>(lrow, l);
+    ld_row<D>(frow, a);
+#pragma unroll
+    for (int j = 0; j < D; j++) g[j] = a[j] * beta[j];
+    const float z = rcp(vsum<D>(g));
+#pragma unroll
+    for (int j = 0; j < D; j++) g[j] *= z;
+    st_row<D>(lrow, g);
+    float w[D], bn[D];
+#pragma unroll
+    for (int j = 0; j < D; j++) w[j] = l[j] * beta[j];
+#pragma unroll
+    for (int r = 0; r < D; r++) {
+        float acc = A[r * D] * w[0];
+#pragma unroll
+        for (int j = 1; j < D; j++) acc = fmaf(A[r * D + j], w[j], acc);
+        bn[r] = acc;
+    }
+    const float sc = pow2_inv(vmax<D>(bn));
+#pragma unroll
+    for (int r = 0; r < D; r++) beta[r] = bn[r] * sc;
+}
+template <int D, int S>
+__device__ __forceinline__ void sp_beta_slice(float* lrows, const float* frows, int nr, const float* A, float* beta) {
+    if (nr == S) {
+#pragma unroll 4
+        for (int i = S - 1; i >= 0; i--) sp_beta_step<D>(lrows + i * D, frows + i * D, A, beta);
+    } else {
+#pragma unroll 1
+        for (int i = nr - 1; i >= 0; i--) sp_beta_step<D>(lrows + i * D, frows + i * D, A, beta);
+    }
+}
+
+// Viterbi forward sweep over one slice (Alg. 4 lines 3-6): backpointers into registers (D <= 4:
+// one 16-bit nibble word per step, two steps per u32; D > 4: one u32 per step), returns the slice
+// map f(x_end) = state before the slice, accumulates sum (o_t + m_t).
+template <int D> __host__ __device__ constexpr int st_bpw(int S) { return D <= 4 ? S / 2 : S; }
+template <int D, int S>
+__device__ __forceinline__ uint64_t vit_fwd_slice(const float* rows, int nr, bool t0, const float* LA,
+                                                  const float* LP, float* V, double& lp, int& zero_i,
+                                                  uint32_t* bpw) {
+    uint32_t olo = 0x03020100u, ohi = 0x07060504u;
+    zero_i = -1;
+    float acc = 0.0f;
+    double dacc = 0.0;
+#pragma unroll
+    for (int i = 0; i < st_bpw<D>(S); i++) bpw[i] = 0u;
+#pragma unroll
+    for (int i = 0; i < S; i++) {
+        if (i < nr) {
+            float v[D];
+            ld_row<D>(rows + i * D, v);
+            float m = vmax<D>(v);
+            if (!(m > neg_inf())) m = 0.0f;
+            float Vh[D];
+            uint32_t sel = 0;
+#pragma unroll
+            for (int j = 0; j < D; j++) {
+                const bool first = t0 && i == 0;
+                float best = V[0] + (first ? LP[j] : LA[j]);
+                int arg = 0;
+#pragma unroll
+                for (int k = 1; k < D; k++) {
+                    const float sc = V[k] + (first ? LP[j] : LA[k * D + j]);
+                    if (sc > best) { best = sc; arg = k; }
+                }
+                Vh[j] = best + (v[j] - m);
+                sel |= (uint32_t)arg << (4 * j);
+            }
+            float o = vmax<D>(Vh);
+            if (!(o > neg_inf())) {
+                if (zero_i < 0) zero_i = i;
+                o = 0.0f;
+            }
+#pragma unroll
+            for (int j = 0; j < D; j++) V[j] = Vh[j] - o;
+            dacc += (double)(o + m);
+            if constexpr (D <= 4) {
+                bpw[i >> 1] |= sel << (16 * (i & 1));
+                olo = __byte_perm(olo, 0u, sel);
+            } else {
+                bpw[i] = sel;
+                const uint32_t nlo = __byte_perm(olo, ohi, sel & 0xffffu);
+                ohi = __byte_perm(olo, ohi, sel >> 16);
+                olo = nlo;
+            }
+        }
+    }
+    (void)acc;
+    lp += dacc;
+    uint64_t f = ((uint64_t)ohi << 32) | olo;
+    if constexpr (D < 8) f &= (1ull << (8 * D)) - 1ull;
+    return f;
+}
+// Backtrack over one slice from its end state x; returns the state before the slice.
+template <int D, int S>
+__device__ __forceinline__ int vit_back_slice(const uint32_t* bpw, int nr, int x, int32_t* out) {
+#pragma unroll
+    for (int i = S - 1; i >= 0; i--) {
+        if (i < nr) {
+            out[i] = x;
+            const uint32_t sel = (D <= 4) ? (bpw[i >> 1] >> (16 * (i & 1))) & 0xffffu : bpw[i];
+            x = (int)((sel >> (4 * x)) & 0xfu);
+        }
+    }
+    return x;
+}
+
+// ---------------------------------------------------------------------------- the kernel
+// grid = G CTAs (one per SM, cooperative), block = NT lanes.  OP 0: smoother, OP 1: Viterbi.
+template <int D, int OP>
+__global__ void __launch_bounds__(stream_nt(D)) hmm_stream_kernel(const SParams p) {
+    constexpr int NT = stream_nt(D);
+    constexpr int NW = NT / 32;
+    constexpr int S = stream_s(D);
+    constexpr int PITCH = stream_pitch(D);
+    constexpr int QB = stream_qb(D);
+    constexpr int BPW = st_bpw<D>(S);     // backpointer words per slice
+    constexpr int BPB = small_bpb(D);     // backpointer bytes per step
+    constexpr bool MP = (OP == 1);
+    constexpr int NN = 2 * NT;
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int c = blockIdx.x, G = gridDim.x;
+    const int64_t T = p.T, n = p.n, tb = p.t_base;
+    const int K = p.K;
+    const int mode = p.mode;
+    const int64_t a0 = ((int64_t)c * NT + tid) * n;           // lane range [a0, a1)
+    const int64_t a1 = (a0 + n < T) ? a0 + n : T;
+    const int nsl = (a0 < a1) ? (int)((a1 - a0 + S - 1) / S) : 0;  // real slices of this lane
+    auto slice_rows = [&](int k) -> int {
+        if (k >= nsl) return 0;
+        const int64_t r0 = a0 + (int64_t)k * S;
+        return (int)((a1 - r0 < S) ? a1 - r0 : S);
+    };
+
+    uint32_t* sync = reinterpret_cast<uint32_t*>(p.ws + p.ws_sync);
+    unsigned long long* arrive1 = reinterpret_cast<unsigned long long*>(sync + 0);
+    unsigned long long* arrive2 = reinterpret_cast<unsigned long long*>(sync + 2);
+    unsigned long long* zero_code = reinterpret_cast<unsigned long long*>(sync + 4);
+    uint32_t* done_ctr = sync + 7;
+    uint32_t* bad_flag = sync + 8;
+    uint8_t* slots = p.ws + p.ws_slots;
+    const size_t map_off = align16((size_t)D * D * 4);
+    const int sw = (int)(p.slot_bytes / 4);
+    uint8_t* myslot = slots + (size_t)c * p.slot_bytes;
+
+    uint8_t* ring = smem + p.L.ring;
+    float* tree = reinterpret_cast<float*>(smem + p.L.tree);
+    uint64_t* maps = reinterpret_cast<uint64_t*>(smem + p.L.maps);
+    int32_t* ends = reinterpret_cast<int32_t*>(smem + p.L.ends);
+    float* stage = reinterpret_cast<float*>(smem + p.L.stage);
+    uint8_t* qbuf = smem + p.L.qbuf;
+    uint64_t* qbar = reinterpret_cast<uint64_t*>(smem + p.L.misc);  // [NW] Q-block barriers
+    double* red = reinterpret_cast<double*>(qbar + NW);
+    float* cta_pre = reinterpret_cast<float*>(red + NW);
+    float* cta_suf = cta_pre + D;
+    int* flag = reinterpret_cast<int*>(cta_suf + D);
+
+    unsigned long long* tmr = p.timers ? p.timers + (size_t)c * 16 : nullptr;
+#define HMM_STAMP(i) do { if (tmr && tid == 0) tmr[i] = global_ns(); } while (0)
+    HMM_STAMP(0);
+    if (tid == 0) {
+        for (int w = 0; w < NW; w++) mbar_init(&qbar[w], 1);
+        fence_mbar_init();
+        flag[0] = -1;
+    }
+    __syncthreads();
+
+    float A[D * D], pv[D];
+#pragma unroll
+    for (int e = 0; e < D * D; e++) {
+        const float la = __ldg(p.log_A + e);
+        A[e] = MP ? la : ex2(la * kLog2e);
+    }
+#pragma unroll
+    for (int d = 0; d < D; d++) {
+        const float lp = __ldg(p.log_pi + d);
+        pv[d] = MP ? lp : ex2(lp * kLog2e);
+    }
+
+    bool bad = false;
+    double acc = 0.0;
+    int64_t zero_t = INT64_MAX;
+    const float* ll = p.log_lik;
+    // lane's slot in ring stage st
+    auto slot = [&](int st) -> float* {
+        return reinterpret_cast<float*>(ring + (size_t)st * NT * PITCH + (size_t)tid * PITCH);
+    };
+    // Warp-cooperative slice movement.  A lane's slice is S*D*4 contiguous bytes, but the 32 lanes of
+    // a warp are n steps apart, so per-lane bulk copies (UBLKCP takes uniform operands: the compiler
+    // serialises them over the lanes) cost ~10 instructions per lane.  Instead the warp moves its 32
+    // slices with 16-B per-thread accesses, CPL consecutive threads per lane slice: cp.async (LDGSTS)
+    // for loads into the ring, LDS + streaming STG.128 for stores -- fully coalesced segments.
+    constexpr int CPL = S * D / 4;  // 16-B chunks per full lane slice
+    const int64_t wbase = ((int64_t)c * NT + warp * 32) * n;  // first step of this warp's lane 0
+    auto lane_rows = [&](int j, int k) -> int {
+        const int64_t rem = T - (wbase + (int64_t)j * n + (int64_t)k * S);
+        return rem <= 0 ? 0 : (rem < S ? (int)rem : S);
+    };
+    auto warp_full = [&](int k) -> bool { return wbase + 31 * n + (int64_t)k * S + S <= T; };
+    // async load of slice k of the warp's lanes into ring stage st (one cp.async group per call)
+    auto coop_load = [&](int k, int st) {
+        uint8_t* sbase = ring + (size_t)st * NT * PITCH + (size_t)warp * 32 * PITCH;
+        bool done = false;
+        if constexpr ((32 % CPL) == 0) {
+            constexpr int LPI = 32 / CPL;
+            const int ch = lane % CPL, j0 = lane / CPL;
+            const float* src = ll + (wbase + (int64_t)j0 * n + (int64_t)k * S) * D + ch * 4;
+            uint8_t* dst = sbase + (size_t)j0 * PITCH + ch * 16;
+            if (warp_full(k)) {
+#pragma unroll
+                for (int it = 0; it < CPL; it++) {
+                    cp_async16(dst, src);
+                    src += (int64_t)LPI * n * D;
+                    dst += LPI * PITCH;
+                }
+            } else {  // the warp holding the end of the sequence: zero-filling copies, no branches
+                int64_t rem64 = (T - (wbase + (int64_t)j0 * n + (int64_t)k * S)) * D - ch * 4;  // floats left
+                int rem = (int)(rem64 < -(1 << 30) ? -(1 << 30) : (rem64 > (1 << 30) ? (1 << 30) : rem64));
+                const int step = LPI * (int)n * D;
+#pragma unroll
+                for (int it = 0; it < CPL; it++) {
+                    const int f = rem < 0 ? 0 : (rem > 4 ? 4 : rem);
+                    cp_async16_zfill(dst, f > 0 ? src : ll, 4u * f);
+                    src += (int64_t)step;
+                    dst += LPI * PITCH;
+                    rem -= step;
+                }
+            }
+            done = true;
+        }
+        if (!done) {
+            for (int q = lane; q < 32 * CPL; q += 32) {
+                const int j = q / CPL, ch = q - j * CPL;
+                const int fl = lane_rows(j, k) * D, f0 = ch * 4;
+                if (f0 >= fl) continue;
+                const float* src = ll + (wbase + (int64_t)j * n + (int64_t)k * S) * D + f0;
+                float* dst = reinterpret_cast<float*>(sbase + (size_t)j * PITCH) + f0;
+                if (f0 + 4 <= fl) {
+                    cp_async16(dst, src);
+                } else {
+                    for (int f = 0; f < fl - f0; f++) cp_async4(dst + f, src + f);
+                }
+            }
+        }
+        cp_async_commit();
+    };
+    // store slice k of the warp's lanes from SMEM slots (stage base `sb`) to the sequence buffer g
+    auto coop_store = [&](int k, const uint8_t* sb, float* g) {
+        const uint8_t* sbase = sb + (size_t)warp * 32 * PITCH;
+        bool done = false;
+        if constexpr ((32 % CPL) == 0) {
+            constexpr int LPI = 32 / CPL;
+            const int ch = lane % CPL, j0 = lane / CPL;
+            float* dst = g + (wbase + (int64_t)j0 * n + (int64_t)k * S) * D + ch * 4;
+            const uint8_t* src = sbase + (size_t)j0 * PITCH + ch * 16;
+            if (warp_full(k)) {
+#pragma unroll
+                for (int it = 0; it < CPL; it++) {
+                    __stcs(reinterpret_cast<float4*>(dst), *reinterpret_cast<const float4*>(src));
+                    dst += (int64_t)LPI * n * D;
+                    src += LPI * PITCH;
+                }
+            } else {
+                int64_t rem64 = (T - (wbase + (int64_t)j0 * n + (int64_t)k * S)) * D - ch * 4;
+                int rem = (int)(rem64 < -(1 << 30) ? -(1 << 30) : (rem64 > (1 << 30) ? (1 << 30) : rem64));
+                const int step = LPI * (int)n * D;
+                const int rem0 = rem;
+#pragma unroll
+                for (int it = 0; it < CPL; it++) {  // whole 16-B chunks: predicated stores only
+                    if (rem >= 4) __stcs(reinterpret_cast<float4*>(dst), *reinterpret_cast<const float4*>(src));
+                    dst += (int64_t)step;
+                    src += LPI * PITCH;
+                    rem -= step;
+                }
+                // the one chunk of the sequence that ends inside 16 B (T*D not a multiple of 4)
+                if (rem0 > 0) {
+                    const int it = rem0 / step, r = rem0 - it * step;
+                    if (it < CPL && r > 0 && r < 4) {
+                        float* d2 = g + (wbase + (int64_t)(j0 + it * LPI) * n + (int64_t)k * S) * D + ch * 4;
+                        const float* s2 = reinterpret_cast<const float*>(sbase + (size_t)(j0 + it * LPI) * PITCH + ch * 16);
+                        for (int f = 0; f < r; f++) d2[f] = s2[f];
+                    }
+                }
+            }
+            done = true;
+        }
+        if (!done) {
+            for (int q = lane; q < 32 * CPL; q += 32) {
+                const int j = q / CPL, ch = q - j * CPL;
+                const int fl = lane_rows(j, k) * D, f0 = ch * 4;
+                if (f0 >= fl) continue;
+                float* dst = g + (wbase + (int64_t)j * n + (int64_t)k * S) * D + f0;
+                const float* src = reinterpret_cast<const float*>(sbase + (size_t)j * PITCH) + f0;
+                if (f0 + 4 <= fl) {
+                    __stcs(reinterpret_cast<float4*>(dst), *reinterpret_cast<const float4*>(src));
+                } else {
+                    for (int f = 0; f < fl - f0; f++) dst[f] = src[f];
+                }
+            }
+        }
+    };
+    auto stage_base = [&](int st) -> uint8_t* { return ring + (size_t)st * NT * PITCH; };
+
+    const bool do_pass1 = (mode == HMM_MODE_FULL || mode == HMM_MODE_REDUCE);
+    float P[D * D];
+    // ===================== pass 1: right-to-left fold of the lane (3-stage ring, 2 slices in flight)
+    if (do_pass1) {
+        mat_identity<D, MP>(P);
+        float dexp = 0.0f, chk = 0.0f;  // pending exponent offset of P (sum-product)
+        const bool lane_t0 = (tb + a0 == 0) && nsl > 0;
+        float* qdst = reinterpret_cast<float*>(p.ws + p.ws_q);
+        coop_load(K - 1, 0);
+        if (K > 1) coop_load(K - 2, 1); else cp_async_commit();
+        for (int it = 0; it < K; it++) {
+            const int k = K - 1 - it;
+            const int st = it % 3;
+            if (it + 2 < K) coop_load(k - 2, (it + 2) % 3); else cp_async_commit();
+            const int nr = slice_rows(k);
+            if constexpr (!MP) {
+                if (nr > 0) {  // Q_k = product of the slices right of k (normalised), warp-contiguous
+                    const float s = pow2_inv(vmax_tree<D * D>(P));
+#pragma unroll
+                    for (int e = 0; e < D * D; e++) P[e] *= s;
+                    dexp = 0.0f;
+                    float* q = qdst + (((size_t)c * K + k) * NT + tid) * (QB / 4);
+                    if constexpr ((D * D) % 4 == 0) {
+#pragma unroll
+                        for (int e = 0; e < D * D; e += 4)
+                            *reinterpret_cast<float4*>(q + e) = make_float4(P[e], P[e + 1], P[e + 2], P[e + 3]);
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < D * D; e++) q[e] = P[e];
+                    }
+                }
+            }
+            cp_async_wait<2>();
+            __syncwarp();
+            if (nr > 0) {
+                const float* rows = slot(st);
+                if constexpr (MP) {
+                    mp_fold_back<D, S>(rows, nr, lane_t0 && k == 0, A, pv, P, chk);
+                    const float m = vmax<D * D>(P);  // renormalise once per slice (max 0)
+                    if (m > neg_inf()) {
+#pragma unroll
+                        for (int e = 0; e < D * D; e++) P[e] -= m;
+                    }
+                } else {
+                    sp_fold_back<D, S>(rows, nr, lane_t0 && k == 0, A, pv, P, dexp);
+                }
+            }
+            __syncwarp();
+        }
+        if constexpr (MP) {
+            bad |= (chk != chk);
+        } else {
+            const float s = pow2_inv(vmax_tree<D * D>(P));
+#pragma unroll
+            for (int e = 0; e < D * D; e++) P[e] *= s;
+            const float ck = vsum<D * D>(P);
+            bad |= (ck != ck);
+        }
+        if (mode == HMM_MODE_REDUCE) {  // lane aggregate persisted for the finish / forward call
+            float* dst = reinterpret_cast<float*>(p.ws + p.ws_lagg) + ((size_t)c * NT + tid) * (QB / 4);
+#pragma unroll
+            for (int e = 0; e < D * D; e++) dst[e] = P[e];
+        }
+    } else if (mode == HMM_MODE_SFINISH || mode == HMM_MODE_VFORWARD) {
+        const float* src = reinterpret_cast<const float*>(p.ws + p.ws_lagg) + ((size_t)c * NT + tid) * (QB / 4);
+#pragma unroll
+        for (int e = 0; e < D * D; e++) P[e] = __ldcg(src + e);
+    }
+    HMM_STAMP(1);
+    if (tmr && lane == 0 && warp == NW - 1) tmr[11] = global_ns();  // last warp done with pass 1
+    // the ring is reused by the trees from here: all lanes done reading it
+    __syncthreads();
+
+    // ===================== CTA tree over the lane aggregates, grid exchange of the CTA roots
+    if (mode != HMM_MODE_VFINISH) {
+        tree_store<D>(tree, NN, NT + tid, P);
+        __syncthreads();
+        tree_up<D, MP>(tree, NT);
+        if (do_pass1 && tid < D * D) reinterpret_cast<float*>(myslot)[tid] = tree[tid * NN + 1];
+        HMM_STAMP(2);
+        if (G > 1 || !do_pass1 || mode == HMM_MODE_REDUCE) {
+            if (do_pass1) group_arrive_wait(arrive1, (uint32_t)G);
+            HMM_STAMP(3);
+            for (int i = tid; i < G; i += NT) {
+                const float* src = reinterpret_cast<const float*>(slots + (size_t)i * p.slot_bytes);
+                float v[D * D];
+#pragma unroll
+                for (int e = 0; e < D * D; e++) v[e] = __ldcg(src + e);
+#pragma unroll
+                for (int e = 0; e < D * D; e++) stage[(size_t)i * sw + e] = v[e];
+            }
+            __syncthreads();
+        }
+        if (mode == HMM_MODE_REDUCE) {
+            if (c == 0 && warp == 0) {
+                float M[D * D];
+                warp_prod<D, MP>(stage, sw, 0, G, M);
+                if (lane < D * D) p.agg_out[lane] = M[lane];
+            }
+        } else if (warp == 0) {
+            float M[D * D];
+            if (c > 0) warp_prod<D, MP>(stage, sw, 0, c, M);
+            if (lane == 0) {
+                float u[D], v[D];
+#pragma unroll
+                for (int d = 0; d < D; d++) u[d] = v[d] = MP ? 0.0f : 1.0f;
+                for (int q = 0; q < p.rank; q++) {  // ranks to the left (split phase)
+                    float X[D * D];
+#pragma unroll
+                    for (int e = 0; e < D * D; e++) X[e] = __ldg(p.agg_all + (size_t)q * p.agg_stride + e);
+                    vec_mat<D, MP>(u, X, v);
+#pragma unroll
+                    for (int d = 0; d < D; d++) u[d] = v[d];
+                }
+                if (c > 0) vec_mat<D, MP>(u, M, v);
+#pragma unroll
+                for (int d = 0; d < D; d++) cta_pre[d] = v[d];
+            }
+        } else if (warp == 1 && !MP) {
+            float M[D * D];
+            if (c < G - 1) warp_prod<D, MP>(stage, sw, c + 1, G, M);
+            if (lane == 0) {
+                float u[D], v[D];
+#pragma unroll
+                for (int d = 0; d < D; d++) u[d] = v[d] = 1.0f;
+                for (int q = p.world - 1; q > p.rank; q--) {  // ranks to the right
+                    float X[D * D];
+#pragma unroll
+                    for (int e = 0; e < D * D; e++) X[e] = __ldg(p.agg_all + (size_t)q * p.agg_stride + e);
+                    mat_vec<D>(X, u, v);
+#pragma unroll
+                    for (int d = 0; d < D; d++) u[d] = v[d];
+                }
+                if (c < G - 1) mat_vec<D>(M, u, v);
+#pragma unroll
+                for (int d = 0; d < D; d++) cta_suf[d] = v[d];
+            }
+        }
+        __syncthreads();
+    }
+    HMM_STAMP(4);
+    const bool do_sweep = (mode == HMM_MODE_FULL || mode == HMM_MODE_SFINISH || mode == HMM_MODE_VFORWARD);
+    float cin[D], cout_[D];  // lane carries: forward (alpha / V) and backward (beta)
+    if (do_sweep) {
+        tree_down<D, MP, !MP>(tree, NT, cta_pre, cta_suf);
+#pragma unroll
+        for (int d = 0; d < D; d++) {
+            cin[d] = tree[d * NN + NT + tid];
+            cout_[d] = MP ? 0.0f : tree[(D + d) * NN + NT + tid];
+        }
+    }
+    HMM_STAMP(5);
+    __syncthreads();          // tree (ring) dead from here
+    fence_proxy_async_smem();  // generic-proxy SMEM accesses before the bulk copies reuse it
+
+    if constexpr (!MP) {
+        // ===================== smoother pass 2: left to right; ring stages 0/1 = rows, stage 2 = filtered
+        if (do_sweep) {
+            float alpha[D];
+            {
+                const float sm_ = vsum<D>(cin);
+                const float r = (sm_ > 0.0f) ? 1.0f / sm_ : 0.0f;
+#pragma unroll
+                for (int d = 0; d < D; d++) alpha[d] = cin[d] * r;
+            }
+            float rprod = 1.0f;
+            int rexp = 0;
+            double msum = 0.0;
+            const bool lane_t0 = (tb + a0 == 0) && nsl > 0;
+            const uint8_t* qsrc = p.ws + p.ws_q;
+            float* frows = slot(2);
+            auto issue_q = [&](int k) {  // the warp's 32 Q_k slots, one bulk copy by lane 0
+                if (lane == 0) {
+                    const uint32_t bytes = 32u * QB;
+                    mbar_arrive_expect_tx(&qbar[warp], bytes);
+                    bulk_g2s(qbuf + (size_t)warp * 32 * QB, qsrc + (((size_t)c * K + k) * NT + warp * 32) * QB, bytes,
+                             &qbar[warp]);
+                }
+            };
+            uint32_t qphase = 0;
+            coop_load(0, 0);
+            issue_q(0);
+            for (int k = 0; k < K; k++) {
+                const int st = k & 1;
+                if (k + 1 < K) coop_load(k + 1, st ^ 1); else cp_async_commit();
+                cp_async_wait<1>();
+                __syncwarp();
+                mbar_wait(&qbar[warp], qphase);
+                qphase ^= 1u;
+                const int nr = slice_rows(k);
+                float beta[D];
+                if (nr > 0) {
+                    float Q[D * D];
+                    const float* qs = reinterpret_cast<const float*>(qbuf + ((size_t)warp * 32 + lane) * QB);
+#pragma unroll
+                    for (int e = 0; e < D * D; e++) Q[e] = qs[e];
+                    mat_vec<D>(Q, cout_, beta);
+                }
+                __syncwarp();  // every lane has read its Q_k
+                if (k + 1 < K) issue_q(k + 1);
+                if (nr > 0) {
+                    float* rows = slot(st);
+                    const int zi = sp_alpha_slice<D, S>(rows, frows, nr, lane_t0 && k == 0, A, pv, alpha, rprod,
+                                                        rexp, msum);
+                    const int64_t r0 = a0 + (int64_t)k * S;
+                    if (zi >= 0 && tb + r0 + zi < zero_t) zero_t = tb + r0 + zi;
+                    sp_beta_slice<D, S>(rows, frows, nr, A, beta);
+                }
+                __syncwarp();
+                coop_store(k, stage_base(st), p.smoothed);
+                if (p.filtered) coop_store(k, stage_base(2), p.filtered);
+                __syncwarp();
+            }
+            if (nsl > 0) acc += log((double)vsum<D>(alpha)) - log((double)rprod) - (double)rexp * (double)kLn2 + msum;
+            if (tmr && lane == 0 && warp == NW - 1) tmr[12] = global_ns();  // last warp done with pass 2
+        }
+        HMM_STAMP(6);
+    } else {
+        // ===================== Viterbi pass 2: left to right, backpointers to the workspace
+        uint8_t* bpg = p.ws + p.ws_bp;
+        uint64_t F = map_identity(D);
+        if (do_sweep) {
+            float V[D];
+#pragma unroll
+            for (int d = 0; d < D; d++) V[d] = cin[d];
+            const bool lane_t0 = (tb + a0 == 0) && nsl > 0;
+            coop_load(0, 0);
+            if (K > 1) coop_load(1, 1); else cp_async_commit();
+            for (int k = 0; k < K; k++) {
+                const int st = k % 3;
+                if (k + 2 < K) coop_load(k + 2, (k + 2) % 3); else cp_async_commit();
+                cp_async_wait<2>();
+                __syncwarp();
+                const int nr = slice_rows(k);
+                if (nr > 0) {
+                    uint32_t bpw[BPW];
+                    int zi;
+                    const uint64_t f = vit_fwd_slice<D, S>(slot(st), nr, lane_t0 && k == 0, A, pv, V, acc, zi, bpw);
+                    const int64_t r0 = a0 + (int64_t)k * S;
+                    if (zi >= 0 && tb + r0 + zi < zero_t) zero_t = tb + r0 + zi;
+                    F = map_compose<D>(F, f);
+                    uint2* dst = reinterpret_cast<uint2*>(bpg + (size_t)r0 * BPB);
+#pragma unroll
+                    for (int w = 0; w < BPW; w += 2) dst[w / 2] = make_uint2(bpw[w], bpw[w + 1]);
+                    if (r0 + nr == T) {  // this slice ends the local sequence: x* = argmax V (smallest)
+                        int xs = 0;
+                        for (int d = D - 1; d >= 0; d--)
+                            if (V[d] == 0.0f) xs = d;
+                        flag[0] = xs;
+                    }
+                }
+                __syncwarp();
+            }
+            if (mode == HMM_MODE_VFORWARD)
+                reinterpret_cast<uint64_t*>(p.ws + p.ws_lmap)[(size_t)c * NT + tid] = F;
+        } else if (mode == HMM_MODE_VFINISH) {
+            F = __ldcg(reinterpret_cast<const unsigned long long*>(p.ws + p.ws_lmap) + (size_t)c * NT + tid);
+        }
+        HMM_STAMP(6);
+        __syncthreads();
+        // CTA map and the end state of every lane
+        uint64_t* smaps = reinterpret_cast<uint64_t*>(stage);
+        if (mode == HMM_MODE_FULL || mode == HMM_MODE_VFORWARD || mode == HMM_MODE_VFINISH) {
+            maps[NT + tid] = F;
+            __syncthreads();
+            map_tree_up<D>(maps, NT);
+        }
+        if (mode == HMM_MODE_FULL || mode == HMM_MODE_VFORWARD) {
+            if (tid == 0) {
+                *reinterpret_cast<uint64_t*>(myslot + map_off) = maps[1];
+                if (c == G - 1) *reinterpret_cast<int32_t*>(myslot + map_off + 16) = flag[0];
+            }
+            if (G > 1) group_arrive_wait(arrive2, (uint32_t)G);
+            else __syncthreads();
+        }
+        if (mode == HMM_MODE_VFORWARD) {
+            for (int i = tid; i < G; i += NT)
+                smaps[i] = __ldcg(reinterpret_cast<const unsigned long long*>(slots + (size_t)i * p.slot_bytes + map_off));
+            __syncthreads();
+            if (c == 0 && warp == 0) {
+                const uint64_t Fr = warp_compose<D>(smaps, 0, G);
+                if (lane == 0) *reinterpret_cast<uint64_t*>(p.rec_out) = Fr;
+            }
+            if (c == G - 1 && tid == 0) *reinterpret_cast<int32_t*>(p.rec_out + 8) = flag[0];
+        }
+        const bool do_path = (mode == HMM_MODE_FULL || mode == HMM_MODE_VFINISH);
+        if (do_path) {
+            int xs = flag[0];
+            if (G > 1 || mode == HMM_MODE_VFINISH) {
+                for (int i = c + 1 + tid; i < G; i += NT) {
+                    smaps[i] = __ldcg(reinterpret_cast<const unsigned long long*>(slots + (size_t)i * p.slot_bytes + map_off));
+                    if (i == G - 1) flag[3] = __ldcg(reinterpret_cast<const int*>(slots + (size_t)i * p.slot_bytes + map_off + 16));
+                }
+                if (mode == HMM_MODE_VFINISH && tid == 0) {
+                    int x = *reinterpret_cast<const int32_t*>(p.rec_all + (size_t)(p.world - 1) * 16 + 8);
+                    for (int q = p.world - 1; q > p.rank; q--)
+                        x = map_apply(*reinterpret_cast<const unsigned long long*>(p.rec_all + (size_t)q * 16), x < 0 ? 0 : x);
+                    flag[0] = x;
+                }
+                __syncthreads();
+                xs = (mode == HMM_MODE_VFINISH) ? flag[0] : ((c < G - 1) ? flag[3] : flag[0]);
+            }
+            if (warp == 0) {
+                uint64_t Fs = map_identity(D);
+                if (c < G - 1) Fs = warp_compose<D>(smaps, c + 1, G);
+                if (lane == 0) flag[1] = map_apply(Fs, xs < 0 ? 0 : xs);
+            }
+            __syncthreads();
+            map_tree_down(maps, ends, NT, flag[1]);
+            int x = ends[NT + tid];
+            HMM_STAMP(7);
+            // ===================== pass 3: backtrack right to left, one slice of backpointers ahead
+            uint32_t cur[BPW], nxt[BPW];
+            auto load_bp = [&](int k, uint32_t* w) {
+                if (k >= 0 && slice_rows(k) > 0) {
+                    const uint2* src = reinterpret_cast<const uint2*>(bpg + (size_t)(a0 + (int64_t)k * S) * BPB);
+#pragma unroll
+                    for (int i = 0; i < BPW; i += 2) {
+                        const uint2 v = __ldcs(src + i / 2);
+                        w[i] = v.x;
+                        w[i + 1] = v.y;
+                    }
+                }
+            };
+            load_bp(nsl - 1, cur);
+            for (int k = nsl - 1; k >= 0; k--) {
+                load_bp(k - 1, nxt);
+                const int nr = slice_rows(k);
+                int32_t out[S];
+                x = vit_back_slice<D, S>(cur, nr, x, out);
+                int32_t* dst = p.path + a0 + (int64_t)k * S;
+                if (nr == S) {
+#pragma unroll
+                    for (int i = 0; i < S; i += 4)
+                        __stcs(reinterpret_cast<int4*>(dst + i), make_int4(out[i], out[i + 1], out[i + 2], out[i + 3]));
+                } else {
+                    for (int i = 0; i < nr; i++) dst[i] = out[i];
+                }
+#pragma unroll
+                for (int i = 0; i < BPW; i++) cur[i] = nxt[i];
+            }
+        }
+        HMM_STAMP(8);
+    }
+
+    // ===================== scalars: log Z / log_prob, info (last CTA)
+    HMM_STAMP(9);
+    if (bad) atomicOr(bad_flag, 1u);
+    if (zero_t != INT64_MAX) atomicMax(zero_code, (1ull << 62) - (unsigned long long)zero_t);
+    const double part = block_sum<NT>(acc, red);
+    if (tid == 0) {
+        *reinterpret_cast<double*>(myslot + map_off + 8) = part;
+        __threadfence();
+        const uint32_t prev = atomicAdd(done_ctr, 1u);
+        flag[2] = (prev == (uint32_t)G - 1) ? 1 : 0;
+    }
+    __syncthreads();
+    if (flag[2]) {
+        __threadfence();
+        double v = 0.0;
+        for (int x = tid; x < G; x += NT) v += __ldcg(reinterpret_cast<const double*>(slots + (size_t)x * p.slot_bytes + map_off + 8));
+        const double tot = block_sum<NT>(v, red);
+        if (tid == 0) {
+            if (p.scalar_out) p.scalar_out[0] = tot;
+            const uint32_t badf = atomicExch(bad_flag, 0u);
+            const unsigned long long zc = atomicExch(zero_code, 0ull);
+            int32_t inf = 0;
+            if (badf) inf = -1;
+            else if (zc) inf = (int32_t)((1ull << 62) - zc + 1ull);
+            if (p.info) p.info[0] = inf;
+            atomicExch(arrive1, 0ull);
+            atomicExch(arrive2, 0ull);
+            atomicExch(done_ctr, 0u);
+        }
+    }
+    HMM_STAMP(10);
+#undef HMM_STAMP
+}
+
+// ---------------------------------------------------------------------------- host launch
+template <int D, int OP>
+static cudaError_t launch_st(unsigned G, const SParams& sp, cudaStream_t stream) {
+    auto kern = hmm_stream_kernel<D, OP>;
+    const size_t smem = sp.L.total;
+    static size_t configured = 0;
+    if (configured < smem) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        configured = smem;
+    }
+    cudaLaunchConfig_t cfg;
+    memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDim = dim3(G, 1, 1);
+    cfg.blockDim = dim3((unsigned)stream_nt(D), 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = G > 1 ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, sp);
+}
+
+template <int OP>
+static cudaError_t launch_st_op(int D, unsigned G, const SParams& sp, cudaStream_t s) {
+    switch (D) {
+        case 1: return launch_st<1, OP>(G, sp, s);
+        case 2: return launch_st<2, OP>(G, sp, s);
+        case 3: return launch_st<3, OP>(G, sp, s);
+        case 4: return launch_st<4, OP>(G, sp, s);
+        case 5: return launch_st<5, OP>(G, sp, s);
+        case 6: return launch_st<6, OP>(G, sp, s);
+        case 7: return launch_st<7, OP>(G, sp, s);
+        case 8: return launch_st<8, OP>(G, sp, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_stream(int D, int op, unsigned G, const SParams& sp, cudaStream_t s) {
+    return op == 0 ? launch_st_op<0>(D, G, sp, s) : launch_st_op<1>(D, G, sp, s);
+}
+
+}  // namespace hmm

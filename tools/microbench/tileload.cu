@@ -49,6 +49,27 @@ __global__ void ldgk_k(const float4* g, int f4_per_cta, unsigned long long* out)
   unsigned long long t1 = global_ns();
   if (threadIdx.x == 0) { out[2 * blockIdx.x] = t0; out[2 * blockIdx.x + 1] = t1; }
 }
+// every thread issues `per` bulk copies of `pb` bytes, all completing on one mbarrier per warp
+__global__ void thr_bulk_k(const float* g, int bytes_per_cta, int per, unsigned long long* out) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  __shared__ __align__(8) uint64_t bar[32];
+  const int w = threadIdx.x >> 5;
+  if (threadIdx.x == 0) { for (int i = 0; i < 32; i++) mbar_init(&bar[i], 32); fence_mbar_init(); }
+  __syncthreads();
+  unsigned long long t0 = global_ns();
+  const char* src = reinterpret_cast<const char*>(g) + (size_t)blockIdx.x * bytes_per_cta;
+  const int nc = blockDim.x * per;
+  const int pb = (bytes_per_cta / nc) & ~15;
+  mbar_arrive_expect_tx(&bar[w], pb * per);
+  for (int j = 0; j < per; j++) {
+    const int i = j * blockDim.x + threadIdx.x;  // interleaved so consecutive threads hit consecutive pieces
+    bulk_g2s(sm + (size_t)i * pb, src + (size_t)i * pb, pb, &bar[w]);
+  }
+  mbar_wait(&bar[w], 0);
+  __syncthreads();
+  unsigned long long t1 = global_ns();
+  if (threadIdx.x == 0) { out[2 * blockIdx.x] = t0; out[2 * blockIdx.x + 1] = t1; }
+}
 int main() {
   const int bytes = 108160; size_t total = (size_t)bytes * 148;
   float* g; cudaMalloc(&g, total + 4096); cudaMemset(g, 0, total);
@@ -78,6 +99,11 @@ int main() {
     char nm[64]; snprintf(nm, 64, "ldg x8 regs x %d thr", nt); report(nm);
     for (int r = 0; r < 3; r++) { cudaMemset(fl, r, 512 << 20); ldgk_k<16><<<148, nt, bytes>>>((const float4*)g, bytes / 16, d); cudaDeviceSynchronize(); }
     snprintf(nm, 64, "ldg x16 regs x %d thr", nt); report(nm);
+  }
+  cudaFuncSetAttribute(thr_bulk_k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  for (int nt : {256, 512}) for (int per : {1, 2, 4}) {
+    for (int r = 0; r < 3; r++) { cudaMemset(fl, r, 512 << 20); thr_bulk_k<<<148, nt, bytes>>>(g, bytes, per, d); cudaError_t e = cudaDeviceSynchronize(); if (e) printf("err %s\n", cudaGetErrorString(e)); }
+    char nm[64]; snprintf(nm, 64, "thr bulk %dthr x%d (%dB)", nt, per, (bytes / (nt * per)) & ~15); report(nm);
   }
   printf("%s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;

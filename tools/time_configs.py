@@ -18,6 +18,7 @@ res = {}
 cfgs = {"1_ge_T1e3": W.ge(1000, 0), "2_ge_T1e6": W.ge(1_000_000, 1), "3_dense_D64_T1e5": W.dense(64, 100_000, 3),
         "4_batch_B1024_D16_T4096": W.dense_batch(1024, 16, 4096)}
 if len(sys.argv) > 1 and sys.argv[1] == "big":
+    cfgs["ge_T1e7"] = W.ge(10_000_000, 5)
     cfgs["5_ge_T1e8_W1"] = W.ge(100_000_000, 5)
 for name, wl in cfgs.items():
     lp, la, ll = (torch.from_numpy(np.ascontiguousarray(x)).to(dev) for x in (wl.log_pi, wl.log_A, wl.log_lik))
