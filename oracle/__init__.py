@@ -43,6 +43,7 @@ def _L():
         i32, i64, p = ctypes.c_int, ctypes.c_int64, ctypes.c_void_p
         _lib.oracle_smooth.argtypes = [i32, i64, p, p, p, p, p, p, p, p]
         _lib.oracle_viterbi.argtypes = [i32, i64, p, p, p, p, p, p]
+        _lib.oracle_smooth_sampled.argtypes = [i32, i64, p, p, p, p, i64, p, p, p, p]
         _lib.oracle_max_marginals.argtypes = [i32, i64, p, p, p, p, p]
         _lib.oracle_joint_weight.argtypes = [i32, i64, p, p, p, p]
         _lib.oracle_joint_weight.restype = ctypes.c_double
@@ -69,6 +70,20 @@ def smooth(log_pi, log_A, log_lik, want_filtered=True, want_smoothed=True):
     _L().oracle_smooth(D, T, _p(log_pi), _p(log_A), _p(log_lik), _p(filt), _p(sm),
                        ctypes.byref(lz), ctypes.byref(lzb), ctypes.byref(info))
     return dict(filtered=filt, smoothed=sm, log_z=lz.value, log_z_bwd=lzb.value, info=info.value)
+
+
+def smooth_sampled(log_pi, log_A, log_lik, ts):
+    """Algorithm 1 keeping only the rows at the sample steps `ts` (O(len(ts)) memory, for full-size
+    checks).  Returns dict(ts, filtered [n,D], smoothed [n,D], log_z, info); ts sorted, unique."""
+    log_pi, log_A, log_lik = _f32(log_pi), _f32(log_A), _f32(log_lik)
+    T, D = log_lik.shape
+    ts = np.unique(np.asarray(ts, np.int64))
+    assert ts.size == 0 or (ts[0] >= 0 and ts[-1] < T)
+    filt = np.empty((ts.size, D)); sm = np.empty((ts.size, D))
+    lz = ctypes.c_double(); info = ctypes.c_int64()
+    _L().oracle_smooth_sampled(D, T, _p(log_pi), _p(log_A), _p(log_lik), _p(ts), ts.size, _p(filt), _p(sm),
+                               ctypes.byref(lz), ctypes.byref(info))
+    return dict(ts=ts, filtered=filt, smoothed=sm, log_z=lz.value, info=info.value)
 
 
 def viterbi(log_pi, log_A, log_lik):

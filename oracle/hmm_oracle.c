@@ -139,6 +139,84 @@ int oracle_smooth(int D, int64_t T, const float* log_pi, const float* log_A, con
     return 0;
 }
 
+/* Algorithm 1 again, keeping only the rows at the sorted sample steps ts[0..ns) (O(ns) memory, for
+ * checking full-size runs at sampled outputs).  Same recursions and normalisation as oracle_smooth:
+ * the forward potentials are kept at the sampled steps during the forward pass, the backward
+ * potentials during the backward pass, and Eq. 14 combines them.  filtered_s / smoothed_s are
+ * [ns*D]; log_z is the forward-pass log Z.                                                          */
+int oracle_smooth_sampled(int D, int64_t T, const float* log_pi, const float* log_A, const float* log_lik,
+                          const int64_t* ts, int64_t ns, double* filtered_s, double* smoothed_s, double* log_z,
+                          int64_t* info) {
+    *info = 0;
+    if (has_bad(log_pi, D) || has_bad(log_A, (int64_t)D * D) || has_bad(log_lik, T * D)) { *info = -1; return 0; }
+    double A[64 * 64], pi[64], a[64], an[64], b[64], bn[64], l[64];
+    if (D > 64) return 1;
+    for (int i = 0; i < D * D; i++) A[i] = exp((double)log_A[i]);
+    for (int i = 0; i < D; i++) pi[i] = exp((double)log_pi[i]);
+    double* bs = (double*)malloc(sizeof(double) * (size_t)(ns > 0 ? ns : 1) * D);
+#define LIKS(t, mx)                                                              \
+    do {                                                                         \
+        mx = -INFINITY;                                                          \
+        for (int d = 0; d < D; d++) if ((double)log_lik[(t) * D + d] > mx) mx = log_lik[(t) * D + d]; \
+        for (int d = 0; d < D; d++)                                              \
+            l[d] = (mx == -INFINITY) ? 0.0 : exp((double)log_lik[(t) * D + d] - mx); \
+    } while (0)
+    /* forward (Alg 1 lines 2-4), normalised */
+    double lz = 0.0, mx;
+    int64_t q = 0;
+    for (int64_t t = 0; t < T; t++) {
+        LIKS(t, mx);
+        if (t == 0) {
+            for (int j = 0; j < D; j++) an[j] = pi[j] * l[j];
+        } else {
+            for (int j = 0; j < D; j++) {
+                double s = 0.0;
+                for (int i = 0; i < D; i++) s += a[i] * A[i * D + j];
+                an[j] = s * l[j];
+            }
+        }
+        double c = 0.0;
+        for (int j = 0; j < D; j++) c += an[j];
+        if (!(c > 0.0)) { *info = t + 1; free(bs); *log_z = NAN; return 0; }
+        for (int j = 0; j < D; j++) a[j] = an[j] / c;
+        lz += log(c) + mx;
+        while (q < ns && ts[q] == t) {
+            for (int j = 0; j < D; j++) filtered_s[q * D + j] = a[j];
+            q++;
+        }
+    }
+    *log_z = lz;
+    /* backward (Alg 1 lines 7-9), normalised like oracle_smooth */
+    for (int d = 0; d < D; d++) b[d] = 1.0;
+    q = ns - 1;
+    for (int64_t t = T - 1; t >= 0; t--) {
+        if (t < T - 1) {
+            LIKS(t + 1, mx);
+            double s = 0.0;
+            for (int i = 0; i < D; i++) {
+                double acc = 0.0;
+                for (int j = 0; j < D; j++) acc += A[i * D + j] * l[j] * b[j];
+                bn[i] = acc;
+                s += acc;
+            }
+            for (int i = 0; i < D; i++) b[i] = bn[i] / s;
+        }
+        while (q >= 0 && ts[q] == t) {
+            for (int j = 0; j < D; j++) bs[q * D + j] = b[j];
+            q--;
+        }
+    }
+    /* Eq. 14 at the sampled steps */
+    for (int64_t k = 0; k < ns; k++) {
+        double z = 0.0;
+        for (int d = 0; d < D; d++) z += filtered_s[k * D + d] * bs[k * D + d];
+        for (int d = 0; d < D; d++) smoothed_s[k * D + d] = filtered_s[k * D + d] * bs[k * D + d] / z;
+    }
+#undef LIKS
+    free(bs);
+    return 0;
+}
+
 /* Algorithm 4 in the log domain.  path[T] int32, log_prob = max_x V_T(x). */
 int oracle_viterbi(int D, int64_t T, const float* log_pi, const float* log_A, const float* log_lik,
                    int32_t* path, double* log_prob, int64_t* info) {

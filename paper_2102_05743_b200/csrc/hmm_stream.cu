@@ -318,6 +318,7 @@ __global__ void __launch_bounds__(stream_nt(D)) hmm_stream_kernel(const SParams 
     constexpr int QB = stream_qb(D);
     constexpr int BPW = st_bpw<D>(S);     // backpointer words per slice
     constexpr int BPB = small_bpb(D);     // backpointer bytes per step
+    constexpr int NCB = S * BPB / 8;      // 8-B chunks of one lane's backpointer slice
     constexpr bool MP = (OP == 1);
     constexpr int NN = 2 * NT;
     extern __shared__ __align__(128) uint8_t smem[];
@@ -745,14 +746,27 @@ __global__ void __launch_bounds__(stream_nt(D)) hmm_stream_kernel(const SParams 
                     const int64_t r0 = a0 + (int64_t)k * S;
                     if (zi >= 0 && tb + r0 + zi < zero_t) zero_t = tb + r0 + zi;
                     F = map_compose<D>(F, f);
-                    uint2* dst = reinterpret_cast<uint2*>(bpg + (size_t)r0 * BPB);
+                    // the slice's rows are consumed: its slot now stages the backpointer words
+                    uint2* sb = reinterpret_cast<uint2*>(slot(st));
 #pragma unroll
-                    for (int w = 0; w < BPW; w += 2) dst[w / 2] = make_uint2(bpw[w], bpw[w + 1]);
+                    for (int w = 0; w < BPW; w += 2) sb[w / 2] = make_uint2(bpw[w], bpw[w + 1]);
                     if (r0 + nr == T) {  // this slice ends the local sequence: x* = argmax V (smallest)
                         int xs = 0;
                         for (int d = D - 1; d >= 0; d--)
                             if (V[d] == 0.0f) xs = d;
                         flag[0] = xs;
+                    }
+                }
+                __syncwarp();
+                // warp-cooperative store of the 32 lanes' backpointer slices (8-B chunks, coalesced)
+                {
+                    const uint8_t* sbase = stage_base(st) + (size_t)warp * 32 * PITCH;
+#pragma unroll
+                    for (int it = 0; it < NCB; it++) {
+                        const int q = lane + 32 * it, j = q / NCB, ch = q - j * NCB;
+                        if (lane_rows(j, k) > 0)
+                            *reinterpret_cast<uint2*>(bpg + (size_t)(wbase + (int64_t)j * n + (int64_t)k * S) * BPB + ch * 8) =
+                                *reinterpret_cast<const uint2*>(sbase + (size_t)j * PITCH + ch * 8);
                     }
                 }
                 __syncwarp();
@@ -815,35 +829,69 @@ __global__ void __launch_bounds__(stream_nt(D)) hmm_stream_kernel(const SParams 
             map_tree_down(maps, ends, NT, flag[1]);
             int x = ends[NT + tid];
             HMM_STAMP(7);
-            // ===================== pass 3: backtrack right to left, one slice of backpointers ahead
-            uint32_t cur[BPW], nxt[BPW];
-            auto load_bp = [&](int k, uint32_t* w) {
-                if (k >= 0 && slice_rows(k) > 0) {
-                    const uint2* src = reinterpret_cast<const uint2*>(bpg + (size_t)(a0 + (int64_t)k * S) * BPB);
+            // ===================== pass 3: backtrack right to left.  The warps' backpointer slices
+            // stream through a deep ring of dense 8-B-chunk stages (cp.async, NSB-1 slices ahead); the
+            // path slice of every lane is staged in SMEM and leaves by coalesced 16-B stores.
+            __syncthreads();  // the map trees above live in the ring region
+            constexpr int BPS = S * BPB;                       // backpointer bytes per lane slice
+            constexpr int PPITCH = S * 4 + 16;                 // path slot pitch
+            constexpr int NSB_CAP = (3 * PITCH - PPITCH) / BPS;   // stages that fit in the ring region
+            constexpr int NSB_BW = 98304 / (NT * BPS);             // ~96 KB of backpointers in flight
+            constexpr int NSB0 = NSB_BW < NSB_CAP ? NSB_BW : NSB_CAP;
+            constexpr int NSB = NSB0 < 2 ? 2 : (NSB0 > 16 ? 16 : NSB0);
+            static_assert(NSB * BPS + PPITCH <= 3 * PITCH, "pass-3 staging exceeds the ring");
+            uint8_t* bring = ring;                              // [NSB][NT][BPS]
+            uint8_t* pbuf = ring + (size_t)NSB * NT * BPS;      // [NT][PPITCH]
+            auto bp_load = [&](int k, int sb) {
+                uint8_t* sbase = bring + ((size_t)sb * NT + warp * 32) * BPS;
+#pragma unroll
+                for (int it = 0; it < NCB; it++) {
+                    const int q = lane + 32 * it, j = q / NCB, ch = q - j * NCB;
+                    const bool ok = k >= 0 && lane_rows(j, k) > 0;
+                    const uint8_t* src = ok ? bpg + (size_t)(wbase + (int64_t)j * n + (int64_t)k * S) * BPB + ch * 8 : bpg;
+                    cp_async8_zfill(sbase + (size_t)j * BPS + ch * 8, src, ok ? 8u : 0u);
+                }
+                cp_async_commit();
+            };
+#pragma unroll 1
+            for (int i = 0; i < NSB - 1; i++) bp_load(K - 1 - i, i % NSB);
+            for (int it = 0; it < K; it++) {
+                const int k = K - 1 - it;
+                bp_load(k - (NSB - 1), (it + NSB - 1) % NSB);
+                cp_async_wait<NSB - 1>();
+                __syncwarp();
+                const int nr = slice_rows(k);
+                int32_t* ps = reinterpret_cast<int32_t*>(pbuf + (size_t)tid * PPITCH);
+                if (nr > 0) {
+                    uint32_t cur[BPW];
+                    const uint2* bs = reinterpret_cast<const uint2*>(bring + ((size_t)(it % NSB) * NT + tid) * BPS);
 #pragma unroll
                     for (int i = 0; i < BPW; i += 2) {
-                        const uint2 v = __ldcs(src + i / 2);
-                        w[i] = v.x;
-                        w[i + 1] = v.y;
+                        const uint2 v = bs[i / 2];
+                        cur[i] = v.x;
+                        cur[i + 1] = v.y;
                     }
-                }
-            };
-            load_bp(nsl - 1, cur);
-            for (int k = nsl - 1; k >= 0; k--) {
-                load_bp(k - 1, nxt);
-                const int nr = slice_rows(k);
-                int32_t out[S];
-                x = vit_back_slice<D, S>(cur, nr, x, out);
-                int32_t* dst = p.path + a0 + (int64_t)k * S;
-                if (nr == S) {
+                    int32_t out[S];
+                    x = vit_back_slice<D, S>(cur, nr, x, out);
 #pragma unroll
                     for (int i = 0; i < S; i += 4)
-                        __stcs(reinterpret_cast<int4*>(dst + i), make_int4(out[i], out[i + 1], out[i + 2], out[i + 3]));
-                } else {
-                    for (int i = 0; i < nr; i++) dst[i] = out[i];
+                        *reinterpret_cast<int4*>(ps + i) = make_int4(out[i], out[i + 1], out[i + 2], out[i + 3]);
                 }
+                __syncwarp();
+                // coalesced path stores: 16-B chunks, the sequence's last chunk word by word
 #pragma unroll
-                for (int i = 0; i < BPW; i++) cur[i] = nxt[i];
+                for (int i2 = 0; i2 < S / 4; i2++) {
+                    const int q = lane + 32 * i2, j = q / (S / 4), ch = q - j * (S / 4);
+                    const int nrj = lane_rows(j, k);
+                    const int32_t* src = reinterpret_cast<const int32_t*>(pbuf + (size_t)(warp * 32 + j) * PPITCH) + 4 * ch;
+                    int32_t* dst = p.path + wbase + (int64_t)j * n + (int64_t)k * S + 4 * ch;
+                    if (4 * ch + 4 <= nrj) {
+                        __stcs(reinterpret_cast<int4*>(dst), *reinterpret_cast<const int4*>(src));
+                    } else {
+                        for (int w = 4 * ch; w < nrj; w++) dst[w - 4 * ch] = src[w - 4 * ch];
+                    }
+                }
+                __syncwarp();
             }
         }
         HMM_STAMP(8);

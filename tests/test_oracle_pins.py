@@ -289,3 +289,23 @@ def test_batched_oracle_matches_single():
         assert sb["log_z"][b] == s["log_z"]
         v = oracle.viterbi(wl.log_pi, wl.log_A, wl.log_lik[b])
         np.testing.assert_array_equal(vb["path"][b], v["path"])
+
+
+# ---------------------------------------------------------------- sampled smoother (full-size checks)
+@pytest.mark.parametrize("D,T", [(4, 5000), (3, 777), (1, 50), (8, 2000)])
+def test_smooth_sampled_matches_full_oracle(D, T):
+    """oracle.smooth_sampled is Algorithm 1 with O(samples) memory: at every sampled step it must give
+    the same numbers as the full oracle (same recursions, same operation order -> bitwise equal)."""
+    wl = W.ge(T, seed=3) if D == 4 else W.dense(D, T, seed=D)
+    full = oracle.smooth(wl.log_pi, wl.log_A, wl.log_lik)
+    ts = np.unique(np.r_[0, T - 1, np.random.default_rng(D).integers(0, T, 40)])
+    s = oracle.smooth_sampled(wl.log_pi, wl.log_A, wl.log_lik, ts)
+    assert s["info"] == 0 and s["log_z"] == full["log_z"]
+    assert np.array_equal(s["filtered"], full["filtered"][ts])
+    assert np.array_equal(s["smoothed"], full["smoothed"][ts])
+
+
+def test_smooth_sampled_info():
+    wl = W.ge(3000, seed=4)
+    wl.log_lik[1234, :] = -np.inf
+    assert oracle.smooth_sampled(wl.log_pi, wl.log_A, wl.log_lik, [5, 10])["info"] == 1235
