@@ -3,12 +3,14 @@
 
 A "step" is one pass of the whole hot path over one batch of synthetic input: the parallel
 sum-product smoother (filtered + smoothed marginals + log Z, hmm_smooth) followed by the parallel
-max-product MAP path (hmm_viterbi) on the same sequence.  Default workload = BASELINE.json configs[1]:
-Gilbert-Elliott channel HMM, D=4, T=1e6.
+max-product MAP path (hmm_viterbi) on the same sequence.  Default workload = BASELINE.json configs[4],
+the configuration the north-star target is quoted on: one Gilbert-Elliott channel HMM sequence
+(PAPER.md:791-836), D=4, T=1e8, partitioned along T across the N GPUs (strong scaling; N=1 runs the
+whole sequence on one B200 -- it fits: 1.6 GB in, 3.6 GB out).  `--T 1000000` gives configs[1].
 
   value   time-steps/s of the device-timed step (CUDA events on the launching stream, inputs resident
-          in HBM, L2 flushed between timed steps), summed over ranks (weak scaling: each rank owns an
-          independent GE sequence; no data-path collective in this workload).
+          in HBM, L2 flushed between timed steps); N>1: the split-phase smoother + Viterbi with their
+          NCCL all-gathers (the method's one exchange step), total T / max-over-ranks step time.
   e2e     the same metric through the public Python API with pinned HOST buffers: H2D of log_lik,
           smooth + viterbi, D2H of log Z / log_prob / info, every step.
   roofline  the dominant kernel vs the measured HBM copy peak (MEASURED_PEAKS.json), plus the Viterbi
@@ -117,7 +119,8 @@ class ClockSampler:
 def make_workload(args, rank):
     import workloads as W
     if args.workload == "ge":
-        return W.ge(args.T, seed=1 + 1000 * rank), f"GE D=4 T={args.T:g} smoother+viterbi"
+        cfg = "BASELINE configs[4]" if args.T == 100_000_000 else ("BASELINE configs[1]" if args.T == 1_000_000 else "GE")
+        return W.ge(args.T, seed=5), f"{cfg}: Gilbert-Elliott D=4, T={args.T:g}, one sequence, smoother+viterbi"
     if args.workload == "dense":
         return W.dense(args.D, args.T, seed=3 + 1000 * rank), f"dense D={args.D} T={args.T:g} smoother+viterbi"
     raise SystemExit(f"unknown workload {args.workload}")
@@ -162,7 +165,7 @@ def run_reference(args):
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": desc, "D": wl.D, "T": wl.T, "B": 1},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -170,9 +173,9 @@ def run_reference(args):
 
 
 def run_multi(args, world, rank, local):
-    """N > 1: one GE sequence of world*T steps partitioned along T (rank r owns T steps); every step
+    """N > 1: one GE sequence of T steps partitioned along T (rank r owns ~T/N steps); every step
     runs the split-phase smoother and Viterbi with their NCCL all-gathers (the method's exchange step).
-    Weak scaling: per-GPU work fixed, value = world*T / max-over-ranks step time."""
+    Strong scaling: total work fixed, value = T / max-over-ranks step time."""
     import torch
     import torch.distributed as dist
     import workloads as W
@@ -185,7 +188,7 @@ def run_multi(args, world, rank, local):
         dist.init_process_group("nccl", device_id=dev)
     else:
         dist.init_process_group("gloo")
-    Tg = world * args.T
+    Tg = args.T
     wl = W.ge(Tg, seed=5)  # counter-based RNG: every rank simulates the same global chain
     t0, n = HD.partition(Tg, world, rank)
     D = wl.D
@@ -194,26 +197,31 @@ def run_multi(args, world, rank, local):
     ll = torch.from_numpy(np.ascontiguousarray(wl.log_lik[t0:t0 + n])).to(dev)
     stream = torch.cuda.current_stream(dev)
 
+    flush_w = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+
     def step():
         f, s, lz, info = HD.smooth_dist(lp, la, ll, t0)
         path, lpr, vinfo = HD.viterbi_dist(lp, la, ll, t0)
         return lz, info, lpr, vinfo
 
     for _ in range(args.warmup):
+        flush_w.zero_()
         out = step()
     torch.cuda.synchronize()
     assert int(out[1].item()) == 0 and int(out[3].item()) == 0
     e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
     dist.barrier()
     torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     with ClockSampler(dev.index) as clk:
-        e0.record(stream)
-        for _ in range(args.steps):
+        for k in range(args.steps):
+            flush_w.zero_()  # 512 MiB write: the per-rank slice does not stay in L2 between steps
+            evs[k][0].record(stream)
             step()
-        e1.record(stream)
+            evs[k][1].record(stream)
         torch.cuda.synchronize()
     dist.barrier()
-    ms = e0.elapsed_time(e1) / args.steps
+    ms = sum(a.elapsed_time(b) for a, b in evs) / args.steps
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if args.dist_backend == "nccl":
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -245,23 +253,27 @@ def run_multi(args, world, rank, local):
         tc = te.cpu(); dist.all_reduce(tc, op=dist.ReduceOp.MAX); te = tc
     ms_e2e = float(te.item())
     peaks = load_peaks()
-    ach = SMOOTH_BYTES_PER_STEP(D) * n / (ms * 1e-3) / 1e9  # per GPU, whole step (smoother + Viterbi)
+    ach = (SMOOTH_BYTES_PER_STEP(D) + VITERBI_BYTES_PER_STEP(D)) * n / (ms * 1e-3) / 1e9  # per GPU, whole step
     if rank == 0:
+        cfg = "BASELINE configs[4]: " if Tg == 100_000_000 else ""
         print(json.dumps({
             "metric": METRIC, "value": Tg / (ms * 1e-3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"GE D=4, one sequence of {world}x{args.T:g} steps T-partitioned across ranks "
-                                   f"(split-phase smoother+viterbi, NCCL all-gather of rank aggregates)",
+            "config": {"workload": f"{cfg}Gilbert-Elliott D=4, one sequence of T={Tg:g} steps partitioned along T "
+                                   f"across {world} ranks (split-phase smoother+viterbi, NCCL all-gather of rank "
+                                   f"aggregates)",
                        "D": D, "T_global": Tg, "T_per_rank": n, "B": 1, "collective": args.dist_backend,
-                       "l2": "inputs resident; per-rank slice 16 MB"},
-            "roofline": {"kernel": "whole split-phase step per GPU (smoother+viterbi)", "bound": "hbm",
+                       "l2": "flushed between timed steps (512 MiB write, outside the events)"},
+            "roofline": {"kernel": "whole split-phase step per GPU (smoother+viterbi), algorithmic bytes "
+                                   f"{SMOOTH_BYTES_PER_STEP(D) + VITERBI_BYTES_PER_STEP(D)} B/step", "bound": "hbm",
                          "achieved": ach, "peak": peaks["hbm"], "unit": "GB/s", "frac": ach / peaks["hbm"],
                          "traffic": None},
             "cpu_baseline": None,
             "e2e": {"value": Tg / (ms_e2e * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h_ll.numel() * 4),
                     "d2h_bytes_per_step": 16, "ms_per_step": ms_e2e},
             "gpu_launches": 5 * args.steps, "clocks": clk.summary(),
+            "smoother_viterbi_split": "5 library launches + 5 NCCL all-gathers per step",
         }), flush=True)
     dist.destroy_process_group()
 
@@ -269,11 +281,11 @@ def run_multi(args, world, rank, local):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="ge", choices=["ge", "dense"])
-    ap.add_argument("--T", type=int, default=1_000_000)
+    ap.add_argument("--T", type=int, default=100_000_000, help="time steps (1e8 = configs[4], 1e6 = configs[1])")
     ap.add_argument("--D", type=int, default=4)
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--ref-sample", type=int, default=100_000)
@@ -360,7 +372,7 @@ def main():
         t = torch.tensor([ms_step, ms_s, ms_v], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_step, ms_s, ms_v = [float(x) for x in t.cpu()]
-    value = world * T / (ms_step * 1e-3)
+    value = T / (ms_step * 1e-3)
 
     # ---- e2e through the public API with pinned host buffers
     e2e = None
@@ -397,7 +409,7 @@ def main():
             t = torch.tensor([ms_e2e], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms_e2e = float(t.item())
-        e2e = {"value": world * T / (ms_e2e * 1e-3), "unit": UNIT,
+        e2e = {"value": T / (ms_e2e * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": int(h_ll.numel() * 4 + h_lp.numel() * 4 + h_la.numel() * 4),
                "d2h_bytes_per_step": int(h_out.numel() * 8), "ms_per_step": ms_e2e}
 
@@ -410,11 +422,12 @@ def main():
     ach_v = vi_bytes / (ms_v * 1e-3) / 1e9
     alu_peak = 148 * 128 * peaks["sm_mhz"] * 1e6 / 1e12  # T lane-op/s
     ach_alu = VITERBI_ALU_PER_STEP(D) * T / (ms_v * 1e-3) / 1e12
-    roof_s = {"kernel": "hmm_small_kernel<4,0> (smoother)", "bound": "hbm", "achieved": ach_s,
+    kname = lambda op: ("hmm_stream_kernel" if H.plan(op, D, T)["fused"] == 2 else "hmm_small_kernel") + f"<{D},{op}>"
+    roof_s = {"kernel": kname(0) + " (smoother)", "bound": "hbm", "achieved": ach_s,
               "peak": peaks["hbm"], "unit": "GB/s", "frac": ach_s / peaks["hbm"],
               "traffic": traffic.get("smooth", {}).get("dram_bytes_per_launch"),
               "peak_source": peaks["src"], "ms_per_launch": ms_s, "algorithmic_bytes_per_launch": sm_bytes}
-    roof_v = {"kernel": "hmm_small_kernel<4,1> (viterbi)", "bound": "alu", "achieved": ach_alu,
+    roof_v = {"kernel": kname(1) + " (viterbi)", "bound": "alu", "achieved": ach_alu,
               "peak": alu_peak, "unit": "Tlane-op/s", "frac": ach_alu / alu_peak,
               "hbm_achieved_gbs": ach_v, "hbm_frac": ach_v / peaks["hbm"],
               "traffic": traffic.get("viterbi", {}).get("dram_bytes_per_launch"), "ms_per_launch": ms_v}
@@ -427,12 +440,12 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": desc, "D": D, "T": T, "B": 1, "per_rank": "independent sequence",
+            "config": {"workload": desc, "D": D, "T": T, "B": 1,
                        "l2": "flushed between timed steps (512 MiB write + 256 MiB read, outside the events)"},
-            "smoother_steps_per_s": world * T / (ms_s * 1e-3),
-            "viterbi_steps_per_s": world * T / (ms_v * 1e-3),
+            "smoother_steps_per_s": T / (ms_s * 1e-3),
+            "viterbi_steps_per_s": T / (ms_v * 1e-3),
             "roofline": dominant, "roofline_all": [roof_s, roof_v],
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": 2 * args.steps,
             "clocks": clk.summary(),

@@ -81,53 +81,130 @@ __device__ __forceinline__ void sp_back_step(const float* row, bool t0, const fl
     for (int e = 0; e < D * D; e++) P[e] = Pn[e];
     d = exp_offset(vmax_tree<D * D>(P));
 }
+// Chain start: X = psi_t = A diag(l_t) itself (no product with an identity), pending offset of max(X).
+template <int D>
+__device__ __forceinline__ void sp_chain_start(const float* row, const float* A, float* X, float& d) {
+    float v[D], l[D];
+    ld_row<D>(row, v);
+    const float m = fmaxf(vmax<D>(v), -1e30f);
+    const float c = -m * kLog2e;
+#pragma unroll
+    for (int j = 0; j < D; j++) l[j] = ex2(fmaf(v[j], kLog2e, c));
+#pragma unroll
+    for (int i = 0; i < D; i++)
+#pragma unroll
+        for (int j = 0; j < D; j++) X[i * D + j] = A[i * D + j] * l[j];
+    d = exp_offset(vmax_tree<D * D>(X));
+}
+template <int D>
+__device__ __forceinline__ void normalize_pow2(float* X) {
+    const float s = pow2_inv(vmax_tree<D * D>(X));
+#pragma unroll
+    for (int e = 0; e < D * D; e++) X[e] *= s;
+}
+// One slice, right to left.  A full slice is split into two independent halves folded as two
+// interleaved chains, X = psi_H ... psi_{S-1} and Y = psi_0 ... psi_{H-1}, combined as P <- Y (X P)
+// (associativity of Def. 3).  Starting a chain from psi itself saves exactly the products the two
+// combining matrix products cost, so the FMA count is unchanged while every step now has a second
+// independent dependency chain to overlap with (the fold is latency-bound at 8 warps/SM).
 template <int D, int S>
 __device__ __forceinline__ void sp_fold_back(const float* rows, int nr, bool t0, const float* A, const float* pi,
                                              float* P, float& d) {
     if (nr == S) {
-#pragma unroll 4
-        for (int ii = S - 1; ii >= 1; ii--) sp_back_step<D>(rows + ii * D, false, A, pi, P, d);
+        constexpr int H = S / 2;
+        float X[D * D], Y[D * D], dX, dY;
+        sp_chain_start<D>(rows + (S - 1) * D, A, X, dX);
+        sp_chain_start<D>(rows + (H - 1) * D, A, Y, dY);
+#pragma unroll 2
+        for (int q = 1; q < H - 1; q++) {
+            sp_back_step<D>(rows + (S - 1 - q) * D, false, A, pi, X, dX);
+            sp_back_step<D>(rows + (H - 1 - q) * D, false, A, pi, Y, dY);
+        }
+        sp_back_step<D>(rows + H * D, false, A, pi, X, dX);
+        sp_back_step<D>(rows, t0, A, pi, Y, dY);
+        normalize_pow2<D>(X);
+        normalize_pow2<D>(Y);
+        float XP[D * D];
+        if (d != 0.0f) normalize_pow2<D>(P);
+        mat_op<D, false>(X, P, XP);
+        mat_op<D, false>(Y, XP, P);
+        d = 0.0f;
     } else {
 #pragma unroll 1
         for (int ii = nr - 1; ii >= 1; ii--) sp_back_step<D>(rows + ii * D, false, A, pi, P, d);
+        sp_back_step<D>(rows, t0, A, pi, P, d);
     }
-    sp_back_step<D>(rows, t0, A, pi, P, d);
 }
 
-// Max-product (log domain), right to left: P(i,j) <- max_k (LA(i,k) + w_t(k) + P(k,j)), w_t = ll_t - m_t
-// (row-independent LP(k) + w_0(k) for the sequence's first step).  `chk` collects NaN evidence.
+// Max-product (log domain), one step right to left: P(i,j) <- max_k (LA(i,k) + w_t(k) + P(k,j)),
+// w_t = ll_t - m_t (row-independent LP(k) + w_0(k) for the sequence's first step).  `chk` collects
+// NaN evidence.
+template <int D>
+__device__ __forceinline__ void mp_back_step(const float* row, bool t0, const float* LA, const float* LP, float* P,
+                                             float& chk) {
+    float v[D], W[D * D];
+    ld_row<D>(row, v);
+    float m = vmax<D>(v);
+    if (!(m > neg_inf())) m = 0.0f;
+    float w[D];
+#pragma unroll
+    for (int k = 0; k < D; k++) w[k] = v[k] - m;
+    chk += vsum<D>(w);
+#pragma unroll
+    for (int k = 0; k < D; k++)
+#pragma unroll
+        for (int j = 0; j < D; j++) W[k * D + j] = w[k] + P[k * D + j];
+    float Pn[D * D];
+#pragma unroll
+    for (int i = 0; i < D; i++) {
+#pragma unroll
+        for (int j = 0; j < D; j++) {
+            float sc[D];
+#pragma unroll
+            for (int k = 0; k < D; k++) sc[k] = (t0 ? LP[k] : LA[i * D + k]) + W[k * D + j];
+            Pn[i * D + j] = vmax<D>(sc);
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < D * D; e++) P[e] = Pn[e];
+}
+template <int D>
+__device__ __forceinline__ void mp_chain_start(const float* row, const float* LA, float* X, float& chk) {
+    float v[D];
+    ld_row<D>(row, v);
+    float m = vmax<D>(v);
+    if (!(m > neg_inf())) m = 0.0f;
+    float w[D];
+#pragma unroll
+    for (int k = 0; k < D; k++) w[k] = v[k] - m;
+    chk += vsum<D>(w);
+#pragma unroll
+    for (int i = 0; i < D; i++)
+#pragma unroll
+        for (int k = 0; k < D; k++) X[i * D + k] = LA[i * D + k] + w[k];
+}
+// Max-product slice fold, two interleaved chains for full slices (as sp_fold_back, Def. 5).
 template <int D, int S>
 __device__ __forceinline__ void mp_fold_back(const float* rows, int nr, bool t0, const float* LA, const float* LP,
                                              float* P, float& chk) {
-#pragma unroll
-    for (int ii = S - 1; ii >= 0; ii--) {
-        if (ii < nr) {
-            float v[D], W[D * D];
-            ld_row<D>(rows + ii * D, v);
-            float m = vmax<D>(v);
-            if (!(m > neg_inf())) m = 0.0f;
-            float w[D];
-#pragma unroll
-            for (int k = 0; k < D; k++) w[k] = v[k] - m;
-            chk += vsum<D>(w);
-#pragma unroll
-            for (int k = 0; k < D; k++)
-#pragma unroll
-                for (int j = 0; j < D; j++) W[k * D + j] = w[k] + P[k * D + j];
-            float Pn[D * D];
-#pragma unroll
-            for (int i = 0; i < D; i++) {
-#pragma unroll
-                for (int j = 0; j < D; j++) {
-                    float sc[D];
-#pragma unroll
-                    for (int k = 0; k < D; k++) sc[k] = ((ii == 0 && t0) ? LP[k] : LA[i * D + k]) + W[k * D + j];
-                    Pn[i * D + j] = vmax<D>(sc);
-                }
-            }
-#pragma unroll
-            for (int e = 0; e < D * D; e++) P[e] = Pn[e];
+    if (nr == S) {
+        constexpr int H = S / 2;
+        float X[D * D], Y[D * D];
+        mp_chain_start<D>(rows + (S - 1) * D, LA, X, chk);
+        mp_chain_start<D>(rows + (H - 1) * D, LA, Y, chk);
+#pragma unroll 2
+        for (int q = 1; q < H - 1; q++) {
+            mp_back_step<D>(rows + (S - 1 - q) * D, false, LA, LP, X, chk);
+            mp_back_step<D>(rows + (H - 1 - q) * D, false, LA, LP, Y, chk);
         }
+        mp_back_step<D>(rows + H * D, false, LA, LP, X, chk);
+        mp_back_step<D>(rows, t0, LA, LP, Y, chk);
+        float XP[D * D];
+        mat_op<D, true>(X, P, XP);
+        mat_op<D, true>(Y, XP, P);
+    } else {
+#pragma unroll 1
+        for (int ii = nr - 1; ii >= 0; ii--) mp_back_step<D>(rows + ii * D, ii == 0 && t0, LA, LP, P, chk);
     }
 }
 

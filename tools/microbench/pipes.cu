@@ -17,6 +17,9 @@ template<int OP> __global__ void kern(float* out, float a, float b) {
       if (OP == 4) x[i] = exp2f(x[i] * a);                     // MUFU.EX2 (+FMUL)
       if (OP == 5) y[i] = __fadd2_rn(y[i], y[(i+1)&7]);         // FADD2
       if (OP == 6) x[i] = x[i] * a + b;                         // FFMA imm-ish (const operands)
+      if (OP == 7) x[i] = fmaxf(x[i], x[(i+1)&7]) - a;          // FMNMX + FADD
+      if (OP == 8) x[i] = x[i] + x[(i+1)&7];                    // FADD
+      if (OP == 9) { float r; asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(x[i]), "f"(x[(i+1)&7]), "f"(x[(i+3)&7])); x[i] = r; } // FMNMX3 only
     }
   }
   float s = 0;
@@ -43,6 +46,7 @@ template<int OP> void run(const char* name, double ops_per_inner) {
 int main() {
   run<0>("FFMA", 1); run<1>("FFMA2", 2); run<2>("FMNMX3+FADD", 2); run<3>("DFMA", 1);
   run<4>("EX2+FMUL", 2); run<5>("FADD2", 2); run<6>("FFMA-c", 1);
+  run<7>("FMNMX+FADD", 2); run<8>("FADD", 1); run<9>("FMNMX3", 1);
   cudaDeviceProp p; cudaGetDeviceProperties(&p, 0);
   printf("SMs %d smemPerBlockOptin %zu smemPerSM %zu L2 %d regsPerSM %d clock %d kHz memclk %d kHz busw %d\n",
          p.multiProcessorCount, p.sharedMemPerBlockOptin, p.sharedMemPerMultiprocessor, p.l2CacheSize,
