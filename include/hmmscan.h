@@ -163,10 +163,11 @@ hmm_status_t hmm_viterbi_dist_finish(int D, int64_t T_local, int64_t t_base, con
  *     CTA; lane-streaming plan: steps per lane), S (steps per leaf / slice), chunk, K (chunks per CTA /
  *     slices per lane), kind (1 fused, 0 chunked, 2 lane-streaming), dynamic smem bytes, threads per
  *     CTA.  Returns 0 if unsupported.
- *   hmm_debug_force_path: for calls made later from the calling host thread with 1 <= D <= 8 and
- *     B == 1, select the decomposition: 0 automatic (default), 1 lane-streaming (16-B aligned
- *     buffers required, else automatic), 2 resident/chunked.  Test and profiling use only; the
- *     results agree within the stated tolerances whichever path runs.
+ *   hmm_debug_force_path: for calls made later from the calling host thread, select the
+ *     decomposition: 0 automatic (default); for 1 <= D <= 8 and B == 1: 1 lane-streaming (16-B
+ *     aligned buffers required, else automatic), 2 resident/chunked; for 33 <= D <= 64: 3 keeps the
+ *     sum-product leaf products on the FP32 CUDA cores instead of the tensor cores.  Test and
+ *     profiling use only; the results agree within the stated tolerances whichever path runs.
  */
 void hmm_debug_set_timers(unsigned long long* device_buf);
 int hmm_debug_plan(int op, int D, int64_t T, int64_t B, int64_t* out);

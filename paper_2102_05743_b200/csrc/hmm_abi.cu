@@ -131,6 +131,8 @@ bool make_plan(int D, int op, int64_t T, int64_t B, Plan& P, bool chunked = fals
     return true;
 }
 
+thread_local int t_force_path = 0;  // hmm_debug_force_path
+
 // Lane-streaming plan (hmm_stream.cu): G CTAs of NT lanes, n steps per lane (a multiple of the slice
 // length S), K = n / S slices per lane.
 struct StPlan {
@@ -173,8 +175,6 @@ bool make_stream_plan(int D, int op, int64_t T, StPlan& P) {
 
 // Long single sequences whose CTA ranges do not fit in shared memory take the streaming kernel
 // (as do all split-phase calls); it needs 16-B aligned sequence buffers for its bulk copies.
-thread_local int t_force_path = 0;  // hmm_debug_force_path
-
 bool use_stream(int D, int64_t T, int64_t B, bool dist) {
     if (D > 8 || B != 1) return false;
     if (t_force_path == 1) return true;
@@ -192,20 +192,23 @@ thread_local unsigned long long* t_timers = nullptr;
 // Large-D plan (9 <= D <= 64): DP = padded state count; leaves of SL steps, NLB leaves per CTA.
 struct LgPlan {
     int DP = 0;
+    bool tc = false;  // sum-product leaf products on the tensor cores (DP = 64)
     int64_t SL = 0, NL = 0, NB = 0;
-    size_t o_sync, o_leaf, o_groot, o_bpre, o_bsuf, o_part, o_bp, o_lmap, o_bmap, o_bend, o_xstar, total;
+    size_t o_sync, o_leaf, o_groot, o_bpre, o_bsuf, o_part, o_bp, o_lmap, o_bmap, o_bend, o_xstar, o_lik, total;
 };
 
-bool make_large_plan(int D, int op, int64_t T, int64_t B, LgPlan& P) {
+bool make_large_plan(int D, int op, int64_t T, int64_t B, LgPlan& P, bool allow_tc = true) {
     DevInfo di;
     if (!dev_info(di)) return false;
     P.DP = D <= 16 ? 16 : (D <= 32 ? 32 : 64);
     const int NLB = hmm::large_leaves_per_block(P.DP);
-    // enough leaves for ~2 waves of 8-warp CTAs, leaves between 16 and 512 steps
-    const int64_t target = (int64_t)di.sms * 2 * NLB;
+    P.tc = (P.DP == 64 && op == 0 && t_force_path != 3 && allow_tc);
+    // enough leaves for ~2 waves of 8-warp CTAs, leaves between 16 and 512 steps; the tensor-core
+    // leaf kernel runs 2 leaf pairs per SM, so it wants ~4 leaves per SM
+    const int64_t target = P.tc ? (int64_t)di.sms * 4 : (int64_t)di.sms * 2 * NLB;
     int64_t SL = cdiv(T * B, target);
     if (SL < 16) SL = 16;
-    if (SL > 512) SL = 512;
+    if (SL > (P.tc ? 2048 : 512)) SL = P.tc ? 2048 : 512;
     if (SL > T) SL = T;
     P.SL = SL;
     P.NL = cdiv(T, SL);
@@ -224,6 +227,7 @@ bool make_large_plan(int D, int op, int64_t T, int64_t B, LgPlan& P) {
     P.o_bmap = take(op == 1 ? (size_t)B * P.NB * P.DP : 0);
     P.o_bend = take(op == 1 ? (size_t)B * P.NB * 4 : 0);
     P.o_xstar = take((size_t)B * 4);
+    P.o_lik = take(P.tc ? (size_t)B * T * 64 * 4 : 0);
     P.total = off;
     return true;
 }
@@ -272,6 +276,8 @@ hmm_status_t run(int op, int D, int64_t T, int64_t B, const float* log_pi, const
         lp.bmap = w + G.o_bmap;
         lp.bend = reinterpret_cast<int32_t*>(w + G.o_bend);
         lp.xstar = reinterpret_cast<int32_t*>(w + G.o_xstar);
+        lp.tc = G.tc ? 1 : 0;
+        lp.lik = reinterpret_cast<float*>(w + G.o_lik);
         cudaError_t e = hmm::launch_large(G.DP, op, lp, static_cast<cudaStream_t>(stream));
         return e == cudaSuccess ? HMM_SUCCESS : HMM_ERR_CUDA;
     }
@@ -350,7 +356,7 @@ const char* hmm_version(void) { return "hmmscan 0.1 sm_100a"; }
 
 void hmm_debug_set_timers(unsigned long long* device_buf) { t_timers = device_buf; }
 
-void hmm_debug_force_path(int path) { t_force_path = (path >= 0 && path <= 2) ? path : 0; }
+void hmm_debug_force_path(int path) { t_force_path = (path >= 0 && path <= 3) ? path : 0; }
 
 int hmm_debug_plan(int op, int D, int64_t T, int64_t B, int64_t* out /*[8]*/) {
     StPlan SP;
@@ -368,10 +374,10 @@ int hmm_debug_plan(int op, int D, int64_t T, int64_t B, int64_t* out /*[8]*/) {
 
 size_t hmm_workspace_size(int op, int D, int64_t T, int64_t B) {
     if ((op != 0 && op != 1) || D < 1 || D > HMM_MAX_D || T < 1 || B < 1) return 0;
-    if (D > 8) {
-        LgPlan G;
-        if (!make_large_plan(D, op, T, B, G)) return 0;
-        return G.total;
+    if (D > 8) {  // either leaf-product engine may run (hmm_debug_force_path): size for both
+        LgPlan G, H2;
+        if (!make_large_plan(D, op, T, B, G, true) || !make_large_plan(D, op, T, B, H2, false)) return 0;
+        return G.total > H2.total ? G.total : H2.total;
     }
     Plan P;
     if (!make_plan(D, op, T, B, P)) return 0;

@@ -25,6 +25,8 @@
 
 namespace hmm {
 
+cudaError_t launch_large_tc_leaf(const LgParams& p, float* lik, cudaStream_t s);
+
 template <int DP>
 struct LG {
     static constexpr int CPL = DP >= 32 ? DP / 32 : 1;  // columns (or rows) per lane
@@ -145,130 +147,141 @@ __global__ void __launch_bounds__(256) lg_leaf_kernel(const LgParams p) {
 #pragma unroll
     for (int o = LPL; o < 32; o <<= 1) nmax = max(nmax, __shfl_xor_sync(0xffffffffu, nmax, o));
 
-    float Acol[CPL][DP], pv[CPL];
-#pragma unroll
-    for (int c = 0; c < CPL; c++) {
-        const int j = cl * CPL + c;
-#pragma unroll
-        for (int k = 0; k < DP; k++) Acol[c][k] = lg_A(p, k, j, MP);
-        pv[c] = lg_pi(p, j, MP);
-    }
-    const float* ll = p.log_lik + (size_t)b * T * p.D;
-    bool bad = false;
-    float s = MP ? 0.0f : 1.0f;  // pending normalisation (scale / offset) from the previous step
-    float chk = 0.0f;
-    for (int i = 0; i < nmax; i++) {
-        const bool act = i < n;
-        const int64_t t = t0 + i;
-        float v[CPL], l[CPL];
-#pragma unroll
+    if (MP || !p.tc) {
+        float Acol[CPL][DP], pv[CPL];
+    #pragma unroll
         for (int c = 0; c < CPL; c++) {
             const int j = cl * CPL + c;
-            v[c] = (act && j < p.D) ? __ldg(ll + t * p.D + j) : neg_inf();
+    #pragma unroll
+            for (int k = 0; k < DP; k++) Acol[c][k] = lg_A(p, k, j, MP);
+            pv[c] = lg_pi(p, j, MP);
         }
-        float m = v[0];
-#pragma unroll
-        for (int c = 1; c < CPL; c++) m = fmaxf(m, v[c]);
-        m = grp_max<LPL>(m);
-        if (!(m > neg_inf())) m = 0.0f;
-#pragma unroll
-        for (int c = 0; c < CPL; c++) {
-            if constexpr (MP) {
-                l[c] = v[c] - m;
-                chk += l[c];
+        const float* ll = p.log_lik + (size_t)b * T * p.D;
+        bool bad = false;
+        float s = MP ? 0.0f : 1.0f;  // pending normalisation (scale / offset) from the previous step
+        float chk = 0.0f;
+        for (int i = 0; i < nmax; i++) {
+            const bool act = i < n;
+            const int64_t t = t0 + i;
+            float v[CPL], l[CPL];
+    #pragma unroll
+            for (int c = 0; c < CPL; c++) {
+                const int j = cl * CPL + c;
+                v[c] = (act && j < p.D) ? __ldg(ll + t * p.D + j) : neg_inf();
+            }
+            float m = v[0];
+    #pragma unroll
+            for (int c = 1; c < CPL; c++) m = fmaxf(m, v[c]);
+            m = grp_max<LPL>(m);
+            if (!(m > neg_inf())) m = 0.0f;
+    #pragma unroll
+            for (int c = 0; c < CPL; c++) {
+                if constexpr (MP) {
+                    l[c] = v[c] - m;
+                    chk += l[c];
+                } else {
+                    l[c] = ex2((v[c] - m) * kLog2e);
+                }
+            }
+            if (i == 0) {
+                if (act) {
+    #pragma unroll
+                    for (int r = 0; r < DP; r++)
+    #pragma unroll
+                        for (int c = 0; c < CPL; c++) {
+                            const float a = (t == 0) ? pv[c] : Acol[c][r];
+                            Pm[r * DP + cl * CPL + c] = MP ? a + l[c] : a * l[c];
+                        }
+                }
+                __syncwarp();
             } else {
-                l[c] = ex2((v[c] - m) * kLog2e);
-            }
-        }
-        if (i == 0) {
-            if (act) {
-#pragma unroll
-                for (int r = 0; r < DP; r++)
-#pragma unroll
-                    for (int c = 0; c < CPL; c++) {
-                        const float a = (t == 0) ? pv[c] : Acol[c][r];
-                        Pm[r * DP + cl * CPL + c] = MP ? a + l[c] : a * l[c];
-                    }
-            }
-            __syncwarp();
-        } else {
-            float mx = MP ? neg_inf() : 0.0f;
-            for (int r = 0; r < DP; r++) {
-                float acc[CPL];
-#pragma unroll
-                for (int c = 0; c < CPL; c++) acc[c] = MP ? neg_inf() : 0.0f;
-#pragma unroll
-                for (int k4 = 0; k4 < DP; k4 += 4) {
-                    const float4 x = *reinterpret_cast<const float4*>(Pm + r * DP + k4);
-#pragma unroll
-                    for (int c = 0; c < CPL; c++) {
-                        if constexpr (MP) {
-                            acc[c] = fmaxf(acc[c], max3(x.x + Acol[c][k4], x.y + Acol[c][k4 + 1],
-                                                        fmaxf(x.z + Acol[c][k4 + 2], x.w + Acol[c][k4 + 3])));
-                        } else {
-                            acc[c] = fmaf(x.x, Acol[c][k4], acc[c]);
-                            acc[c] = fmaf(x.y, Acol[c][k4 + 1], acc[c]);
-                            acc[c] = fmaf(x.z, Acol[c][k4 + 2], acc[c]);
-                            acc[c] = fmaf(x.w, Acol[c][k4 + 3], acc[c]);
+                float mx = MP ? neg_inf() : 0.0f;
+                for (int r = 0; r < DP; r++) {
+                    float acc[CPL];
+    #pragma unroll
+                    for (int c = 0; c < CPL; c++) acc[c] = MP ? neg_inf() : 0.0f;
+    #pragma unroll
+                    for (int k4 = 0; k4 < DP; k4 += 4) {
+                        const float4 x = *reinterpret_cast<const float4*>(Pm + r * DP + k4);
+    #pragma unroll
+                        for (int c = 0; c < CPL; c++) {
+                            if constexpr (MP) {
+                                acc[c] = fmaxf(acc[c], max3(x.x + Acol[c][k4], x.y + Acol[c][k4 + 1],
+                                                            fmaxf(x.z + Acol[c][k4 + 2], x.w + Acol[c][k4 + 3])));
+                            } else {
+                                acc[c] = fmaf(x.x, Acol[c][k4], acc[c]);
+                                acc[c] = fmaf(x.y, Acol[c][k4 + 1], acc[c]);
+                                acc[c] = fmaf(x.z, Acol[c][k4 + 2], acc[c]);
+                                acc[c] = fmaf(x.w, Acol[c][k4 + 3], acc[c]);
+                            }
                         }
                     }
-                }
-                __syncwarp();
-                if (act) {
-#pragma unroll
-                    for (int c = 0; c < CPL; c++) {
-                        const float val = MP ? acc[c] + (l[c] - s) : acc[c] * (l[c] * s);
-                        Pm[r * DP + cl * CPL + c] = val;
-                        mx = fmaxf(mx, val);
+                    __syncwarp();
+                    if (act) {
+    #pragma unroll
+                        for (int c = 0; c < CPL; c++) {
+                            const float val = MP ? acc[c] + (l[c] - s) : acc[c] * (l[c] * s);
+                            Pm[r * DP + cl * CPL + c] = val;
+                            mx = fmaxf(mx, val);
+                        }
                     }
+                    __syncwarp();
                 }
-                __syncwarp();
-            }
-            mx = grp_max<LPL>(mx);
-            if constexpr (MP) {
-                s = (mx > neg_inf()) ? mx : 0.0f;
-            } else {
-                s = pow2_inv(mx);
+                mx = grp_max<LPL>(mx);
+                if constexpr (MP) {
+                    s = (mx > neg_inf()) ? mx : 0.0f;
+                } else {
+                    s = pow2_inv(mx);
+                }
             }
         }
-    }
-    // final normalisation and NaN check, then write the leaf aggregate (reductions warp-uniform: the
-    // two half-warp leaves of DP = 16 may differ in length)
-    float mx = MP ? neg_inf() : 0.0f;
-    float sum = 0.0f;
-    if (n > 0) {
-        for (int r = 0; r < DP; r++)
-#pragma unroll
-            for (int c = 0; c < CPL; c++) {
-                mx = fmaxf(mx, Pm[r * DP + cl * CPL + c]);
-                sum += Pm[r * DP + cl * CPL + c];
-            }
-    }
-    mx = grp_max<LPL>(mx);
-    if (n > 0) {
-        if constexpr (!MP) bad |= (sum != sum);
-        float* dst = p.leafagg + ((size_t)b * p.NL + L) * DP * DP;
-        for (int r = 0; r < DP; r++)
-#pragma unroll
-            for (int c = 0; c < CPL; c++) {
-                float& x = Pm[r * DP + cl * CPL + c];
-                if constexpr (MP) {
-                    if (mx > neg_inf()) x -= mx;
-                } else {
-                    x *= pow2_inv(mx);
+        // final normalisation and NaN check, then write the leaf aggregate (reductions warp-uniform: the
+        // two half-warp leaves of DP = 16 may differ in length)
+        float mx = MP ? neg_inf() : 0.0f;
+        float sum = 0.0f;
+        if (n > 0) {
+            for (int r = 0; r < DP; r++)
+    #pragma unroll
+                for (int c = 0; c < CPL; c++) {
+                    mx = fmaxf(mx, Pm[r * DP + cl * CPL + c]);
+                    sum += Pm[r * DP + cl * CPL + c];
                 }
-                dst[r * DP + cl * CPL + c] = x;
-            }
+        }
+        mx = grp_max<LPL>(mx);
+        if (n > 0) {
+            if constexpr (!MP) bad |= (sum != sum);
+            float* dst = p.leafagg + ((size_t)b * p.NL + L) * DP * DP;
+            for (int r = 0; r < DP; r++)
+    #pragma unroll
+                for (int c = 0; c < CPL; c++) {
+                    float& x = Pm[r * DP + cl * CPL + c];
+                    if constexpr (MP) {
+                        if (mx > neg_inf()) x -= mx;
+                    } else {
+                        x *= pow2_inv(mx);
+                    }
+                    dst[r * DP + cl * CPL + c] = x;
+                }
+        } else {
+            for (int r = 0; r < DP; r++)
+    #pragma unroll
+                for (int c = 0; c < CPL; c++) {
+                    const int j = cl * CPL + c;
+                    Pm[r * DP + j] = (r == j) ? (MP ? 0.0f : 1.0f) : lg_pad(MP);
+                }
+        }
+        if constexpr (MP) bad |= (chk != chk);
+        if (bad) atomicOr(reinterpret_cast<uint32_t*>(p.ws_sync + b * 64) + 8, 1u);
     } else {
+        // leaf products computed by the tensor-core kernel (hmm_large_tc.cu): load them for the tree
+        const float* srcm = p.leafagg + ((size_t)b * p.NL + L) * DP * DP;
         for (int r = 0; r < DP; r++)
 #pragma unroll
             for (int c = 0; c < CPL; c++) {
                 const int j = cl * CPL + c;
-                Pm[r * DP + j] = (r == j) ? (MP ? 0.0f : 1.0f) : lg_pad(MP);
+                Pm[r * DP + j] = (L < p.NL) ? __ldcg(srcm + r * DP + j) : ((r == j) ? 1.0f : 0.0f);
             }
     }
-    if constexpr (MP) bad |= (chk != chk);
-    if (bad) atomicOr(reinterpret_cast<uint32_t*>(p.ws_sync + b * 64) + 8, 1u);
     __syncthreads();
 
     // block root: ordered tree over the NLB leaf buffers (products by leaf lane-groups)
@@ -296,7 +309,8 @@ __global__ void __launch_bounds__(256) lg_leaf_kernel(const LgParams p) {
 }
 
 // ------------------------------------------------------------------------------------------- K2
-// Vector chains through NB block roots (one warp each).  Lane owns output columns / rows.
+// Vector chains through a few matrices (one warp each; the leaf carries inside a block, K3).  Lane
+// owns output columns / rows.
 template <int DP, bool MP>
 __device__ void lg_chain_fwd(const float* mats, int64_t nm, const float* v0, float* out /*[nm][DP]*/, float* vs) {
     constexpr int Q = DP >= 32 ? DP / 32 : 1;
@@ -365,19 +379,76 @@ __device__ void lg_chain_bwd(const float* mats, int64_t nm, const float* w0, flo
     }
 }
 
+// Vector chains through the NB block roots of a sequence (the carries of Thms 1-2 / Props 2-3 at
+// block granularity): grid (B, 2) -- y = 0 forward (v <- v (op) R_i), y = 1 backward (w <- R_i w,
+// sum-product only).  The chain is serial, so the roots stream through an NS-deep cp.async ring
+// (16-B chunks XOR-swizzled by row: both the column reads of the forward step and the row reads of
+// the backward step are bank-conflict-free) and every step is pure SMEM math on 64 threads.
 template <int DP, int OP>
 __global__ void __launch_bounds__(64) lg_carry_kernel(const LgParams p) {
     constexpr bool MP = (OP == 1);
-    __shared__ float v0[DP], vs[2][DP];
+    constexpr int NS = 6;                 // ring depth (roots in flight)
+    constexpr int CH = DP / 4;            // 16-B chunks per row
+    extern __shared__ __align__(16) float ring[];  // [NS][DP*DP]
+    __shared__ float vec[DP];
+    __shared__ float red[2];
     const int64_t b = blockIdx.x;
-    const int warp = threadIdx.x >> 5;
-    const float* roots = p.groot + (size_t)b * p.NB * DP * DP;
-    for (int j = threadIdx.x; j < DP; j += blockDim.x) v0[j] = (MP ? 0.0f : 1.0f);
+    const bool fwd = blockIdx.y == 0;
+    if (!fwd && MP) return;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int64_t NB = p.NB;
+    const float* roots = p.groot + (size_t)b * NB * DP * DP;
+    float* out = (fwd ? p.bpre : p.bsuf) + (size_t)b * NB * DP;
+    auto sw = [&](int r, int c) -> int { return r * DP + ((c ^ (r & (CH - 1))) << 2); };  // chunk c of row r
+    auto load = [&](int64_t i, int st) {
+        if (i >= 0 && i < NB) {
+            const float* src = roots + (size_t)i * DP * DP;
+            float* dst = ring + (size_t)st * DP * DP;
+            for (int q = tid; q < DP * CH; q += 64) {
+                const int r = q / CH, c = q % CH;
+                cp_async16(dst + sw(r, c), src + r * DP + 4 * c);
+            }
+        }
+        cp_async_commit();
+    };
+    for (int j = tid; j < DP; j += 64) vec[j] = MP ? 0.0f : 1.0f;
+    for (int s = 0; s < NS - 1; s++) load(fwd ? s : NB - 1 - s, s);
     __syncthreads();
-    if (warp == 0) {
-        lg_chain_fwd<DP, MP>(roots, p.NB, v0, p.bpre + (size_t)b * p.NB * DP, vs[0]);
-    } else if (!MP) {
-        lg_chain_bwd<DP>(roots, p.NB, v0, p.bsuf + (size_t)b * p.NB * DP, vs[1]);
+    for (int64_t it = 0; it < NB; it++) {
+        const int64_t i = fwd ? it : NB - 1 - it;
+        load(fwd ? it + NS - 1 : NB - 1 - (it + NS - 1), (int)((it + NS - 1) % NS));
+        cp_async_wait<NS - 1>();
+        __syncthreads();
+        const float* M = ring + (size_t)(it % NS) * DP * DP;
+        float y = MP ? neg_inf() : 0.0f;
+        if (tid < DP) {
+            out[(size_t)i * DP + tid] = vec[tid];  // the carry entering root i
+            const int c = tid >> 2, w = tid & 3;
+            if (fwd) {
+#pragma unroll 16
+                for (int k = 0; k < DP; k++) {
+                    const float mk = M[sw(k, c) + w];
+                    y = MP ? fmaxf(y, vec[k] + mk) : fmaf(vec[k], mk, y);
+                }
+            } else {
+#pragma unroll 4
+                for (int cc = 0; cc < CH; cc++) {
+                    const float4 m4 = *reinterpret_cast<const float4*>(M + sw(tid, cc));
+                    y = fmaf(m4.x, vec[4 * cc], y);
+                    y = fmaf(m4.y, vec[4 * cc + 1], y);
+                    y = fmaf(m4.z, vec[4 * cc + 2], y);
+                    y = fmaf(m4.w, vec[4 * cc + 3], y);
+                }
+            }
+        }
+        float m = (tid < DP) ? y : (MP ? neg_inf() : 0.0f);
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if (lane == 0) red[tid >> 5] = m;
+        __syncthreads();
+        m = fmaxf(red[0], red[1]);
+        if (tid < DP) vec[tid] = MP ? ((m > neg_inf()) ? y - m : y) : y * pow2_inv(m);
+        // (the next iteration's barrier orders these writes before the reads)
     }
 }
 
@@ -794,8 +865,21 @@ static cudaError_t lg_launch(const LgParams& p, cudaStream_t s) {
         cfg3 = sm3;
     }
     const dim3 grid((unsigned)p.NB, (unsigned)p.B);
+    if (OP == 0 && DP == 64 && p.tc) {
+        cudaError_t e = launch_large_tc_leaf(p, p.lik, s);
+        if (e != cudaSuccess) return e;
+    }
     lg_leaf_kernel<DP, OP><<<grid, 256, sm1, s>>>(p);
-    lg_carry_kernel<DP, OP><<<(unsigned)p.B, 64, 0, s>>>(p);
+    {
+        const size_t smc = (size_t)6 * DP * DP * 4;
+        static size_t cfgc = 0;
+        if (cfgc < smc) {
+            cudaError_t e = cudaFuncSetAttribute(lg_carry_kernel<DP, OP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smc);
+            if (e != cudaSuccess) return e;
+            cfgc = smc;
+        }
+        lg_carry_kernel<DP, OP><<<dim3((unsigned)p.B, 2), 64, smc, s>>>(p);
+    }
     lg_sweep_kernel<DP, OP><<<grid, 256, sm3, s>>>(p);
     if (OP == 1) {
         lg_resolve_kernel<<<(unsigned)p.B, 32, 0, s>>>(p, DP);

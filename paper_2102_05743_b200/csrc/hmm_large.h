@@ -31,6 +31,9 @@ struct LgParams {
     uint8_t* bmap;      // [B][NB][DP]  Viterbi block maps
     int32_t* bend;      // [B][NB]      Viterbi block end states
     int32_t* xstar;     // [B]
+    // tensor-core leaf products (sum-product, DP = 64): hmm_large_tc.cu
+    int tc;             // 1: leaf aggregates come from lg_leaf_tc_kernel
+    float* lik;         // [B][T][64] likelihood rows exp(ll - m_t), padded with 0
 };
 
 }  // namespace hmm
