@@ -44,6 +44,7 @@ def _L():
         _lib.oracle_smooth.argtypes = [i32, i64, p, p, p, p, p, p, p, p]
         _lib.oracle_viterbi.argtypes = [i32, i64, p, p, p, p, p, p]
         _lib.oracle_smooth_sampled.argtypes = [i32, i64, p, p, p, p, i64, p, p, p, p]
+        _lib.oracle_smooth_stats.argtypes = [i32, i64, p, p, p, p, p, p, p]
         _lib.oracle_max_marginals.argtypes = [i32, i64, p, p, p, p, p]
         _lib.oracle_joint_weight.argtypes = [i32, i64, p, p, p, p]
         _lib.oracle_joint_weight.restype = ctypes.c_double
@@ -84,6 +85,18 @@ def smooth_sampled(log_pi, log_A, log_lik, ts):
     _L().oracle_smooth_sampled(D, T, _p(log_pi), _p(log_A), _p(log_lik), _p(ts), ts.size, _p(filt), _p(sm),
                                ctypes.byref(lz), ctypes.byref(info))
     return dict(ts=ts, filtered=filt, smoothed=sm, log_z=lz.value, info=info.value)
+
+
+def smooth_stats(log_pi, log_A, log_lik):
+    """Baum-Welch E-step statistics: dict(xi_sum [D,D] = sum_{t>=1} p(x_{t-1}=i, x_t=j|y),
+    gamma_sum [D] = sum_t p(x_t=d|y), log_z, info)."""
+    log_pi, log_A, log_lik = _f32(log_pi), _f32(log_A), _f32(log_lik)
+    T, D = log_lik.shape
+    xi = np.empty((D, D)); g = np.empty(D)
+    lz = ctypes.c_double(); info = ctypes.c_int64()
+    _L().oracle_smooth_stats(D, T, _p(log_pi), _p(log_A), _p(log_lik), _p(xi), _p(g), ctypes.byref(lz),
+                             ctypes.byref(info))
+    return dict(xi_sum=xi, gamma_sum=g, log_z=lz.value, info=info.value)
 
 
 def viterbi(log_pi, log_A, log_lik):

@@ -63,6 +63,23 @@ def smooth(log_pi, log_A, log_lik):
     return dict(log_z=lz, smoothed=sm, filtered=filt)
 
 
+def pair_stats(log_pi, log_A, log_lik):
+    """Baum-Welch E-step statistics by enumeration: xi_sum[i,j] = sum_{t>=1} p(x_{t-1}=i, x_t=j | y)
+    and gamma_sum[d] = sum_t p(x_t=d | y) over the normalised joint weights of Eq. 6."""
+    ll = np.asarray(log_lik, np.float64)
+    T, D = ll.shape
+    X = _all_sequences(D, T)
+    w = joint_log_weights(log_pi, log_A, ll, X)
+    p = np.exp(w - _logsumexp(w))
+    xi = np.zeros((D, D))
+    for t in range(1, T):
+        np.add.at(xi, (X[:, t - 1], X[:, t]), p)
+    g = np.zeros(D)
+    for t in range(T):
+        g += np.bincount(X[:, t], weights=p, minlength=D)
+    return dict(xi_sum=xi, gamma_sum=g)
+
+
 def viterbi(log_pi, log_A, log_lik, tie_tol: float = 1e-9):
     """MAP sequence by enumeration; among sequences within tie_tol of the best, the lexicographically
     smallest.  Returns dict(path, log_prob, gap) with gap = best - second best distinct-sequence weight."""

@@ -217,6 +217,60 @@ int oracle_smooth_sampled(int D, int64_t T, const float* log_pi, const float* lo
     return 0;
 }
 
+/* Baum-Welch expectation statistics ("in expectation step, BWA uses the forward-backward
+ * algorithm"): with the normalised forward potentials alpha_t and backward potentials beta_t of
+ * Algorithm 1 (as in oracle_smooth), the pairwise posterior of Eq. 6's factorisation
+ *   xi_t(i,j) = p(x_{t-1}=i, x_t=j | y) = alpha_{t-1}(i) A(i,j) l_t(j) beta_t(j) / sum_{i,j}(same)
+ * summed over t = 1..T-1 into xi_sum[D*D], and the occupancies gamma_sum[d] = sum_t p(x_t=d | y)
+ * (Eq. 14).  log_z as oracle_smooth's forward pass.                                                   */
+int oracle_smooth_stats(int D, int64_t T, const float* log_pi, const float* log_A, const float* log_lik,
+                        double* xi_sum, double* gamma_sum, double* log_z, int64_t* info) {
+    double* sm = (double*)malloc(sizeof(double) * (size_t)T * D);
+    double* fl = (double*)malloc(sizeof(double) * (size_t)T * D);
+    double lzb;
+    oracle_smooth(D, T, log_pi, log_A, log_lik, fl, sm, log_z, &lzb, info);
+    for (int i = 0; i < D * D; i++) xi_sum[i] = 0.0;
+    for (int i = 0; i < D; i++) gamma_sum[i] = 0.0;
+    if (*info != 0) { free(sm); free(fl); return 0; }
+    /* smoothed_t = alpha_t beta_t / Z_t  =>  beta_t(j) proportional to smoothed_t(j) / alpha_t(j) where
+     * alpha_t(j) > 0; recompute beta directly instead (Alg 1 lines 7-9) to stay on the definition. */
+    double* A = (double*)malloc(sizeof(double) * D * D);
+    double* beta = (double*)malloc(sizeof(double) * (size_t)T * D);
+    double* l = (double*)malloc(sizeof(double) * D);
+    for (int i = 0; i < D * D; i++) A[i] = exp((double)log_A[i]);
+    for (int d = 0; d < D; d++) beta[(size_t)(T - 1) * D + d] = 1.0;
+    for (int64_t t = T - 2; t >= 0; t--) {
+        double mx = -INFINITY;
+        for (int d = 0; d < D; d++) if ((double)log_lik[(t + 1) * D + d] > mx) mx = log_lik[(t + 1) * D + d];
+        for (int d = 0; d < D; d++) l[d] = (mx == -INFINITY) ? 0.0 : exp((double)log_lik[(t + 1) * D + d] - mx);
+        double s = 0.0;
+        for (int i = 0; i < D; i++) {
+            double acc = 0.0;
+            for (int j = 0; j < D; j++) acc += A[i * D + j] * l[j] * beta[(size_t)(t + 1) * D + j];
+            beta[(size_t)t * D + i] = acc;
+            s += acc;
+        }
+        for (int i = 0; i < D; i++) beta[(size_t)t * D + i] /= s;
+    }
+    double* x = (double*)malloc(sizeof(double) * D * D);
+    for (int64_t t = 1; t < T; t++) {
+        double mx = -INFINITY;
+        for (int d = 0; d < D; d++) if ((double)log_lik[t * D + d] > mx) mx = log_lik[t * D + d];
+        for (int d = 0; d < D; d++) l[d] = (mx == -INFINITY) ? 0.0 : exp((double)log_lik[t * D + d] - mx);
+        double z = 0.0;
+        for (int i = 0; i < D; i++)
+            for (int j = 0; j < D; j++) {
+                x[i * D + j] = fl[(size_t)(t - 1) * D + i] * A[i * D + j] * l[j] * beta[(size_t)t * D + j];
+                z += x[i * D + j];
+            }
+        for (int i = 0; i < D * D; i++) xi_sum[i] += x[i] / z;
+    }
+    for (int64_t t = 0; t < T; t++)
+        for (int d = 0; d < D; d++) gamma_sum[d] += sm[(size_t)t * D + d];
+    free(A); free(beta); free(l); free(x); free(sm); free(fl);
+    return 0;
+}
+
 /* Algorithm 4 in the log domain.  path[T] int32, log_prob = max_x V_T(x). */
 int oracle_viterbi(int D, int64_t T, const float* log_pi, const float* log_A, const float* log_lik,
                    int32_t* path, double* log_prob, int64_t* info) {

@@ -309,3 +309,32 @@ def test_smooth_sampled_info():
     wl = W.ge(3000, seed=4)
     wl.log_lik[1234, :] = -np.inf
     assert oracle.smooth_sampled(wl.log_pi, wl.log_A, wl.log_lik, [5, 10])["info"] == 1235
+
+
+# ---------------------------------------------------------------- Baum-Welch E-step statistics (f2)
+@pytest.mark.parametrize("seed", range(12))
+def test_smooth_stats_brute_force(seed):
+    """xi_sum / gamma_sum from the forward-backward potentials equal the enumeration of all D^T paths."""
+    rng = np.random.default_rng(100 + seed)
+    D, T = int(rng.integers(2, 5)), int(rng.integers(2, 7))
+    if seed % 2:
+        wl = W.random_potentials(D, T, seed=seed)
+    else:
+        wl = W.dense(D, T, seed=seed)
+    o = oracle.smooth_stats(wl.log_pi, wl.log_A, wl.log_lik)
+    b = brute.pair_stats(wl.log_pi, wl.log_A, wl.log_lik)
+    assert o["info"] == 0
+    np.testing.assert_allclose(o["xi_sum"], b["xi_sum"], rtol=1e-10, atol=1e-12)
+    np.testing.assert_allclose(o["gamma_sum"], b["gamma_sum"], rtol=1e-10, atol=1e-12)
+
+
+def test_smooth_stats_invariants():
+    wl = W.ge(20_000, seed=3)
+    o = oracle.smooth_stats(wl.log_pi, wl.log_A, wl.log_lik)
+    sm = oracle.smooth(wl.log_pi, wl.log_A, wl.log_lik)["smoothed"]
+    T = 20_000
+    assert abs(o["xi_sum"].sum() - (T - 1)) < 1e-8 * T
+    # marginalising xi over x_t gives the occupancies of x_{t-1} (t = 0..T-2), and vice versa
+    np.testing.assert_allclose(o["xi_sum"].sum(1), sm[:-1].sum(0), rtol=1e-9)
+    np.testing.assert_allclose(o["xi_sum"].sum(0), sm[1:].sum(0), rtol=1e-9)
+    np.testing.assert_allclose(o["gamma_sum"], sm.sum(0), rtol=1e-12)
