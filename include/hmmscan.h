@@ -57,7 +57,7 @@ typedef enum {
     HMM_ERR_CUDA = 4
 } hmm_status_t;
 
-typedef enum { HMM_OP_SMOOTH = 0, HMM_OP_VITERBI = 1 } hmm_op_t;
+typedef enum { HMM_OP_SMOOTH = 0, HMM_OP_VITERBI = 1, HMM_OP_SMOOTH_STATS = 2 } hmm_op_t;
 
 /* Human-readable name of a status code (static storage, never NULL). */
 const char* hmm_status_string(hmm_status_t status);
@@ -66,7 +66,8 @@ const char* hmm_status_string(hmm_status_t status);
 const char* hmm_version(void);
 
 /* Bytes of device workspace needed by the hmm_smooth and hmm_viterbi families for (op, D, T, B) on the current
- * device.  Returns 0 for invalid arguments.  The value depends on the device's SM count. */
+ * device (op = HMM_OP_SMOOTH_STATS: hmm_smooth_stats, B = 1).  Returns 0 for invalid arguments.  The value
+ * depends on the device's SM count. */
 size_t hmm_workspace_size(int op, int D, int64_t T, int64_t B);
 
 /*
@@ -82,6 +83,24 @@ size_t hmm_workspace_size(int op, int D, int64_t T, int64_t B);
 hmm_status_t hmm_smooth(int D, int64_t T, const float* log_pi, const float* log_A, const float* log_lik,
                         float* filtered, float* smoothed, double* log_likelihood, int32_t* info,
                         void* workspace, size_t workspace_bytes, void* stream);
+
+/*
+ * Smoother + Baum-Welch expectation statistics ("in expectation step, BWA uses the
+ * forward-backward algorithm, which can be parallelized using the methods proposed in this article").
+ * Same outputs as hmm_smooth (filtered and smoothed may both be NULL: statistics only) plus
+ *   xi_sum [D*D] out (double): sum_{t=1..T-1} p(x_{t-1}=i, x_t=j | y), the pairwise posteriors of the
+ *                       factorisation Eq. 6 from the forward / backward potentials
+ *                       (row-major, i = previous state);
+ *   gamma_sum [D] out (double): sum_{t=0..T-1} p(x_t=d | y) (Eq. 14).
+ * The M-step transition update is A'(i,j) = xi_sum(i,j) / sum_j xi_sum(i,j).  1 <= D <= 8, one
+ * sequence; log_lik / filtered / smoothed must be 16-byte aligned (HMM_ERR_INVALID_VALUE otherwise),
+ * D > 8 -> HMM_ERR_UNSUPPORTED.  Workspace: hmm_workspace_size(HMM_OP_SMOOTH_STATS, D, T, 1).
+ * Statistics are fp32 per 16-step slice, fp64 across slices, summed in a fixed order (deterministic).
+ */
+hmm_status_t hmm_smooth_stats(int D, int64_t T, const float* log_pi, const float* log_A, const float* log_lik,
+                              float* filtered, float* smoothed, double* log_likelihood, double* xi_sum,
+                              double* gamma_sum, int32_t* info, void* workspace, size_t workspace_bytes,
+                              void* stream);
 
 /*
  * Parallel max-product MAP (Viterbi) — Definition 5 / Propositions 2-3 for the

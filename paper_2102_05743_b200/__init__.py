@@ -21,7 +21,7 @@ import torch
 
 from .build import LIB, ROOT
 
-HMM_OP_SMOOTH, HMM_OP_VITERBI = 0, 1
+HMM_OP_SMOOTH, HMM_OP_VITERBI, HMM_OP_SMOOTH_STATS = 0, 1, 2
 HMM_MAX_D = 64
 STATUS = {0: "HMM_SUCCESS", 1: "HMM_ERR_INVALID_VALUE", 2: "HMM_ERR_WORKSPACE", 3: "HMM_ERR_UNSUPPORTED",
           4: "HMM_ERR_CUDA"}
@@ -54,6 +54,8 @@ def lib() -> ctypes.CDLL:
         L.hmm_debug_set_timers.argtypes = [p]
         L.hmm_debug_set_timers.restype = None
         L.hmm_debug_plan.argtypes = [i32, i32, i64, i64, p]
+        L.hmm_smooth_stats.argtypes = [i32, i64, p, p, p, p, p, p, p, p, p, p, sz, p]
+        L.hmm_smooth_stats.restype = i32
         L.hmm_debug_force_path.argtypes = [i32]
         L.hmm_debug_force_path.restype = None
         L.hmm_debug_plan.restype = i32
@@ -163,6 +165,29 @@ def smooth(log_pi, log_A, log_lik, want_filtered: bool = True, out=None, ws=None
                           _ptr(info), _ptr(ws), ws.numel(), _stream(stream))
     _check(st, "hmm_smooth")
     return filt, sm, lz, info
+
+
+def smooth_stats(log_pi, log_A, log_lik, want_marginals: bool = True, stream=None):
+    """Smoother + Baum-Welch E-step statistics for one sequence, 1 <= D <= 8.
+
+    Returns (filtered or None, smoothed or None, log_likelihood [1], xi_sum [D,D] f64, gamma_sum [D] f64,
+    info [1]); xi_sum(i,j) = sum_t p(x_{t-1}=i, x_t=j | y), gamma_sum(d) = sum_t p(x_t=d | y).
+    """
+    batched, B, T, D = _inputs(log_pi, log_A, log_lik)
+    if batched:
+        raise HmmError("smooth_stats: one sequence")
+    dev = log_lik.device
+    filt = torch.empty_like(log_lik) if want_marginals else None
+    sm = torch.empty_like(log_lik) if want_marginals else None
+    lz = torch.empty(1, dtype=torch.float64, device=dev)
+    xi = torch.empty((D, D), dtype=torch.float64, device=dev)
+    g = torch.empty(D, dtype=torch.float64, device=dev)
+    info = torch.empty(1, dtype=torch.int32, device=dev)
+    ws = workspace(HMM_OP_SMOOTH_STATS, D, T, 1, dev)
+    st = lib().hmm_smooth_stats(D, T, _ptr(log_pi), _ptr(log_A), _ptr(log_lik), _ptr(filt), _ptr(sm), _ptr(lz),
+                                _ptr(xi), _ptr(g), _ptr(info), _ptr(ws), ws.numel(), _stream(stream))
+    _check(st, "hmm_smooth_stats")
+    return filt, sm, lz, xi, g, info
 
 
 def viterbi(log_pi, log_A, log_lik, out=None, ws=None, stream=None):

@@ -140,7 +140,7 @@ struct StPlan {
     int64_t n = 0;
     int K = 0;
     size_t smem = 0;
-    size_t ws_sync, ws_slots, slot_bytes, ws_q, ws_lagg, ws_bp, ws_lmap, ws_total;
+    size_t ws_sync, ws_slots, slot_bytes, ws_q, ws_lagg, ws_bp, ws_lmap, ws_stats, ws_total;
 };
 
 bool make_stream_plan(int D, int op, int64_t T, StPlan& P) {
@@ -165,10 +165,11 @@ bool make_stream_plan(int D, int op, int64_t T, StPlan& P) {
     P.ws_sync = take(64);
     P.slot_bytes = hmm::small_slot_bytes(D);
     P.ws_slots = take((size_t)P.G * P.slot_bytes);
-    P.ws_q = take(op == 0 ? lanes * P.K * QB : 0);
+    P.ws_q = take(op != 1 ? lanes * P.K * QB : 0);
     P.ws_lagg = take(lanes * QB);
     P.ws_bp = take(op == 1 ? (size_t)(T + S) * hmm::small_bpb(D) + 16 : 0);
     P.ws_lmap = take(op == 1 ? lanes * 8 : 0);
+    P.ws_stats = take(op == 2 ? (size_t)P.G * (D * D + D) * 8 : 0);
     P.ws_total = off;
     return true;
 }
@@ -337,6 +338,35 @@ hmm_status_t run(int op, int D, int64_t T, int64_t B, const float* log_pi, const
     return e == cudaSuccess ? HMM_SUCCESS : HMM_ERR_CUDA;
 }
 
+// Smoother + Baum-Welch E-step statistics: lane-streaming kernel only (D <= 8, one sequence).
+hmm_status_t run_stats(int D, int64_t T, const float* log_pi, const float* log_A, const float* log_lik,
+                       float* filtered, float* smoothed, double* log_likelihood, double* xi_sum, double* gamma_sum,
+                       int32_t* info, void* ws, size_t ws_bytes, void* stream) {
+    if (D < 1 || T < 1) return HMM_ERR_INVALID_VALUE;
+    if (D > 8) return HMM_ERR_UNSUPPORTED;
+    if (!log_pi || !log_A || !log_lik || !log_likelihood || !xi_sum || !gamma_sum || !info) return HMM_ERR_INVALID_VALUE;
+    if (!al4(log_pi) || !al4(log_A) || !al8(log_likelihood) || !al8(xi_sum) || !al8(gamma_sum) || !al4(info))
+        return HMM_ERR_INVALID_VALUE;
+    if (!al16(log_lik) || (filtered && !al16(filtered)) || (smoothed && !al16(smoothed))) return HMM_ERR_INVALID_VALUE;
+    StPlan SP;
+    if (!make_stream_plan(D, 2, T, SP)) return HMM_ERR_UNSUPPORTED;
+    if (!ws || ws_bytes < SP.ws_total || (reinterpret_cast<uintptr_t>(ws) & 255u)) return HMM_ERR_WORKSPACE;
+    hmm::SParams sp;
+    std::memset(&sp, 0, sizeof(sp));
+    sp.T = T; sp.n = SP.n; sp.K = SP.K;
+    sp.log_pi = log_pi; sp.log_A = log_A; sp.log_lik = log_lik;
+    sp.filtered = filtered; sp.smoothed = smoothed; sp.scalar_out = log_likelihood; sp.info = info;
+    sp.ws = static_cast<uint8_t*>(ws);
+    sp.ws_sync = SP.ws_sync; sp.ws_slots = SP.ws_slots; sp.slot_bytes = SP.slot_bytes; sp.ws_q = SP.ws_q;
+    sp.ws_lagg = SP.ws_lagg; sp.ws_stats = SP.ws_stats;
+    sp.xi_out = xi_sum; sp.gamma_out = gamma_sum;
+    sp.L = hmm::stream_smem_layout(D, SP.G);
+    sp.timers = t_timers;
+    sp.mode = hmm::HMM_MODE_FULL; sp.world = 1;
+    cudaError_t e = hmm::launch_stream(D, 2, (unsigned)SP.G, sp, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? HMM_SUCCESS : HMM_ERR_CUDA;
+}
+
 }  // namespace
 
 extern "C" {
@@ -373,6 +403,11 @@ int hmm_debug_plan(int op, int D, int64_t T, int64_t B, int64_t* out /*[8]*/) {
 }
 
 size_t hmm_workspace_size(int op, int D, int64_t T, int64_t B) {
+    if (op == 2) {  // smoother with E-step statistics (hmm_smooth_stats)
+        StPlan SP;
+        if (D < 1 || D > 8 || T < 1 || B != 1 || !make_stream_plan(D, 2, T, SP)) return 0;
+        return SP.ws_total;
+    }
     if ((op != 0 && op != 1) || D < 1 || D > HMM_MAX_D || T < 1 || B < 1) return 0;
     if (D > 8) {  // either leaf-product engine may run (hmm_debug_force_path): size for both
         LgPlan G, H2;
@@ -392,6 +427,13 @@ hmm_status_t hmm_smooth(int D, int64_t T, const float* log_pi, const float* log_
                         size_t workspace_bytes, void* stream) {
     return run(0, D, T, 1, log_pi, log_A, log_lik, filtered, smoothed, nullptr, log_likelihood, info, workspace,
                workspace_bytes, stream);
+}
+
+hmm_status_t hmm_smooth_stats(int D, int64_t T, const float* log_pi, const float* log_A, const float* log_lik,
+                              float* filtered, float* smoothed, double* log_likelihood, double* xi_sum,
+                              double* gamma_sum, int32_t* info, void* workspace, size_t workspace_bytes, void* stream) {
+    return run_stats(D, T, log_pi, log_A, log_lik, filtered, smoothed, log_likelihood, xi_sum, gamma_sum, info,
+                     workspace, workspace_bytes, stream);
 }
 
 hmm_status_t hmm_viterbi(int D, int64_t T, const float* log_pi, const float* log_A, const float* log_lik,

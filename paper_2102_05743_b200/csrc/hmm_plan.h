@@ -185,6 +185,9 @@ struct SParams {
     size_t ws_lagg;  // [G][NT] lane aggregates (split phase: reduce -> finish / forward)
     size_t ws_bp;    // Viterbi: backpointers by local step (bpb bytes each)
     size_t ws_lmap;  // Viterbi: [G][NT] lane maps (split phase: forward -> finish)
+    size_t ws_stats; // smoother statistics: [G][D*D + D] fp64 CTA partials
+    double* xi_out;    // [D*D] sum_t xi_t (E-step statistics), or unused
+    double* gamma_out; // [D]   sum_t gamma_t
     StreamLayout L;
     unsigned long long* timers;
     int mode, rank, world;

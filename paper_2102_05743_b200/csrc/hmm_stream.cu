@@ -309,6 +309,73 @@ __device__ __forceinline__ void sp_beta_slice(float* lrows, const float* frows, 
     }
 }
 
+// Backward pass + Eq. 14 as sp_beta_slice, also accumulating the Baum-Welch E-step statistics
+// (PAPER.md:762-763): the pairwise posterior xi_t(i,j) = a_{t-1}(i) A(i,j) l_t(j) b_t(j) / z_t with the
+// normaliser z_t = a_{t-1} . (A (l_t o b_t)) -- the product the backward update computes anyway --
+// and the occupancies gamma_t = smoothed_t.  `aprev` is the filtered row entering the slice;
+// `skip0` drops xi at the sequence's first step (no predecessor).  Partials are fp32 per slice.
+template <int D>
+__device__ __forceinline__ void sp_beta_stats_step(float* lrow, const float* frow, const float* aprev,
+                                                   const float* A, float* beta, bool want_xi, float* xi,
+                                                   float* gs) {
+    float l[D], a[D], g[D];
+    ld_row<D>(lrow, l);
+    ld_row<D>(frow, a);
+#pragma unroll
+    for (int j = 0; j < D; j++) g[j] = a[j] * beta[j];
+    const float zz = rcp(vsum<D>(g));
+#pragma unroll
+    for (int j = 0; j < D; j++) {
+        g[j] *= zz;
+        gs[j] += g[j];
+    }
+    st_row<D>(lrow, g);
+    float w[D], bn[D];
+#pragma unroll
+    for (int j = 0; j < D; j++) w[j] = l[j] * beta[j];
+#pragma unroll
+    for (int r = 0; r < D; r++) {
+        float acc = A[r * D] * w[0];
+#pragma unroll
+        for (int j = 1; j < D; j++) acc = fmaf(A[r * D + j], w[j], acc);
+        bn[r] = acc;
+    }
+    if (want_xi) {
+        float ap[D];
+        ld_row<D>(aprev, ap);
+        float z = ap[0] * bn[0];
+#pragma unroll
+        for (int r = 1; r < D; r++) z = fmaf(ap[r], bn[r], z);
+        const float rz = (z > 0.0f) ? 1.0f / z : 0.0f;
+#pragma unroll
+        for (int r = 0; r < D; r++) {
+            const float ar = ap[r] * rz;
+#pragma unroll
+            for (int j = 0; j < D; j++) xi[r * D + j] = fmaf(ar, A[r * D + j] * w[j], xi[r * D + j]);
+        }
+    }
+    const float sc = pow2_inv(vmax<D>(bn));
+#pragma unroll
+    for (int r = 0; r < D; r++) beta[r] = bn[r] * sc;
+}
+template <int D, int S>
+__device__ __forceinline__ void sp_beta_slice_stats(float* lrows, const float* frows, int nr, const float* A,
+                                                    float* beta, const float* aprev, bool skip0, double* xi_l,
+                                                    double* g_l) {
+    float xi[D * D], gs[D];
+#pragma unroll
+    for (int e = 0; e < D * D; e++) xi[e] = 0.0f;
+#pragma unroll
+    for (int d = 0; d < D; d++) gs[d] = 0.0f;
+#pragma unroll 1
+    for (int i = nr - 1; i >= 1; i--) sp_beta_stats_step<D>(lrows + i * D, frows + i * D, frows + (i - 1) * D, A, beta, true, xi, gs);
+    sp_beta_stats_step<D>(lrows, frows, aprev, A, beta, !skip0, xi, gs);
+#pragma unroll
+    for (int e = 0; e < D * D; e++) xi_l[e] += (double)xi[e];
+#pragma unroll
+    for (int d = 0; d < D; d++) g_l[d] += (double)gs[d];
+}
+
 // Viterbi forward sweep over one slice (Alg. 4 lines 3-6): backpointers into registers (D <= 4:
 // one 16-bit nibble word per step, two steps per u32; D > 4: one u32 per step), returns the slice
 // map f(x_end) = state before the slice, accumulates sum (o_t + m_t).
@@ -397,6 +464,7 @@ __global__ void __launch_bounds__(stream_nt(D)) hmm_stream_kernel(const SParams 
     constexpr int BPB = small_bpb(D);     // backpointer bytes per step
     constexpr int NCB = S * BPB / 8;      // 8-B chunks of one lane's backpointer slice
     constexpr bool MP = (OP == 1);
+    constexpr bool STATS = (OP == 2);  // smoother + Baum-Welch E-step statistics
     constexpr int NN = 2 * NT;
     extern __shared__ __align__(128) uint8_t smem[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -762,6 +830,11 @@ __global__ void __launch_bounds__(stream_nt(D)) hmm_stream_kernel(const SParams 
                 }
             };
             uint32_t qphase = 0;
+            double xi_l[STATS ? D * D : 1], g_l[STATS ? D : 1];
+#pragma unroll
+            for (int e = 0; e < (STATS ? D * D : 1); e++) xi_l[e] = 0.0;
+#pragma unroll
+            for (int e = 0; e < (STATS ? D : 1); e++) g_l[e] = 0.0;
             coop_load(0, 0);
             issue_q(0);
             for (int k = 0; k < K; k++) {
@@ -784,18 +857,42 @@ __global__ void __launch_bounds__(stream_nt(D)) hmm_stream_kernel(const SParams 
                 if (k + 1 < K) issue_q(k + 1);
                 if (nr > 0) {
                     float* rows = slot(st);
+                    float aprev[D];
+#pragma unroll
+                    for (int d = 0; d < D; d++) aprev[d] = alpha[d];
                     const int zi = sp_alpha_slice<D, S>(rows, frows, nr, lane_t0 && k == 0, A, pv, alpha, rprod,
                                                         rexp, msum);
                     const int64_t r0 = a0 + (int64_t)k * S;
                     if (zi >= 0 && tb + r0 + zi < zero_t) zero_t = tb + r0 + zi;
-                    sp_beta_slice<D, S>(rows, frows, nr, A, beta);
+                    if constexpr (STATS)
+                        sp_beta_slice_stats<D, S>(rows, frows, nr, A, beta, aprev, lane_t0 && k == 0, xi_l, g_l);
+                    else
+                        sp_beta_slice<D, S>(rows, frows, nr, A, beta);
                 }
                 __syncwarp();
-                coop_store(k, stage_base(st), p.smoothed);
+                if (p.smoothed) coop_store(k, stage_base(st), p.smoothed);
                 if (p.filtered) coop_store(k, stage_base(2), p.filtered);
                 __syncwarp();
             }
             if (nsl > 0) acc += log((double)vsum<D>(alpha)) - log((double)rprod) - (double)rexp * (double)kLn2 + msum;
+            if constexpr (STATS) {  // fixed-order CTA sums of the lanes' fp64 partials -> workspace
+                double* cst = reinterpret_cast<double*>(p.ws + p.ws_stats) + (size_t)c * (D * D + D);
+                double* rbuf = reinterpret_cast<double*>(ring);  // ring is free after the loop
+                __syncthreads();
+#pragma unroll
+                for (int e = 0; e < D * D + D; e++) {
+                    double v = (e < D * D) ? xi_l[e < D * D ? e : 0] : g_l[e >= D * D ? e - D * D : 0];
+#pragma unroll
+                    for (int o = 16; o >= 1; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+                    if (lane == 0) rbuf[e * NW + warp] = v;
+                }
+                __syncthreads();
+                for (int e = tid; e < D * D + D; e += NT) {
+                    double v = 0.0;
+                    for (int w = 0; w < NW; w++) v += rbuf[e * NW + w];
+                    cst[e] = v;
+                }
+            }
             if (tmr && lane == 0 && warp == NW - 1) tmr[12] = global_ns();  // last warp done with pass 2
         }
         HMM_STAMP(6);
@@ -993,6 +1090,15 @@ __global__ void __launch_bounds__(stream_nt(D)) hmm_stream_kernel(const SParams 
         const double tot = block_sum<NT>(v, red);
         if (tid == 0) {
             if (p.scalar_out) p.scalar_out[0] = tot;
+            if constexpr (STATS) {
+                const double* cst = reinterpret_cast<const double*>(p.ws + p.ws_stats);
+                for (int e = 0; e < D * D + D; e++) {
+                    double v = 0.0;
+                    for (int x = 0; x < G; x++) v += __ldcg(cst + (size_t)x * (D * D + D) + e);
+                    if (e < D * D) p.xi_out[e] = v;
+                    else p.gamma_out[e - D * D] = v;
+                }
+            }
             const uint32_t badf = atomicExch(bad_flag, 0u);
             const unsigned long long zc = atomicExch(zero_code, 0ull);
             int32_t inf = 0;
@@ -1049,6 +1155,7 @@ static cudaError_t launch_st_op(int D, unsigned G, const SParams& sp, cudaStream
 }
 
 cudaError_t launch_stream(int D, int op, unsigned G, const SParams& sp, cudaStream_t s) {
+    if (op == 2) return launch_st_op<2>(D, G, sp, s);
     return op == 0 ? launch_st_op<0>(D, G, sp, s) : launch_st_op<1>(D, G, sp, s);
 }
 
