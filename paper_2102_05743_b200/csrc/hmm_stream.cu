@@ -81,59 +81,20 @@ __device__ __forceinline__ void sp_back_step(const float* row, bool t0, const fl
     for (int e = 0; e < D * D; e++) P[e] = Pn[e];
     d = exp_offset(vmax_tree<D * D>(P));
 }
-// Chain start: X = psi_t = A diag(l_t) itself (no product with an identity), pending offset of max(X).
-template <int D>
-__device__ __forceinline__ void sp_chain_start(const float* row, const float* A, float* X, float& d) {
-    float v[D], l[D];
-    ld_row<D>(row, v);
-    const float m = fmaxf(vmax<D>(v), -1e30f);
-    const float c = -m * kLog2e;
-#pragma unroll
-    for (int j = 0; j < D; j++) l[j] = ex2(fmaf(v[j], kLog2e, c));
-#pragma unroll
-    for (int i = 0; i < D; i++)
-#pragma unroll
-        for (int j = 0; j < D; j++) X[i * D + j] = A[i * D + j] * l[j];
-    d = exp_offset(vmax_tree<D * D>(X));
-}
-template <int D>
-__device__ __forceinline__ void normalize_pow2(float* X) {
-    const float s = pow2_inv(vmax_tree<D * D>(X));
-#pragma unroll
-    for (int e = 0; e < D * D; e++) X[e] *= s;
-}
-// One slice, right to left.  A full slice is split into two independent halves folded as two
-// interleaved chains, X = psi_H ... psi_{S-1} and Y = psi_0 ... psi_{H-1}, combined as P <- Y (X P)
-// (associativity of Def. 3).  Starting a chain from psi itself saves exactly the products the two
-// combining matrix products cost, so the FMA count is unchanged while every step now has a second
-// independent dependency chain to overlap with (the fold is latency-bound at 8 warps/SM).
+// One slice, right to left (sum-product).  Unlike the max-product fold below, the sum-product step is
+// issue-bound rather than latency-bound at 8 warps/SM (ncu: 66% issue-active, `wait` stalls 0.34 per
+// issue), so the two-chain split would only add its combine/normalise instructions (~7%): one chain.
 template <int D, int S>
 __device__ __forceinline__ void sp_fold_back(const float* rows, int nr, bool t0, const float* A, const float* pi,
                                              float* P, float& d) {
     if (nr == S) {
-        constexpr int H = S / 2;
-        float X[D * D], Y[D * D], dX, dY;
-        sp_chain_start<D>(rows + (S - 1) * D, A, X, dX);
-        sp_chain_start<D>(rows + (H - 1) * D, A, Y, dY);
-#pragma unroll 2
-        for (int q = 1; q < H - 1; q++) {
-            sp_back_step<D>(rows + (S - 1 - q) * D, false, A, pi, X, dX);
-            sp_back_step<D>(rows + (H - 1 - q) * D, false, A, pi, Y, dY);
-        }
-        sp_back_step<D>(rows + H * D, false, A, pi, X, dX);
-        sp_back_step<D>(rows, t0, A, pi, Y, dY);
-        normalize_pow2<D>(X);
-        normalize_pow2<D>(Y);
-        float XP[D * D];
-        if (d != 0.0f) normalize_pow2<D>(P);
-        mat_op<D, false>(X, P, XP);
-        mat_op<D, false>(Y, XP, P);
-        d = 0.0f;
+#pragma unroll 4
+        for (int ii = S - 1; ii >= 1; ii--) sp_back_step<D>(rows + ii * D, false, A, pi, P, d);
     } else {
 #pragma unroll 1
         for (int ii = nr - 1; ii >= 1; ii--) sp_back_step<D>(rows + ii * D, false, A, pi, P, d);
-        sp_back_step<D>(rows, t0, A, pi, P, d);
     }
+    sp_back_step<D>(rows, t0, A, pi, P, d);
 }
 
 // Max-product (log domain), one step right to left: P(i,j) <- max_k (LA(i,k) + w_t(k) + P(k,j)),
