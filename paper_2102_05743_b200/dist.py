@@ -188,3 +188,34 @@ def viterbi_dist(log_pi, log_A, log_lik_local, t_base: int, group=None, backend=
         log_prob += parts[r, 0]
     info = _combine_info(parts[:, 1:].reshape(-1).to(torch.int32))
     return path, log_prob, info
+
+
+def smooth_viterbi_dist(log_pi, log_A, log_lik_local, t_base: int, group=None, backend=None):
+    """Smoother and MAP path of the same T-partitioned sequence with the collectives of both merged:
+    two all-gathers per call instead of five (the rank aggregates of both semirings together; then the
+    Viterbi rank records together with every scalar partial).  Returns
+    (filtered, smoothed, log_z [1], info [1], path, log_prob [1], vinfo [1]) for the local slice."""
+    be = _backend(backend)
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    s_agg, s_i1 = be.smooth_reduce(log_pi, log_A, log_lik_local, t_base)
+    v_agg, v_i1 = be.viterbi_reduce(log_pi, log_A, log_lik_local, t_base)
+    na = s_agg.numel()
+    both = _all_gather(torch.cat([s_agg.view(-1), v_agg.view(-1)]), group).view(world, 2 * na)
+    s_all = both[:, :na].contiguous().view(-1)
+    v_all = both[:, na:].contiguous().view(-1)
+    filt, sm, lzp, s_i2 = be.smooth_finish(log_pi, log_A, log_lik_local, t_base, s_all, rank, world)
+    rec, lpp, v_i2 = be.viterbi_forward(log_pi, log_A, log_lik_local, t_base, v_all, rank, world)
+    sc = torch.stack([lzp.view(()), lpp.view(()), s_i1.double().view(()), s_i2.double().view(()),
+                      v_i1.double().view(()), v_i2.double().view(())])
+    packed = torch.cat([rec.view(torch.float64).view(-1).to(sc.device), sc])  # 2 + 6 float64 per rank
+    g = _all_gather(packed, group).view(world, 8)
+    rec_all = g[:, :2].contiguous().view(-1).view(torch.uint8)
+    path, _ = be.viterbi_finish(log_pi, log_A, log_lik_local, t_base, rec_all, rank, world)
+    log_z = torch.zeros(1, dtype=torch.float64, device=g.device)
+    log_prob = torch.zeros(1, dtype=torch.float64, device=g.device)
+    for r in range(world):  # fixed rank order
+        log_z += g[r, 2]
+        log_prob += g[r, 3]
+    info = _combine_info(g[:, 4:6].reshape(-1).to(torch.int32))
+    vinfo = _combine_info(g[:, 6:8].reshape(-1).to(torch.int32))
+    return filt, sm, log_z, info, path, log_prob, vinfo

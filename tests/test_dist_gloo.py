@@ -116,6 +116,11 @@ def _worker(rank, world, port, T, outdir):
     be = NumpyBackend()
     filt, sm, lz, info = HD.smooth_dist(lp, la, ll, t0, backend=be)
     path, lpr, vinfo = HD.viterbi_dist(lp, la, ll, t0, backend=be)
+    # the merged-collective variant returns the same values
+    f2, s2, lz2, i2, p2, lp2, vi2 = HD.smooth_viterbi_dist(lp, la, ll, t0, backend=be)
+    assert torch.equal(s2, sm) and torch.equal(f2, filt) and torch.equal(p2, path)
+    assert float(lz2[0]) == float(lz[0]) and float(lp2[0]) == float(lpr[0])
+    assert int(i2[0]) == int(info[0]) and int(vi2[0]) == int(vinfo[0])
     np.savez(os.path.join(outdir, f"r{rank}.npz"), t0=t0, filt=filt.numpy(), sm=sm.numpy(), lz=lz.numpy(),
              info=info.numpy(), path=path.numpy(), lpr=lpr.numpy(), vinfo=vinfo.numpy())
     dist.destroy_process_group()
