@@ -99,6 +99,21 @@ def smooth_stats(log_pi, log_A, log_lik):
     return dict(xi_sum=xi, gamma_sum=g, log_z=lz.value, info=info.value)
 
 
+def symbols_loglik(log_B, y):
+    """Eq. 5b with discrete observations: log_lik_t(d) = log p(y_t | x_t = d) = log_B[d, y_t]."""
+    log_B = _f32(log_B)
+    return np.ascontiguousarray(log_B[:, np.asarray(y, np.int64)].T)
+
+
+def smooth_symbols(log_pi, log_A, log_B, y, want_filtered=True, want_smoothed=True):
+    """The smoother of `smooth` on the emissions gathered from the symbol sequence."""
+    return smooth(log_pi, log_A, symbols_loglik(log_B, y), want_filtered, want_smoothed)
+
+
+def viterbi_symbols(log_pi, log_A, log_B, y):
+    return viterbi(log_pi, log_A, symbols_loglik(log_B, y))
+
+
 def viterbi(log_pi, log_A, log_lik):
     """Returns dict(path [T] int32, log_prob, info)."""
     log_pi, log_A, log_lik = _f32(log_pi), _f32(log_A), _f32(log_lik)

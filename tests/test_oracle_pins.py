@@ -338,3 +338,31 @@ def test_smooth_stats_invariants():
     np.testing.assert_allclose(o["xi_sum"].sum(1), sm[:-1].sum(0), rtol=1e-9)
     np.testing.assert_allclose(o["xi_sum"].sum(0), sm[1:].sum(0), rtol=1e-9)
     np.testing.assert_allclose(o["gamma_sum"], sm.sum(0), rtol=1e-12)
+
+
+# ---------------------------------------------------------------- symbol inputs (f1)
+@pytest.mark.parametrize("which", ["ge_T5", "spec_D2"])
+def test_symbol_oracle_matches_fixture(golden_dir, which):
+    """Discrete observations through the emission matrix: the printed fixture values."""
+    if which == "ge_T5":
+        g = _load(golden_dir, "ge_T5.json"); gm = _load(golden_dir, "ge_model.json")
+        lp, la, B = np.log(gm["prior"]), np.log(gm["Pi"]), np.array(gm["O"])
+    else:
+        g = _load(golden_dir, "spec_D2_T4.json")
+        lp, la, B = np.log(g["prior"]), np.log(g["A"]), np.array(g["B"])
+    y = np.array(g["obs"], np.uint8)
+    o = oracle.smooth_symbols(lp, la, np.log(B), y)
+    assert abs(o["log_z"] - g["log_z"]) < 1e-7
+    np.testing.assert_allclose(o["smoothed"], g["smoothed"], atol=1e-7)
+    v = oracle.viterbi_symbols(lp, la, np.log(B), y)
+    if "map_path" in g:
+        assert list(v["path"]) == g["map_path"]
+
+
+def test_symbol_workload_matches_loglik_workload():
+    """ge_symbols is the same chain as ge: gathering log O at y reproduces ge's log_lik exactly."""
+    ws = W.ge_symbols(10_000, 3)
+    wl = W.ge(10_000, 3)
+    np.testing.assert_array_equal(oracle.symbols_loglik(ws.log_B, ws.y), wl.log_lik)
+    d = W.discrete(5, 7, 1000, 2)
+    assert d.y.max() < 7 and np.allclose(np.exp(d.log_B.astype(np.float64)).sum(1), 1.0, atol=1e-6)

@@ -117,6 +117,36 @@ def ge(T: int, seed: int, jitter: float = 0.0, jitter_seed: int | None = None, *
                     f"ge_T{T}_s{seed}" + (f"_j{jitter}" if jitter else ""))
 
 
+class SymbolWorkload:
+    """Discrete-observation workload: log_pi [D], log_A [D,D], log_B [D,V] (log emission matrix), y [T] uint8."""
+
+    def __init__(self, log_pi, log_A, log_B, y, states=None, name=""):
+        self.log_pi, self.log_A, self.log_B, self.y, self.states, self.name = log_pi, log_A, log_B, y, states, name
+        self.T, self.D, self.V = y.shape[0], log_B.shape[0], log_B.shape[1]
+
+
+def ge_symbols(T: int, seed: int, **params) -> SymbolWorkload:
+    """The GE channel in its native form (PAPER.md:826): y_t in {0,1} with emission matrix O (Eq. 22);
+    same chain / observations as ge(T, seed)."""
+    p = dict(GE_PARAMS); p.update(params)
+    Pi, O, pr = ge_model(**p)
+    states, obs = simulate_discrete(pr, Pi, O, T, seed)
+    return SymbolWorkload(np.log(pr).astype(np.float32), np.log(Pi).astype(np.float32),
+                          np.log(O).astype(np.float32), obs.astype(np.uint8), states, f"ge_sym_T{T}_s{seed}")
+
+
+def discrete(D: int, V: int, T: int, seed: int) -> SymbolWorkload:
+    """Dense Dirichlet(1) transitions (dense_model) and Dirichlet(1) emission rows over V symbols
+    (normalised -log u from counter stream 2^40 + seed), simulated chain and observations."""
+    log_pi, log_A = dense_model(D, 1000003 + seed)
+    u = uniform((1 << 40) + seed, 0, D * V)
+    e = -np.log(np.maximum(u, 1e-300)).reshape(D, V)
+    B = e / e.sum(1, keepdims=True)
+    states, obs = simulate_discrete(np.exp(log_pi.astype(np.float64)), np.exp(log_A.astype(np.float64)), B, T, seed)
+    return SymbolWorkload(log_pi, log_A, np.log(B).astype(np.float32), obs.astype(np.uint8), states,
+                          f"discrete_D{D}_V{V}_T{T}_s{seed}")
+
+
 def dense_model(D: int, seed: int):
     log_pi = np.empty(D, np.float32); log_A = np.empty((D, D), np.float32)
     _L().hmmgen_dense_model(D, seed, _ptr(log_pi), _ptr(log_A), None)
