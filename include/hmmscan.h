@@ -103,6 +103,22 @@ hmm_status_t hmm_smooth_stats(int D, int64_t T, const float* log_pi, const float
                               void* stream);
 
 /*
+ * Symbol-input variants: discrete observations y_t in [0, V) with emission matrix
+ * log_B[d*V + v] = log p(y_t = v | x_t = d) (the O matrix of the paper's GE channel);
+ * the elements use log_lik_t(d) = log_B[d*V + y_t] (Eq. 5b), gathered on chip from a table, so the
+ * input is 1 byte per step instead of 4*D.  Outputs and semantics as hmm_smooth / hmm_viterbi.
+ * 1 <= D <= 8, 1 <= V <= 256, one sequence; y 4-byte aligned, outputs 16-byte aligned.  A symbol
+ * >= V or a NaN / +inf entry of log_B is reported as info = -1.  Workspace:
+ * hmm_workspace_size(HMM_OP_SMOOTH or HMM_OP_VITERBI, D, T, 1).
+ */
+hmm_status_t hmm_smooth_symbols(int D, int V, int64_t T, const float* log_pi, const float* log_A, const float* log_B,
+                                const uint8_t* y, float* filtered, float* smoothed, double* log_likelihood,
+                                int32_t* info, void* workspace, size_t workspace_bytes, void* stream);
+hmm_status_t hmm_viterbi_symbols(int D, int V, int64_t T, const float* log_pi, const float* log_A, const float* log_B,
+                                 const uint8_t* y, int32_t* path, double* log_prob, int32_t* info, void* workspace,
+                                 size_t workspace_bytes, void* stream);
+
+/*
  * Parallel max-product MAP (Viterbi) — Definition 5 / Propositions 2-3 for the
  * forward max-potentials, argmax backpointers (Alg. 4 line 5) and a parallel
  * backtrack by composition of chunk backpointer maps (DESIGN.md §"Viterbi").

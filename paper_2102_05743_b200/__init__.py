@@ -56,6 +56,10 @@ def lib() -> ctypes.CDLL:
         L.hmm_debug_plan.argtypes = [i32, i32, i64, i64, p]
         L.hmm_smooth_stats.argtypes = [i32, i64, p, p, p, p, p, p, p, p, p, p, sz, p]
         L.hmm_smooth_stats.restype = i32
+        L.hmm_smooth_symbols.argtypes = [i32, i32, i64, p, p, p, p, p, p, p, p, p, sz, p]
+        L.hmm_smooth_symbols.restype = i32
+        L.hmm_viterbi_symbols.argtypes = [i32, i32, i64, p, p, p, p, p, p, p, p, sz, p]
+        L.hmm_viterbi_symbols.restype = i32
         L.hmm_debug_force_path.argtypes = [i32]
         L.hmm_debug_force_path.restype = None
         L.hmm_debug_plan.restype = i32
@@ -188,6 +192,46 @@ def smooth_stats(log_pi, log_A, log_lik, want_marginals: bool = True, stream=Non
                                 _ptr(xi), _ptr(g), _ptr(info), _ptr(ws), ws.numel(), _stream(stream))
     _check(st, "hmm_smooth_stats")
     return filt, sm, lz, xi, g, info
+
+
+def _sym_inputs(log_pi, log_A, log_B, y):
+    for name, t in (("log_pi", log_pi), ("log_A", log_A), ("log_B", log_B), ("y", y)):
+        if not t.is_cuda:
+            raise HmmError(f"{name} must be a CUDA tensor (no CPU path)")
+    if y.dtype != torch.uint8 or y.dim() != 1 or not y.is_contiguous():
+        raise HmmError("y: contiguous uint8 [T]")
+    D, V = log_B.shape
+    return D, V, y.numel()
+
+
+def smooth_symbols(log_pi, log_A, log_B, y, want_filtered: bool = True, stream=None):
+    """Smoother over discrete observations y [T] uint8 with emissions log_B [D, V].
+    Returns (filtered or None, smoothed, log_likelihood [1], info [1])."""
+    D, V, T = _sym_inputs(log_pi, log_A, log_B, y)
+    dev = y.device
+    filt = torch.empty((T, D), dtype=torch.float32, device=dev) if want_filtered else None
+    sm = torch.empty((T, D), dtype=torch.float32, device=dev)
+    lz = torch.empty(1, dtype=torch.float64, device=dev)
+    info = torch.empty(1, dtype=torch.int32, device=dev)
+    ws = workspace(HMM_OP_SMOOTH, D, T, 1, dev)
+    st = lib().hmm_smooth_symbols(D, V, T, _ptr(log_pi), _ptr(log_A), _ptr(log_B), _ptr(y), _ptr(filt), _ptr(sm),
+                                  _ptr(lz), _ptr(info), _ptr(ws), ws.numel(), _stream(stream))
+    _check(st, "hmm_smooth_symbols")
+    return filt, sm, lz, info
+
+
+def viterbi_symbols(log_pi, log_A, log_B, y, stream=None):
+    """MAP path over discrete observations.  Returns (path [T] int32, log_prob [1], info [1])."""
+    D, V, T = _sym_inputs(log_pi, log_A, log_B, y)
+    dev = y.device
+    path = torch.empty(T, dtype=torch.int32, device=dev)
+    lp = torch.empty(1, dtype=torch.float64, device=dev)
+    info = torch.empty(1, dtype=torch.int32, device=dev)
+    ws = workspace(HMM_OP_VITERBI, D, T, 1, dev)
+    st = lib().hmm_viterbi_symbols(D, V, T, _ptr(log_pi), _ptr(log_A), _ptr(log_B), _ptr(y), _ptr(path), _ptr(lp),
+                                   _ptr(info), _ptr(ws), ws.numel(), _stream(stream))
+    _check(st, "hmm_viterbi_symbols")
+    return path, lp, info
 
 
 def viterbi(log_pi, log_A, log_lik, out=None, ws=None, stream=None):

@@ -367,6 +367,38 @@ hmm_status_t run_stats(int D, int64_t T, const float* log_pi, const float* log_A
     return e == cudaSuccess ? HMM_SUCCESS : HMM_ERR_CUDA;
 }
 
+// Symbol inputs: log_lik_t(d) = log_B[d][y_t] gathered on chip; lane-streaming
+// kernel (OP 3 smoother, OP 4 Viterbi), D <= 8, one sequence.
+hmm_status_t run_symbols(int op, int D, int V, int64_t T, const float* log_pi, const float* log_A, const float* log_B,
+                         const uint8_t* y, float* filtered, float* smoothed, int32_t* path, double* scalar,
+                         int32_t* info, void* ws, size_t ws_bytes, void* stream) {
+    if (D < 1 || T < 1 || V < 1 || V > hmm::kStreamMaxV) return HMM_ERR_INVALID_VALUE;
+    if (D > 8) return HMM_ERR_UNSUPPORTED;
+    if (!log_pi || !log_A || !log_B || !y || !scalar || !info) return HMM_ERR_INVALID_VALUE;
+    if (op == 0 && !smoothed) return HMM_ERR_INVALID_VALUE;
+    if (op == 1 && !path) return HMM_ERR_INVALID_VALUE;
+    if (!al4(log_pi) || !al4(log_A) || !al4(log_B) || !al4(y) || !al8(scalar) || !al4(info)) return HMM_ERR_INVALID_VALUE;
+    if ((filtered && !al16(filtered)) || (smoothed && !al16(smoothed)) || (path && !al16(path)))
+        return HMM_ERR_INVALID_VALUE;
+    StPlan SP;
+    if (!make_stream_plan(D, op, T, SP)) return HMM_ERR_UNSUPPORTED;
+    if (!ws || ws_bytes < SP.ws_total || (reinterpret_cast<uintptr_t>(ws) & 255u)) return HMM_ERR_WORKSPACE;
+    hmm::SParams sp;
+    std::memset(&sp, 0, sizeof(sp));
+    sp.T = T; sp.n = SP.n; sp.K = SP.K;
+    sp.log_pi = log_pi; sp.log_A = log_A; sp.log_lik = nullptr;
+    sp.y = y; sp.log_B = log_B; sp.V = V;
+    sp.filtered = filtered; sp.smoothed = smoothed; sp.path = path; sp.scalar_out = scalar; sp.info = info;
+    sp.ws = static_cast<uint8_t*>(ws);
+    sp.ws_sync = SP.ws_sync; sp.ws_slots = SP.ws_slots; sp.slot_bytes = SP.slot_bytes; sp.ws_q = SP.ws_q;
+    sp.ws_lagg = SP.ws_lagg; sp.ws_bp = SP.ws_bp; sp.ws_lmap = SP.ws_lmap;
+    sp.L = hmm::stream_smem_layout(D, SP.G);
+    sp.timers = t_timers;
+    sp.mode = hmm::HMM_MODE_FULL; sp.world = 1;
+    cudaError_t e = hmm::launch_stream(D, op == 0 ? 3 : 4, (unsigned)SP.G, sp, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? HMM_SUCCESS : HMM_ERR_CUDA;
+}
+
 }  // namespace
 
 extern "C" {
@@ -434,6 +466,20 @@ hmm_status_t hmm_smooth_stats(int D, int64_t T, const float* log_pi, const float
                               double* gamma_sum, int32_t* info, void* workspace, size_t workspace_bytes, void* stream) {
     return run_stats(D, T, log_pi, log_A, log_lik, filtered, smoothed, log_likelihood, xi_sum, gamma_sum, info,
                      workspace, workspace_bytes, stream);
+}
+
+hmm_status_t hmm_smooth_symbols(int D, int V, int64_t T, const float* log_pi, const float* log_A, const float* log_B,
+                                const uint8_t* y, float* filtered, float* smoothed, double* log_likelihood, int32_t* info,
+                                void* workspace, size_t workspace_bytes, void* stream) {
+    return run_symbols(0, D, V, T, log_pi, log_A, log_B, y, filtered, smoothed, nullptr, log_likelihood, info,
+                       workspace, workspace_bytes, stream);
+}
+
+hmm_status_t hmm_viterbi_symbols(int D, int V, int64_t T, const float* log_pi, const float* log_A, const float* log_B,
+                                 const uint8_t* y, int32_t* path, double* log_prob, int32_t* info, void* workspace,
+                                 size_t workspace_bytes, void* stream) {
+    return run_symbols(1, D, V, T, log_pi, log_A, log_B, y, nullptr, nullptr, path, log_prob, info, workspace,
+                       workspace_bytes, stream);
 }
 
 hmm_status_t hmm_viterbi(int D, int64_t T, const float* log_pi, const float* log_A, const float* log_lik,

@@ -148,8 +148,9 @@ __host__ __device__ constexpr int stream_pitch(int D) { return stream_s(D) * D *
 __host__ __device__ constexpr int stream_qb(int D) { return (D * D * 4 + 15) & ~15; }
 
 struct StreamLayout {
-    size_t ring, qbuf, tree, maps, ends, stage, misc, total;
+    size_t ring, qbuf, tab, tree, maps, ends, stage, misc, total;
 };
+constexpr int kStreamMaxV = 256;  // symbol alphabet of the symbol-input entry points (uint8 y)
 __host__ __device__ inline StreamLayout stream_smem_layout(int D, int G) {
     const int NT = stream_nt(D), NE = small_ne(D);
     StreamLayout L{};
@@ -162,7 +163,8 @@ __host__ __device__ inline StreamLayout stream_smem_layout(int D, int G) {
     size_t u = L.stage + align16((size_t)G * small_slot_bytes(D));
     if (u < ring) u = ring;
     L.qbuf = align16(u);
-    L.misc = L.qbuf + (size_t)NT * stream_qb(D);
+    L.tab = L.qbuf + (size_t)NT * stream_qb(D);   // symbol table log_B^T [V][D] (symbol inputs)
+    L.misc = L.tab + align16((size_t)kStreamMaxV * D * 4);
     L.total = align16(L.misc + 512);
     return L;
 }
@@ -188,6 +190,9 @@ struct SParams {
     size_t ws_stats; // smoother statistics: [G][D*D + D] fp64 CTA partials
     double* xi_out;    // [D*D] sum_t xi_t (E-step statistics), or unused
     double* gamma_out; // [D]   sum_t gamma_t
+    const uint8_t* y;  // symbol inputs (OP 3/4): y[T] and log_B[D][V]; log_lik rows are gathered on chip
+    const float* log_B;
+    int V;
     StreamLayout L;
     unsigned long long* timers;
     int mode, rank, world;

@@ -424,8 +424,9 @@ __global__ void __launch_bounds__(stream_nt(D)) hmm_stream_kernel(const SParams 
     constexpr int BPW = st_bpw<D>(S);     // backpointer words per slice
     constexpr int BPB = small_bpb(D);     // backpointer bytes per step
     constexpr int NCB = S * BPB / 8;      // 8-B chunks of one lane's backpointer slice
-    constexpr bool MP = (OP == 1);
+    constexpr bool MP = (OP == 1 || OP == 4);
     constexpr bool STATS = (OP == 2);  // smoother + Baum-Welch E-step statistics
+    constexpr bool SYM = (OP >= 3);    // symbol inputs y[T], log_B[D][V]
     constexpr int NN = 2 * NT;
     extern __shared__ __align__(128) uint8_t smem[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -491,6 +492,16 @@ __global__ void __launch_bounds__(stream_nt(D)) hmm_stream_kernel(const SParams 
     double acc = 0.0;
     int64_t zero_t = INT64_MAX;
     const float* ll = p.log_lik;
+    float* tab = reinterpret_cast<float*>(smem + p.L.tab);  // [V][D] = log_B transposed (symbol inputs)
+    if constexpr (SYM) {
+        for (int e = tid; e < p.V * D; e += NT) {
+            const int v = e / D, d = e - v * D;
+            const float x = __ldg(p.log_B + d * p.V + v);
+            tab[e] = x;
+            if (x != x || (x == INFINITY)) bad = true;  // NaN / +inf in log_B (reported like log_lik)
+        }
+        __syncthreads();
+    }
     // lane's slot in ring stage st
     auto slot = [&](int st) -> float* {
         return reinterpret_cast<float*>(ring + (size_t)st * NT * PITCH + (size_t)tid * PITCH);
@@ -510,6 +521,19 @@ __global__ void __launch_bounds__(stream_nt(D)) hmm_stream_kernel(const SParams 
     // async load of slice k of the warp's lanes into ring stage st (one cp.async group per call)
     auto coop_load = [&](int k, int st) {
         uint8_t* sbase = ring + (size_t)st * NT * PITCH + (size_t)warp * 32 * PITCH;
+        if constexpr (SYM) {  // the warp's 32 lane slices of symbols: S bytes each, 4-B chunks, zero-filled
+            constexpr int NCY = S / 4;
+#pragma unroll
+            for (int it = 0; it < NCY; it++) {
+                const int q = lane + 32 * it, j = q / NCY, cy = q - j * NCY;
+                const int64_t r0 = wbase + (int64_t)j * n + (int64_t)k * S + 4 * cy;
+                const int64_t rem = T - r0;
+                const uint32_t nb = rem <= 0 ? 0u : (rem >= 4 ? 4u : (uint32_t)rem);
+                cp_async4_zfill(sbase + (size_t)j * PITCH + 4 * cy, nb ? (const void*)(p.y + r0) : (const void*)p.y, nb);
+            }
+            cp_async_commit();
+            return;
+        }
         bool done = false;
         if constexpr ((32 % CPL) == 0) {
             constexpr int LPI = 32 / CPL;
@@ -610,6 +634,25 @@ __global__ void __launch_bounds__(stream_nt(D)) hmm_stream_kernel(const SParams 
         }
     };
     auto stage_base = [&](int st) -> uint8_t* { return ring + (size_t)st * NT * PITCH; };
+    // symbol inputs: turn this lane's landed symbol slice into log_lik rows in place (row i <- tab[y_i])
+    auto expand = [&](int st, int nr) {
+        if constexpr (SYM) {
+            float* rows = slot(st);
+            uint32_t yw[S / 4];
+#pragma unroll
+            for (int w = 0; w < S / 4; w++) yw[w] = reinterpret_cast<const uint32_t*>(rows)[w];
+#pragma unroll
+            for (int i = 0; i < S; i++) {
+                if (i < nr) {
+                    const int sym = (int)((yw[i >> 2] >> (8 * (i & 3))) & 0xffu);
+                    float v[D];
+                    ld_row<D>(tab + (sym < p.V ? sym : 0) * D, v);
+                    if (sym >= p.V) bad = true;
+                    st_row<D>(rows + i * D, v);
+                }
+            }
+        }
+    };
 
     const bool do_pass1 = (mode == HMM_MODE_FULL || mode == HMM_MODE_REDUCE);
     float P[D * D];
@@ -645,6 +688,7 @@ __global__ void __launch_bounds__(stream_nt(D)) hmm_stream_kernel(const SParams 
             }
             cp_async_wait<2>();
             __syncwarp();
+            expand(st, nr);
             if (nr > 0) {
                 const float* rows = slot(st);
                 if constexpr (MP) {
@@ -806,6 +850,7 @@ __global__ void __launch_bounds__(stream_nt(D)) hmm_stream_kernel(const SParams 
                 mbar_wait(&qbar[warp], qphase);
                 qphase ^= 1u;
                 const int nr = slice_rows(k);
+                expand(st, nr);
                 float beta[D];
                 if (nr > 0) {
                     float Q[D * D];
@@ -874,6 +919,7 @@ __global__ void __launch_bounds__(stream_nt(D)) hmm_stream_kernel(const SParams 
                 cp_async_wait<2>();
                 __syncwarp();
                 const int nr = slice_rows(k);
+                expand(st, nr);
                 if (nr > 0) {
                     uint32_t bpw[BPW];
                     int zi;
@@ -1117,6 +1163,8 @@ static cudaError_t launch_st_op(int D, unsigned G, const SParams& sp, cudaStream
 
 cudaError_t launch_stream(int D, int op, unsigned G, const SParams& sp, cudaStream_t s) {
     if (op == 2) return launch_st_op<2>(D, G, sp, s);
+    if (op == 3) return launch_st_op<3>(D, G, sp, s);
+    if (op == 4) return launch_st_op<4>(D, G, sp, s);
     return op == 0 ? launch_st_op<0>(D, G, sp, s) : launch_st_op<1>(D, G, sp, s);
 }
 
