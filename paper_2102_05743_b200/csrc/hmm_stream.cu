@@ -33,6 +33,18 @@
 namespace hmm {
 
 // ---------------------------------------------------------------------------- slice folds
+// Where step i of a slice reads its log-likelihood row: the staged rows, or (symbol inputs, SURVEY.md
+// §8(f) f1) the emission table row of the staged symbol, log_B[:, y_i] (Eq. 5b).
+template <int D, bool SY>
+struct RowSrc {
+    const float* rows;
+    const uint8_t* ys;
+    const float* tab;
+    __device__ __forceinline__ const float* operator()(int i) const {
+        if constexpr (SY) return tab + (int)ys[i] * D;
+        else return rows + i * D;
+    }
+};
 // Sum-product, right to left over one slice: P <- psi_t P for t = nr-1 .. 0 (psi_t = A diag(l_t),
 // psi_0 = 1 (pi o l_0)^T when the slice starts the sequence).  Renormalisation is exact and free: the
 // power-of-two factor 2^d that brings max(P) into [1,2) is added to the next step's ex2 argument,
@@ -84,17 +96,17 @@ __device__ __forceinline__ void sp_back_step(const float* row, bool t0, const fl
 // One slice, right to left (sum-product).  Unlike the max-product fold below, the sum-product step is
 // issue-bound rather than latency-bound at 8 warps/SM (ncu: 66% issue-active, `wait` stalls 0.34 per
 // issue), so the two-chain split would only add its combine/normalise instructions (~7%): one chain.
-template <int D, int S>
-__device__ __forceinline__ void sp_fold_back(const float* rows, int nr, bool t0, const float* A, const float* pi,
+template <int D, int S, class RS>
+__device__ __forceinline__ void sp_fold_back(const RS rows, int nr, bool t0, const float* A, const float* pi,
                                              float* P, float& d) {
     if (nr == S) {
 #pragma unroll 4
-        for (int ii = S - 1; ii >= 1; ii--) sp_back_step<D>(rows + ii * D, false, A, pi, P, d);
+        for (int ii = S - 1; ii >= 1; ii--) sp_back_step<D>(rows(ii), false, A, pi, P, d);
     } else {
 #pragma unroll 1
-        for (int ii = nr - 1; ii >= 1; ii--) sp_back_step<D>(rows + ii * D, false, A, pi, P, d);
+        for (int ii = nr - 1; ii >= 1; ii--) sp_back_step<D>(rows(ii), false, A, pi, P, d);
     }
-    sp_back_step<D>(rows, t0, A, pi, P, d);
+    sp_back_step<D>(rows(0), t0, A, pi, P, d);
 }
 
 // Max-product (log domain), one step right to left: P(i,j) <- max_k (LA(i,k) + w_t(k) + P(k,j)),
@@ -145,27 +157,27 @@ __device__ __forceinline__ void mp_chain_start(const float* row, const float* LA
         for (int k = 0; k < D; k++) X[i * D + k] = LA[i * D + k] + w[k];
 }
 // Max-product slice fold, two interleaved chains for full slices (as sp_fold_back, Def. 5).
-template <int D, int S>
-__device__ __forceinline__ void mp_fold_back(const float* rows, int nr, bool t0, const float* LA, const float* LP,
+template <int D, int S, class RS>
+__device__ __forceinline__ void mp_fold_back(const RS rows, int nr, bool t0, const float* LA, const float* LP,
                                              float* P, float& chk) {
     if (nr == S) {
         constexpr int H = S / 2;
         float X[D * D], Y[D * D];
-        mp_chain_start<D>(rows + (S - 1) * D, LA, X, chk);
-        mp_chain_start<D>(rows + (H - 1) * D, LA, Y, chk);
+        mp_chain_start<D>(rows(S - 1), LA, X, chk);
+        mp_chain_start<D>(rows(H - 1), LA, Y, chk);
 #pragma unroll 2
         for (int q = 1; q < H - 1; q++) {
-            mp_back_step<D>(rows + (S - 1 - q) * D, false, LA, LP, X, chk);
-            mp_back_step<D>(rows + (H - 1 - q) * D, false, LA, LP, Y, chk);
+            mp_back_step<D>(rows(S - 1 - q), false, LA, LP, X, chk);
+            mp_back_step<D>(rows(H - 1 - q), false, LA, LP, Y, chk);
         }
-        mp_back_step<D>(rows + H * D, false, LA, LP, X, chk);
-        mp_back_step<D>(rows, t0, LA, LP, Y, chk);
+        mp_back_step<D>(rows(H), false, LA, LP, X, chk);
+        mp_back_step<D>(rows(0), t0, LA, LP, Y, chk);
         float XP[D * D];
         mat_op<D, true>(X, P, XP);
         mat_op<D, true>(Y, XP, P);
     } else {
 #pragma unroll 1
-        for (int ii = nr - 1; ii >= 0; ii--) mp_back_step<D>(rows + ii * D, ii == 0 && t0, LA, LP, P, chk);
+        for (int ii = nr - 1; ii >= 0; ii--) mp_back_step<D>(rows(ii), ii == 0 && t0, LA, LP, P, chk);
     }
 }
 
@@ -175,10 +187,10 @@ __device__ __forceinline__ void mp_fold_back(const float* rows, int nr, bool t0,
 // fp32 within the slice (<= 64 terms) and added to the fp64 total once per slice.  Rows are turned
 // into l_t in place; filtered rows go to `frows`.  Returns the first zero-mass row, or -1.
 template <int D>
-__device__ __forceinline__ bool sp_alpha_step(float* row, float* frow, bool t0, const float* A, const float* pi,
-                                              float* alpha, float& rprod, int& rexp, float& msl) {
+__device__ __forceinline__ bool sp_alpha_step(const float* srow, float* row, float* frow, bool t0, const float* A,
+                                              const float* pi, float* alpha, float& rprod, int& rexp, float& msl) {
     float l[D];
-    ld_row<D>(row, l);
+    ld_row<D>(srow, l);
     const float m = vmax<D>(l);
     const bool ok = m > -FLT_MAX;  // false: impossible step (all -inf), l = 0
     msl += ok ? m : 0.0f;
@@ -210,22 +222,24 @@ __device__ __forceinline__ bool sp_alpha_step(float* row, float* frow, bool t0, 
     rprod = __uint_as_float((bits & 0x807fffffu) | 0x3f800000u);
     return c > 0.0f;
 }
-template <int D, int S>
-__device__ __forceinline__ int sp_alpha_slice(float* rows, float* frows, int nr, bool t0, const float* A,
+template <int D, int S, class RS>
+__device__ __forceinline__ int sp_alpha_slice(const RS src, float* rows, float* frows, int nr, bool t0, const float* A,
                                               const float* pi, float* alpha, float& rprod, int& rexp,
                                               double& msum) {
     int zero_i = -1;
     float msl = 0.0f;
-    if (!sp_alpha_step<D>(rows, frows, t0, A, pi, alpha, rprod, rexp, msl)) zero_i = 0;
+    if (!sp_alpha_step<D>(src(0), rows, frows, t0, A, pi, alpha, rprod, rexp, msl)) zero_i = 0;
     if (nr == S) {
 #pragma unroll 4
         for (int i = 1; i < S; i++)
-            if (!sp_alpha_step<D>(rows + i * D, frows + i * D, false, A, pi, alpha, rprod, rexp, msl) && zero_i < 0)
+            if (!sp_alpha_step<D>(src(i), rows + i * D, frows + i * D, false, A, pi, alpha, rprod, rexp, msl) &&
+                zero_i < 0)
                 zero_i = i;
     } else {
 #pragma unroll 1
         for (int i = 1; i < nr; i++)
-            if (!sp_alpha_step<D>(rows + i * D, frows + i * D, false, A, pi, alpha, rprod, rexp, msl) && zero_i < 0)
+            if (!sp_alpha_step<D>(src(i), rows + i * D, frows + i * D, false, A, pi, alpha, rprod, rexp, msl) &&
+                zero_i < 0)
                 zero_i = i;
     }
     msum += (double)msl;
@@ -341,8 +355,8 @@ __device__ __forceinline__ void sp_beta_slice_stats(float* lrows, const float* f
 // one 16-bit nibble word per step, two steps per u32; D > 4: one u32 per step), returns the slice
 // map f(x_end) = state before the slice, accumulates sum (o_t + m_t).
 template <int D> __host__ __device__ constexpr int st_bpw(int S) { return D <= 4 ? S / 2 : S; }
-template <int D, int S>
-__device__ __forceinline__ uint64_t vit_fwd_slice(const float* rows, int nr, bool t0, const float* LA,
+template <int D, int S, class RS>
+__device__ __forceinline__ uint64_t vit_fwd_slice(const RS rows, int nr, bool t0, const float* LA,
                                                   const float* LP, float* V, double& lp, int& zero_i,
                                                   uint32_t* bpw) {
     uint32_t olo = 0x03020100u, ohi = 0x07060504u;
@@ -355,7 +369,7 @@ __device__ __forceinline__ uint64_t vit_fwd_slice(const float* rows, int nr, boo
     for (int i = 0; i < S; i++) {
         if (i < nr) {
             float v[D];
-            ld_row<D>(rows + i * D, v);
+            ld_row<D>(rows(i), v);
             float m = vmax<D>(v);
             if (!(m > neg_inf())) m = 0.0f;
             float Vh[D];
@@ -512,6 +526,10 @@ __global__ void __launch_bounds__(stream_nt(D)) hmm_stream_kernel(const SParams 
     // slices with 16-B per-thread accesses, CPL consecutive threads per lane slice: cp.async (LDGSTS)
     // for loads into the ring, LDS + streaming STG.128 for stores -- fully coalesced segments.
     constexpr int CPL = S * D / 4;  // 16-B chunks per full lane slice
+    // symbol inputs: the S symbol bytes of a lane slice sit at the END of its row area, so the in-order
+    // sweep that overwrites rows with l_t (smoother pass 2) only ever overwrites symbols it has consumed:
+    // row i ends at byte 4D(i+1) <= YOFF + i + 1 for every i < S.
+    constexpr int YOFF = S * D * 4 - S;
     const int64_t wbase = ((int64_t)c * NT + warp * 32) * n;  // first step of this warp's lane 0
     auto lane_rows = [&](int j, int k) -> int {
         const int64_t rem = T - (wbase + (int64_t)j * n + (int64_t)k * S);
@@ -529,7 +547,8 @@ __global__ void __launch_bounds__(stream_nt(D)) hmm_stream_kernel(const SParams 
                 const int64_t r0 = wbase + (int64_t)j * n + (int64_t)k * S + 4 * cy;
                 const int64_t rem = T - r0;
                 const uint32_t nb = rem <= 0 ? 0u : (rem >= 4 ? 4u : (uint32_t)rem);
-                cp_async4_zfill(sbase + (size_t)j * PITCH + 4 * cy, nb ? (const void*)(p.y + r0) : (const void*)p.y, nb);
+                cp_async4_zfill(sbase + (size_t)j * PITCH + YOFF + 4 * cy, nb ? (const void*)(p.y + r0) : (const void*)p.y,
+                                nb);
             }
             cp_async_commit();
             return;
@@ -634,24 +653,21 @@ __global__ void __launch_bounds__(stream_nt(D)) hmm_stream_kernel(const SParams 
         }
     };
     auto stage_base = [&](int st) -> uint8_t* { return ring + (size_t)st * NT * PITCH; };
-    // symbol inputs: turn this lane's landed symbol slice into log_lik rows in place (row i <- tab[y_i])
-    auto expand = [&](int st, int nr) {
+    // row source of slice k in ring stage st; symbol inputs are range-checked once per slice
+    auto rsrc = [&](int st, int nr) -> RowSrc<D, SYM> {
+        const float* rows = slot(st);
+        const uint8_t* ys = reinterpret_cast<const uint8_t*>(rows) + YOFF;
         if constexpr (SYM) {
-            float* rows = slot(st);
-            uint32_t yw[S / 4];
+            if (p.V < 256) {
+                const uint32_t vrep = 0x01010101u * (uint32_t)p.V;
+                uint32_t badw = 0;
 #pragma unroll
-            for (int w = 0; w < S / 4; w++) yw[w] = reinterpret_cast<const uint32_t*>(rows)[w];
-#pragma unroll
-            for (int i = 0; i < S; i++) {
-                if (i < nr) {
-                    const int sym = (int)((yw[i >> 2] >> (8 * (i & 3))) & 0xffu);
-                    float v[D];
-                    ld_row<D>(tab + (sym < p.V ? sym : 0) * D, v);
-                    if (sym >= p.V) bad = true;
-                    st_row<D>(rows + i * D, v);
-                }
+                for (int w = 0; w < S / 4; w++)
+                    if (4 * w < nr) badw |= __vcmpgeu4(reinterpret_cast<const uint32_t*>(ys)[w], vrep);
+                if (badw) bad = true;  // (the zero-filled bytes past the sequence end are symbol 0: valid)
             }
         }
+        return RowSrc<D, SYM>{rows, ys, tab};
     };
 
     const bool do_pass1 = (mode == HMM_MODE_FULL || mode == HMM_MODE_REDUCE);
@@ -688,9 +704,8 @@ __global__ void __launch_bounds__(stream_nt(D)) hmm_stream_kernel(const SParams 
             }
             cp_async_wait<2>();
             __syncwarp();
-            expand(st, nr);
             if (nr > 0) {
-                const float* rows = slot(st);
+                const RowSrc<D, SYM> rows = rsrc(st, nr);
                 if constexpr (MP) {
                     mp_fold_back<D, S>(rows, nr, lane_t0 && k == 0, A, pv, P, chk);
                     const float m = vmax<D * D>(P);  // renormalise once per slice (max 0)
@@ -850,7 +865,6 @@ __global__ void __launch_bounds__(stream_nt(D)) hmm_stream_kernel(const SParams 
                 mbar_wait(&qbar[warp], qphase);
                 qphase ^= 1u;
                 const int nr = slice_rows(k);
-                expand(st, nr);
                 float beta[D];
                 if (nr > 0) {
                     float Q[D * D];
@@ -866,8 +880,8 @@ __global__ void __launch_bounds__(stream_nt(D)) hmm_stream_kernel(const SParams 
                     float aprev[D];
 #pragma unroll
                     for (int d = 0; d < D; d++) aprev[d] = alpha[d];
-                    const int zi = sp_alpha_slice<D, S>(rows, frows, nr, lane_t0 && k == 0, A, pv, alpha, rprod,
-                                                        rexp, msum);
+                    const int zi = sp_alpha_slice<D, S>(rsrc(st, nr), rows, frows, nr, lane_t0 && k == 0, A, pv, alpha,
+                                                        rprod, rexp, msum);
                     const int64_t r0 = a0 + (int64_t)k * S;
                     if (zi >= 0 && tb + r0 + zi < zero_t) zero_t = tb + r0 + zi;
                     if constexpr (STATS)
@@ -919,11 +933,10 @@ __global__ void __launch_bounds__(stream_nt(D)) hmm_stream_kernel(const SParams 
                 cp_async_wait<2>();
                 __syncwarp();
                 const int nr = slice_rows(k);
-                expand(st, nr);
                 if (nr > 0) {
                     uint32_t bpw[BPW];
                     int zi;
-                    const uint64_t f = vit_fwd_slice<D, S>(slot(st), nr, lane_t0 && k == 0, A, pv, V, acc, zi, bpw);
+                    const uint64_t f = vit_fwd_slice<D, S>(rsrc(st, nr), nr, lane_t0 && k == 0, A, pv, V, acc, zi, bpw);
                     const int64_t r0 = a0 + (int64_t)k * S;
                     if (zi >= 0 && tb + r0 + zi < zero_t) zero_t = tb + r0 + zi;
                     F = map_compose<D>(F, f);
