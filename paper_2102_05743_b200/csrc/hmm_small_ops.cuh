@@ -707,13 +707,16 @@ __device__ __forceinline__ uint64_t vit_sweep(const float* rows, void* bprow, in
 #pragma unroll
         for (int j = 0; j < D; j++) {
             const bool first = t0 && i == 0;
-            float best = V[0] + (first ? LP[j] : LA[j]);
-            int arg = 0;
+            float sc[D];
 #pragma unroll
-            for (int k = 1; k < D; k++) {
-                const float sc = V[k] + (first ? LP[j] : LA[k * D + j]);
-                if (sc > best) { best = sc; arg = k; }
-            }
+            for (int k = 0; k < D; k++) sc[k] = V[k] + (first ? LP[j] : LA[k * D + j]);
+            // max by a 2-input tree (short V critical path); argmax = smallest index attaining it
+            float best;
+            if constexpr (D == 4) best = fmaxf(fmaxf(sc[0], sc[1]), fmaxf(sc[2], sc[3]));
+            else best = vmax<D>(sc);
+            int arg = D - 1;
+#pragma unroll
+            for (int k = D - 2; k >= 0; k--) arg = (sc[k] == best) ? k : arg;
             Vh[j] = best + (v[j] - m);
             sel |= (uint32_t)arg << (4 * j);
         }

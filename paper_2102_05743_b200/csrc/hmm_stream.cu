@@ -361,8 +361,7 @@ __device__ __forceinline__ uint64_t vit_fwd_slice(const RS rows, int nr, bool t0
                                                   uint32_t* bpw) {
     uint32_t olo = 0x03020100u, ohi = 0x07060504u;
     zero_i = -1;
-    float acc = 0.0f;
-    double dacc = 0.0;
+    float facc = 0.0f;  // sum of (o_t + m_t) over the slice (<= 64 terms), added to the fp64 total once
 #pragma unroll
     for (int i = 0; i < st_bpw<D>(S); i++) bpw[i] = 0u;
 #pragma unroll
@@ -377,13 +376,17 @@ __device__ __forceinline__ uint64_t vit_fwd_slice(const RS rows, int nr, bool t0
 #pragma unroll
             for (int j = 0; j < D; j++) {
                 const bool first = t0 && i == 0;
-                float best = V[0] + (first ? LP[j] : LA[j]);
-                int arg = 0;
+                float sc[D];
 #pragma unroll
-                for (int k = 1; k < D; k++) {
-                    const float sc = V[k] + (first ? LP[j] : LA[k * D + j]);
-                    if (sc > best) { best = sc; arg = k; }
-                }
+                for (int k = 0; k < D; k++) sc[k] = V[k] + (first ? LP[j] : LA[k * D + j]);
+                // the max by a 2-input tree keeps the V recursion's critical path short; the argmax
+                // (smallest index attaining it: DESIGN.md reading 5) hangs off it
+                float best;
+                if constexpr (D == 4) best = fmaxf(fmaxf(sc[0], sc[1]), fmaxf(sc[2], sc[3]));
+                else best = vmax<D>(sc);
+                int arg = D - 1;
+#pragma unroll
+                for (int k = D - 2; k >= 0; k--) arg = (sc[k] == best) ? k : arg;
                 Vh[j] = best + (v[j] - m);
                 sel |= (uint32_t)arg << (4 * j);
             }
@@ -394,7 +397,7 @@ __device__ __forceinline__ uint64_t vit_fwd_slice(const RS rows, int nr, bool t0
             }
 #pragma unroll
             for (int j = 0; j < D; j++) V[j] = Vh[j] - o;
-            dacc += (double)(o + m);
+            facc += o + m;
             if constexpr (D <= 4) {
                 bpw[i >> 1] |= sel << (16 * (i & 1));
                 olo = __byte_perm(olo, 0u, sel);
@@ -406,7 +409,7 @@ __device__ __forceinline__ uint64_t vit_fwd_slice(const RS rows, int nr, bool t0
             }
         }
     }
-    (void)acc;
+    const double dacc = (double)facc;
     lp += dacc;
     uint64_t f = ((uint64_t)ohi << 32) | olo;
     if constexpr (D < 8) f &= (1ull << (8 * D)) - 1ull;
