@@ -1026,66 +1026,82 @@ __global__ void __launch_bounds__(stream_nt(D)) hmm_stream_kernel(const SParams 
             map_tree_down(maps, ends, NT, flag[1]);
             int x = ends[NT + tid];
             HMM_STAMP(7);
-            // ===================== pass 3: backtrack right to left.  The warps' backpointer slices
-            // stream through a deep ring of dense 8-B-chunk stages (cp.async, NSB-1 slices ahead); the
-            // path slice of every lane is staged in SMEM and leaves by coalesced 16-B stores.
+            // ===================== pass 3: backtrack right to left, U slices at a time ("super-slice":
+            // ~256 B of path per lane, so every lane's path leaves as full 128-B lines -- 64-B runs
+            // scattered over 37k lanes cost DRAM row locality).  Backpointers stream through a 3-stage
+            // cp.async ring of 8-B chunks; the path is staged in SMEM and stored with coalesced 16-B
+            // stores.
             __syncthreads();  // the map trees above live in the ring region
-            constexpr int BPS = S * BPB;                       // backpointer bytes per lane slice
-            constexpr int PPITCH = S * 4 + 16;                 // path slot pitch
-            constexpr int NSB_CAP = (3 * PITCH - PPITCH) / BPS;   // stages that fit in the ring region
-            constexpr int NSB_BW = 98304 / (NT * BPS);             // ~96 KB of backpointers in flight
-            constexpr int NSB0 = NSB_BW < NSB_CAP ? NSB_BW : NSB_CAP;
-            constexpr int NSB = NSB0 < 2 ? 2 : (NSB0 > 16 ? 16 : NSB0);
-            static_assert(NSB * BPS + PPITCH <= 3 * PITCH, "pass-3 staging exceeds the ring");
-            uint8_t* bring = ring;                              // [NSB][NT][BPS]
-            uint8_t* pbuf = ring + (size_t)NSB * NT * BPS;      // [NT][PPITCH]
-            auto bp_load = [&](int k, int sb) {
-                uint8_t* sbase = bring + ((size_t)sb * NT + warp * 32) * BPS;
+            constexpr int BPS = S * BPB;                                   // backpointer bytes per lane slice
+            constexpr int U_RUN = (256 / (S * 4)) < 1 ? 1 : 256 / (S * 4);
+            constexpr int U_FIT = (3 * PITCH - 16) / (3 * BPS + S * 4);
+            constexpr int U = U_RUN < U_FIT ? U_RUN : U_FIT;              // slices per super-slice
+            constexpr int SBS = U * BPS;                                   // backpointer bytes per lane per stage
+            constexpr int PPITCH = U * S * 4 + 16;                         // path slot pitch
+            static_assert(U >= 1 && 3 * SBS + PPITCH <= 3 * PITCH, "pass-3 staging exceeds the ring");
+            constexpr int NCU = SBS / 8;                                   // 8-B chunks per lane per stage
+            constexpr int PCU = U * S / 4;                                 // 16-B path chunks per lane
+            const int KU = (K + U - 1) / U;
+            uint8_t* bring = ring;                              // [3][NT][SBS]
+            uint8_t* pbuf = ring + (size_t)3 * NT * SBS;        // [NT][PPITCH]
+            const int64_t lane_end_w = T - wbase;               // steps from this warp's lane 0 to the end
+            auto bp_load = [&](int u, int sb) {
+                uint8_t* sbase = bring + ((size_t)sb * NT + warp * 32) * SBS;
 #pragma unroll
-                for (int it = 0; it < NCB; it++) {
-                    const int q = lane + 32 * it, j = q / NCB, ch = q - j * NCB;
-                    const bool ok = k >= 0 && lane_rows(j, k) > 0;
-                    const uint8_t* src = ok ? bpg + (size_t)(wbase + (int64_t)j * n + (int64_t)k * S) * BPB + ch * 8 : bpg;
-                    cp_async8_zfill(sbase + (size_t)j * BPS + ch * 8, src, ok ? 8u : 0u);
+                for (int it = 0; it < NCU; it++) {
+                    const int q = lane + 32 * it, j = q / NCU, rem = q - j * NCU;
+                    const int64_t so = (int64_t)u * U * S + (8 * rem) / BPB;   // step offset inside the lane
+                    const bool ok = u >= 0 && so < n && (int64_t)j * n + so < lane_end_w;
+                    const uint8_t* src = ok ? bpg + (size_t)(wbase + (int64_t)j * n + (int64_t)u * U * S) * BPB + 8 * rem : bpg;
+                    cp_async8_zfill(sbase + (size_t)j * SBS + 8 * rem, src, ok ? 8u : 0u);
                 }
                 cp_async_commit();
             };
-#pragma unroll 1
-            for (int i = 0; i < NSB - 1; i++) bp_load(K - 1 - i, i % NSB);
-            for (int it = 0; it < K; it++) {
-                const int k = K - 1 - it;
-                bp_load(k - (NSB - 1), (it + NSB - 1) % NSB);
-                cp_async_wait<NSB - 1>();
+            bp_load(KU - 1, 0);
+            if (KU > 1) bp_load(KU - 2, 1); else cp_async_commit();
+            for (int it = 0; it < KU; it++) {
+                const int u = KU - 1 - it;
+                const int sb = it % 3;
+                if (it + 2 < KU) bp_load(u - 2, (it + 2) % 3); else cp_async_commit();
+                cp_async_wait<2>();
                 __syncwarp();
-                const int nr = slice_rows(k);
                 int32_t* ps = reinterpret_cast<int32_t*>(pbuf + (size_t)tid * PPITCH);
-                if (nr > 0) {
-                    uint32_t cur[BPW];
-                    const uint2* bs = reinterpret_cast<const uint2*>(bring + ((size_t)(it % NSB) * NT + tid) * BPS);
+                const uint8_t* bsl = bring + ((size_t)sb * NT + tid) * SBS;
+#pragma unroll 1
+                for (int kk = U - 1; kk >= 0; kk--) {
+                    const int k = u * U + kk;
+                    const int nr = (k < K) ? slice_rows(k) : 0;
+                    if (nr > 0) {
+                        uint32_t cur[BPW];
+                        const uint2* bs = reinterpret_cast<const uint2*>(bsl + kk * BPS);
 #pragma unroll
-                    for (int i = 0; i < BPW; i += 2) {
-                        const uint2 v = bs[i / 2];
-                        cur[i] = v.x;
-                        cur[i + 1] = v.y;
+                        for (int i = 0; i < BPW; i += 2) {
+                            const uint2 v = bs[i / 2];
+                            cur[i] = v.x;
+                            cur[i + 1] = v.y;
+                        }
+                        int32_t out[S];
+                        x = vit_back_slice<D, S>(cur, nr, x, out);
+#pragma unroll
+                        for (int i = 0; i < S; i += 4)
+                            *reinterpret_cast<int4*>(ps + kk * S + i) = make_int4(out[i], out[i + 1], out[i + 2], out[i + 3]);
                     }
-                    int32_t out[S];
-                    x = vit_back_slice<D, S>(cur, nr, x, out);
-#pragma unroll
-                    for (int i = 0; i < S; i += 4)
-                        *reinterpret_cast<int4*>(ps + i) = make_int4(out[i], out[i + 1], out[i + 2], out[i + 3]);
                 }
                 __syncwarp();
-                // coalesced path stores: 16-B chunks, the sequence's last chunk word by word
+                // coalesced path stores of the super-slice: 16-B chunks, the sequence's last chunk by words
 #pragma unroll
-                for (int i2 = 0; i2 < S / 4; i2++) {
-                    const int q = lane + 32 * i2, j = q / (S / 4), ch = q - j * (S / 4);
-                    const int nrj = lane_rows(j, k);
+                for (int i2 = 0; i2 < PCU; i2++) {
+                    const int q = lane + 32 * i2, j = q / PCU, ch = q - j * PCU;
+                    const int64_t so = (int64_t)u * U * S + 4 * ch;                 // step offset inside lane j
+                    int64_t lim = lane_end_w - (int64_t)j * n;                      // steps of lane j before T
+                    if (lim > n) lim = n;
+                    const int64_t nv = lim - so;
                     const int32_t* src = reinterpret_cast<const int32_t*>(pbuf + (size_t)(warp * 32 + j) * PPITCH) + 4 * ch;
-                    int32_t* dst = p.path + wbase + (int64_t)j * n + (int64_t)k * S + 4 * ch;
-                    if (4 * ch + 4 <= nrj) {
+                    int32_t* dst = p.path + wbase + (int64_t)j * n + so;
+                    if (nv >= 4) {
                         __stcs(reinterpret_cast<int4*>(dst), *reinterpret_cast<const int4*>(src));
                     } else {
-                        for (int w = 4 * ch; w < nrj; w++) dst[w - 4 * ch] = src[w - 4 * ch];
+                        for (int w = 0; w < nv; w++) dst[w] = src[w];
                     }
                 }
                 __syncwarp();
