@@ -208,6 +208,9 @@ bool make_large_plan(int D, int op, int64_t T, int64_t B, LgPlan& P, bool allow_
     // leaf kernel runs 2 leaf pairs per SM, so it wants ~4 leaves per SM
     const int64_t target = P.tc ? (int64_t)di.sms * 4 : (int64_t)di.sms * 2 * NLB;
     int64_t SL = cdiv(T * B, target);
+    // many sequences (one block each): fill every block's NLB leaf slots -- the leaf chains are
+    // latency-bound, so idle slots cost throughput directly
+    if (!P.tc && B >= di.sms) SL = cdiv(T, NLB);
     if (SL < 16) SL = 16;
     if (SL > (P.tc ? 2048 : 512)) SL = P.tc ? 2048 : 512;
     if (SL > T) SL = T;

@@ -424,22 +424,25 @@ __global__ void __launch_bounds__(64) lg_carry_kernel(const LgParams p) {
         if (tid < DP) {
             out[(size_t)i * DP + tid] = vec[tid];  // the carry entering root i
             const int c = tid >> 2, w = tid & 3;
+            // four independent partial accumulators: the serial chain is latency-bound
+            float y4[4] = {y, y, y, y};
             if (fwd) {
 #pragma unroll 16
                 for (int k = 0; k < DP; k++) {
                     const float mk = M[sw(k, c) + w];
-                    y = MP ? fmaxf(y, vec[k] + mk) : fmaf(vec[k], mk, y);
+                    y4[k & 3] = MP ? fmaxf(y4[k & 3], vec[k] + mk) : fmaf(vec[k], mk, y4[k & 3]);
                 }
             } else {
 #pragma unroll 4
                 for (int cc = 0; cc < CH; cc++) {
                     const float4 m4 = *reinterpret_cast<const float4*>(M + sw(tid, cc));
-                    y = fmaf(m4.x, vec[4 * cc], y);
-                    y = fmaf(m4.y, vec[4 * cc + 1], y);
-                    y = fmaf(m4.z, vec[4 * cc + 2], y);
-                    y = fmaf(m4.w, vec[4 * cc + 3], y);
+                    y4[0] = fmaf(m4.x, vec[4 * cc], y4[0]);
+                    y4[1] = fmaf(m4.y, vec[4 * cc + 1], y4[1]);
+                    y4[2] = fmaf(m4.z, vec[4 * cc + 2], y4[2]);
+                    y4[3] = fmaf(m4.w, vec[4 * cc + 3], y4[3]);
                 }
             }
+            y = MP ? fmaxf(fmaxf(y4[0], y4[1]), fmaxf(y4[2], y4[3])) : (y4[0] + y4[1]) + (y4[2] + y4[3]);
         }
         float m = (tid < DP) ? y : (MP ? neg_inf() : 0.0f);
 #pragma unroll
