@@ -196,34 +196,44 @@ __global__ void __launch_bounds__(256) lg_leaf_kernel(const LgParams p) {
                 __syncwarp();
             } else {
                 float mx = MP ? neg_inf() : 0.0f;
-                for (int r = 0; r < DP; r++) {
-                    float acc[CPL];
+                // rows in groups of RG: row r of P psi depends only on row r of P, so a group is read,
+                // computed with RG independent accumulator chains, then written back in place
+                constexpr int RG = (CPL == 1) ? (DP < 32 ? DP : 16) : 8;
+                for (int r0 = 0; r0 < DP; r0 += RG) {
+                    float acc[RG][CPL];
     #pragma unroll
-                    for (int c = 0; c < CPL; c++) acc[c] = MP ? neg_inf() : 0.0f;
+                    for (int rr = 0; rr < RG; rr++)
     #pragma unroll
-                    for (int k4 = 0; k4 < DP; k4 += 4) {
-                        const float4 x = *reinterpret_cast<const float4*>(Pm + r * DP + k4);
+                        for (int c = 0; c < CPL; c++) acc[rr][c] = MP ? neg_inf() : 0.0f;
     #pragma unroll
-                        for (int c = 0; c < CPL; c++) {
-                            if constexpr (MP) {
-                                acc[c] = fmaxf(acc[c], max3(x.x + Acol[c][k4], x.y + Acol[c][k4 + 1],
-                                                            fmaxf(x.z + Acol[c][k4 + 2], x.w + Acol[c][k4 + 3])));
-                            } else {
-                                acc[c] = fmaf(x.x, Acol[c][k4], acc[c]);
-                                acc[c] = fmaf(x.y, Acol[c][k4 + 1], acc[c]);
-                                acc[c] = fmaf(x.z, Acol[c][k4 + 2], acc[c]);
-                                acc[c] = fmaf(x.w, Acol[c][k4 + 3], acc[c]);
+                    for (int rr = 0; rr < RG; rr++) {
+    #pragma unroll
+                        for (int k4 = 0; k4 < DP; k4 += 4) {
+                            const float4 x = *reinterpret_cast<const float4*>(Pm + (r0 + rr) * DP + k4);
+    #pragma unroll
+                            for (int c = 0; c < CPL; c++) {
+                                if constexpr (MP) {
+                                    acc[rr][c] = fmaxf(acc[rr][c], max3(x.x + Acol[c][k4], x.y + Acol[c][k4 + 1],
+                                                                        fmaxf(x.z + Acol[c][k4 + 2], x.w + Acol[c][k4 + 3])));
+                                } else {
+                                    acc[rr][c] = fmaf(x.x, Acol[c][k4], acc[rr][c]);
+                                    acc[rr][c] = fmaf(x.y, Acol[c][k4 + 1], acc[rr][c]);
+                                    acc[rr][c] = fmaf(x.z, Acol[c][k4 + 2], acc[rr][c]);
+                                    acc[rr][c] = fmaf(x.w, Acol[c][k4 + 3], acc[rr][c]);
+                                }
                             }
                         }
                     }
                     __syncwarp();
                     if (act) {
     #pragma unroll
-                        for (int c = 0; c < CPL; c++) {
-                            const float val = MP ? acc[c] + (l[c] - s) : acc[c] * (l[c] * s);
-                            Pm[r * DP + cl * CPL + c] = val;
-                            mx = fmaxf(mx, val);
-                        }
+                        for (int rr = 0; rr < RG; rr++)
+    #pragma unroll
+                            for (int c = 0; c < CPL; c++) {
+                                const float val = MP ? acc[rr][c] + (l[c] - s) : acc[rr][c] * (l[c] * s);
+                                Pm[(r0 + rr) * DP + cl * CPL + c] = val;
+                                mx = fmaxf(mx, val);
+                            }
                     }
                     __syncwarp();
                 }
