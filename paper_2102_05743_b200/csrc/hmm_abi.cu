@@ -206,7 +206,9 @@ bool make_large_plan(int D, int op, int64_t T, int64_t B, LgPlan& P, bool allow_
     P.tc = (P.DP == 64 && op == 0 && t_force_path != 3 && allow_tc);
     // enough leaves for ~2 waves of 8-warp CTAs, leaves between 16 and 512 steps; the tensor-core
     // leaf kernel runs 2 leaf pairs per SM, so it wants ~4 leaves per SM
-    const int64_t target = P.tc ? (int64_t)di.sms * 4 : (int64_t)di.sms * 2 * NLB;
+    // (tensor-core leaves: 2 leaf pairs per SM per wave; 2 waves so the sweep kernel, NLB leaves
+    // per CTA, still covers every SM)
+    const int64_t target = P.tc ? (int64_t)di.sms * 8 : (int64_t)di.sms * 2 * NLB;
     int64_t SL = cdiv(T * B, target);
     // many sequences (one block each): fill every block's NLB leaf slots -- the leaf chains are
     // latency-bound, so idle slots cost throughput directly
