@@ -1034,16 +1034,17 @@ __global__ void __launch_bounds__(stream_nt(D)) hmm_stream_kernel(const SParams 
             __syncthreads();  // the map trees above live in the ring region
             constexpr int BPS = S * BPB;                                   // backpointer bytes per lane slice
             constexpr int U_RUN = (256 / (S * 4)) < 1 ? 1 : 256 / (S * 4);
-            constexpr int U_FIT = (3 * PITCH - 16) / (3 * BPS + S * 4);
+            constexpr int NS3 = 4;                                         // backpointer ring depth
+            constexpr int U_FIT = (3 * PITCH - 16) / (NS3 * BPS + S * 4);
             constexpr int U = U_RUN < U_FIT ? U_RUN : U_FIT;              // slices per super-slice
             constexpr int SBS = U * BPS;                                   // backpointer bytes per lane per stage
             constexpr int PPITCH = U * S * 4 + 16;                         // path slot pitch
-            static_assert(U >= 1 && 3 * SBS + PPITCH <= 3 * PITCH, "pass-3 staging exceeds the ring");
+            static_assert(U >= 1 && NS3 * SBS + PPITCH <= 3 * PITCH, "pass-3 staging exceeds the ring");
             constexpr int NCU = SBS / 8;                                   // 8-B chunks per lane per stage
             constexpr int PCU = U * S / 4;                                 // 16-B path chunks per lane
             const int KU = (K + U - 1) / U;
-            uint8_t* bring = ring;                              // [3][NT][SBS]
-            uint8_t* pbuf = ring + (size_t)3 * NT * SBS;        // [NT][PPITCH]
+            uint8_t* bring = ring;                              // [NS3][NT][SBS]
+            uint8_t* pbuf = ring + (size_t)NS3 * NT * SBS;      // [NT][PPITCH]
             const int64_t lane_end_w = T - wbase;               // steps from this warp's lane 0 to the end
             auto bp_load = [&](int u, int sb) {
                 uint8_t* sbase = bring + ((size_t)sb * NT + warp * 32) * SBS;
@@ -1057,13 +1058,15 @@ __global__ void __launch_bounds__(stream_nt(D)) hmm_stream_kernel(const SParams 
                 }
                 cp_async_commit();
             };
-            bp_load(KU - 1, 0);
-            if (KU > 1) bp_load(KU - 2, 1); else cp_async_commit();
+#pragma unroll 1
+            for (int i = 0; i < NS3 - 1; i++) {
+                if (i < KU) bp_load(KU - 1 - i, i); else cp_async_commit();
+            }
             for (int it = 0; it < KU; it++) {
                 const int u = KU - 1 - it;
-                const int sb = it % 3;
-                if (it + 2 < KU) bp_load(u - 2, (it + 2) % 3); else cp_async_commit();
-                cp_async_wait<2>();
+                const int sb = it % NS3;
+                if (it + NS3 - 1 < KU) bp_load(u - (NS3 - 1), (it + NS3 - 1) % NS3); else cp_async_commit();
+                cp_async_wait<NS3 - 1>();
                 __syncwarp();
                 int32_t* ps = reinterpret_cast<int32_t*>(pbuf + (size_t)tid * PPITCH);
                 const uint8_t* bsl = bring + ((size_t)sb * NT + tid) * SBS;
