@@ -293,6 +293,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo only for single-GPU multi-process smoke runs")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="run the split-phase (multi-GPU) path even with one rank (tests the NCCL plumbing)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -307,7 +309,10 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    if world > 1 or args.force_dist:
+        if not dist.is_initialized() and world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1"); os.environ.setdefault("MASTER_PORT", "29511")
+            os.environ.setdefault("RANK", "0"); os.environ.setdefault("WORLD_SIZE", "1")
         run_multi(args, world, rank, local)
         return
     torch.cuda.set_device(local)
