@@ -153,6 +153,17 @@ __device__ __forceinline__ float exp_offset(float m) {
     const float biased = __uint_as_float((__float_as_uint(m) >> 23) | 0x4B000000u);  // 2^23 + E (m >= 0)
     return 8388735.0f - biased;                                                      // (2^23 + 127) - (2^23 + E)
 }
+// Max of N values with 2-input FMNMX (full rate on sm_100; the 3-input FMNMX3 issues at half rate,
+// tools/microbench/pipes.cu) as a balanced tree.
+template <int N>
+__device__ __forceinline__ float vmax2_tree(const float* v) {
+    if constexpr (N == 1) {
+        return v[0];
+    } else {
+        constexpr int H = N / 2;
+        return fmaxf(vmax2_tree<H>(v), vmax2_tree<N - H>(v + H));
+    }
+}
 // Max of N values by a 3-ary tree (depth ~log3 N instead of a serial chain).
 template <int N>
 __device__ __forceinline__ float vmax_tree(const float* v) {

@@ -56,7 +56,7 @@ __device__ __forceinline__ void sp_back_step(const float* row, bool t0, const fl
                                              float& d) {
     float v[D], l[D];
     ld_row<D>(row, v);
-    const float m = fmaxf(vmax<D>(v), -1e30f);  // all -inf (impossible step): l = 0, -m*log2e stays finite
+    const float m = fmaxf(vmax2_tree<D>(v), -1e30f);  // all -inf (impossible step): l = 0, -m*log2e stays finite
     const float c = fmaf(-m, kLog2e, d);
 #pragma unroll
     for (int j = 0; j < D; j++) l[j] = ex2(fmaf(v[j], kLog2e, c));
@@ -91,7 +91,7 @@ __device__ __forceinline__ void sp_back_step(const float* row, bool t0, const fl
     }
 #pragma unroll
     for (int e = 0; e < D * D; e++) P[e] = Pn[e];
-    d = exp_offset(vmax_tree<D * D>(P));
+    d = exp_offset(vmax2_tree<D * D>(P));
 }
 // One slice, right to left (sum-product).  Unlike the max-product fold below, the sum-product step is
 // issue-bound rather than latency-bound at 8 warps/SM (ncu: 66% issue-active, `wait` stalls 0.34 per
