@@ -416,7 +416,41 @@ def main():
             ms_e2e = float(t.item())
         e2e = {"value": T / (ms_e2e * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": int(h_ll.numel() * 4 + h_lp.numel() * 4 + h_la.numel() * 4),
-               "d2h_bytes_per_step": int(h_out.numel() * 8), "ms_per_step": ms_e2e}
+               "d2h_bytes_per_step": int(h_out.numel() * 8), "ms_per_step": ms_e2e,
+               "note": "PCIe-bound: the step's log_lik (16 B/step) crosses the host link every step"}
+        del h_ll, d_ll
+        # the same GE sequence through the symbol-input API: a GE user holds the
+        # channel outputs y (1 B/step) and the emission matrix, not log_lik
+        if args.workload == "ge":
+            import workloads as W
+            wsym = W.ge_symbols(T, seed=5)
+            h_y = torch.from_numpy(wsym.y).pin_memory()
+            h_lb = torch.from_numpy(wsym.log_B).pin_memory()
+            d_y = torch.empty_like(h_y, device=dev); d_lb = torch.empty_like(h_lb, device=dev)
+
+            def e2e_sym_step():
+                d_y.copy_(h_y, non_blocking=True); d_lb.copy_(h_lb, non_blocking=True)
+                d_lp.copy_(h_lp, non_blocking=True); d_la.copy_(h_la, non_blocking=True)
+                f, s, lz, info = H.smooth_symbols(d_lp, d_la, d_lb, d_y)
+                p, lpr, vinfo = H.viterbi_symbols(d_lp, d_la, d_lb, d_y)
+                d_out[0] = lz[0]; d_out[1] = lpr[0]; d_out[2] = info[0]; d_out[3] = vinfo[0]
+                h_out.copy_(d_out, non_blocking=True)
+
+            for _ in range(args.warmup):
+                e2e_sym_step()
+            torch.cuda.synchronize()
+            assert int(h_out[2]) == 0 and int(h_out[3]) == 0
+            e0.record(stream)
+            for _ in range(args.steps):
+                e2e_sym_step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms_sym = e0.elapsed_time(e1) / args.steps
+            e2e["symbols"] = {"value": T / (ms_sym * 1e-3), "unit": UNIT, "ms_per_step": ms_sym,
+                              "h2d_bytes_per_step": int(h_y.numel() + h_lb.numel() * 4 + h_lp.numel() * 4 +
+                                                        h_la.numel() * 4),
+                              "d2h_bytes_per_step": int(h_out.numel() * 8),
+                              "api": "smooth_symbols + viterbi_symbols (y uint8 + log_B)"}
 
     # ---- roofline (dominant kernel) + cpu baseline (rank 0, N=1 only)
     peaks = load_peaks()
