@@ -30,6 +30,13 @@
 #include "hmm_plan.h"
 #include "hmm_small_ops.cuh"
 
+#ifndef HMM_QPAIR
+#define HMM_QPAIR 0
+#endif
+#ifndef HMM_SP_TWO_CHAIN
+#define HMM_SP_TWO_CHAIN 1
+#endif
+
 namespace hmm {
 
 // ---------------------------------------------------------------------------- slice folds
@@ -93,18 +100,126 @@ __device__ __forceinline__ void sp_back_step(const float* row, bool t0, const fl
     for (int e = 0; e < D * D; e++) P[e] = Pn[e];
     d = exp_offset(vmax2_tree<D * D>(P));
 }
+// The same step (t > 0, even D) on packed pairs: P2[k*H + jj] = (P(k,2jj), P(k,2jj+1)), H = D/2, and
+// A2[i*D + k] = (A(i,k), A(i,k)).  psi_t P = A (diag(l_t) P): diag(l) P is D*H FMUL2, the product D*D*H
+// FFMA2/FMUL2 -- the same D^3 + D^2 FP32 multiply-adds as the scalar step (bit-identical roundings
+// per element are not needed: only the operand order differs), in half the issue slots.  The fold is
+// issue-bound, so the freed slots absorb the MUFU/FMNMX/integer work.
+template <int D>
+__device__ __forceinline__ void sp_back_step2(const float* row, const float2* A2, float2* P2, float& d) {
+    constexpr int H = D / 2;
+    float v[D];
+    ld_row<D>(row, v);
+    const float m = fmaxf(vmax2_tree<D>(v), -1e30f);
+    const float c = fmaf(-m, kLog2e, d);
+    float2 R[D * H];
+#pragma unroll
+    for (int k = 0; k < D; k++) {
+        const float lk = ex2(fmaf(v[k], kLog2e, c));
+        const float2 l2 = make_float2(lk, lk);
+#pragma unroll
+        for (int jj = 0; jj < H; jj++) R[k * H + jj] = __fmul2_rn(l2, P2[k * H + jj]);
+    }
+#pragma unroll
+    for (int i = 0; i < D; i++) {
+#pragma unroll
+        for (int jj = 0; jj < H; jj++) {
+            float2 acc = __fmul2_rn(A2[i * D], R[jj]);
+#pragma unroll
+            for (int k = 1; k < D; k++) acc = __ffma2_rn(A2[i * D + k], R[k * H + jj], acc);
+            P2[i * H + jj] = acc;
+        }
+    }
+    float mx[D * H];
+#pragma unroll
+    for (int e = 0; e < D * H; e++) mx[e] = fmaxf(P2[e].x, P2[e].y);
+    d = exp_offset(vmax2_tree<D * H>(mx));
+}
+// Start of a chain: X = psi_t = A diag(l_t) (packed pairs as in sp_back_step2), d = its offset.
+template <int D>
+__device__ __forceinline__ void sp_chain_start2(const float* row, const float2* A2, float2* X2, float& d) {
+    constexpr int H = D / 2;
+    float v[D];
+    ld_row<D>(row, v);
+    const float m = fmaxf(vmax2_tree<D>(v), -1e30f);
+    const float c = -m * kLog2e;
+    float l[D];
+#pragma unroll
+    for (int k = 0; k < D; k++) l[k] = ex2(fmaf(v[k], kLog2e, c));
+#pragma unroll
+    for (int i = 0; i < D; i++)
+#pragma unroll
+        for (int jj = 0; jj < H; jj++) X2[i * H + jj] = __fmul2_rn(make_float2(A2[i * D + 2 * jj].x, A2[i * D + 2 * jj + 1].x),
+                                                    make_float2(l[2 * jj], l[2 * jj + 1]));
+    float mx[D * H];
+#pragma unroll
+    for (int e = 0; e < D * H; e++) mx[e] = fmaxf(X2[e].x, X2[e].y);
+    d = exp_offset(vmax2_tree<D * H>(mx));
+}
 // One slice, right to left (sum-product).  Unlike the max-product fold below, the sum-product step is
 // issue-bound rather than latency-bound at 8 warps/SM (ncu: 66% issue-active, `wait` stalls 0.34 per
 // issue), so the two-chain split would only add its combine/normalise instructions (~7%): one chain.
+// Even D runs the packed-pair step for every step but the sequence's first.
 template <int D, int S, class RS>
 __device__ __forceinline__ void sp_fold_back(const RS rows, int nr, bool t0, const float* A, const float* pi,
                                              float* P, float& d) {
-    if (nr == S) {
+    if constexpr (D % 2 == 0) {
+        constexpr int H = D / 2;
+        float2 A2[D * D], P2[D * H];
+#pragma unroll
+        for (int e = 0; e < D * D; e++) A2[e] = make_float2(A[e], A[e]);
+#if HMM_SP_TWO_CHAIN
+        if (nr == S && !t0) {
+            // two independent chains X = psi_{S/2} .. psi_{S-1}, Y = psi_0 .. psi_{S/2-1} (2x ILP for
+            // the latency-bound step chain), combined as P <- Y (X P); each chain starts from psi itself,
+            // which saves exactly the products the combine costs.  Scales are free (pass 1 keeps only
+            // normalised products).
+            constexpr int HS = S / 2;
+            float2 X2[D * H], Y2[D * H];
+            float dx = 0.0f, dy = 0.0f;
+            sp_chain_start2<D>(rows(S - 1), A2, X2, dx);
+            sp_chain_start2<D>(rows(HS - 1), A2, Y2, dy);
+#pragma unroll 2
+            for (int q = 1; q < HS; q++) {
+                sp_back_step2<D>(rows(S - 1 - q), A2, X2, dx);
+                sp_back_step2<D>(rows(HS - 1 - q), A2, Y2, dy);
+            }
+            float X[D * D], Y[D * D], XP[D * D];
+#pragma unroll
+            for (int e = 0; e < D * H; e++) {
+                X[2 * e] = X2[e].x;
+                X[2 * e + 1] = X2[e].y;
+                Y[2 * e] = Y2[e].x;
+                Y[2 * e + 1] = Y2[e].y;
+            }
+            mat_op<D, false>(X, P, XP);
+            mat_op<D, false>(Y, XP, P);
+            d = 0.0f;
+            return;
+        }
+#endif
+#pragma unroll
+        for (int e = 0; e < D * H; e++) P2[e] = make_float2(P[2 * e], P[2 * e + 1]);
+        if (nr == S) {
 #pragma unroll 4
-        for (int ii = S - 1; ii >= 1; ii--) sp_back_step<D>(rows(ii), false, A, pi, P, d);
-    } else {
+            for (int ii = S - 1; ii >= 1; ii--) sp_back_step2<D>(rows(ii), A2, P2, d);
+        } else {
 #pragma unroll 1
-        for (int ii = nr - 1; ii >= 1; ii--) sp_back_step<D>(rows(ii), false, A, pi, P, d);
+            for (int ii = nr - 1; ii >= 1; ii--) sp_back_step2<D>(rows(ii), A2, P2, d);
+        }
+#pragma unroll
+        for (int e = 0; e < D * H; e++) {
+            P[2 * e] = P2[e].x;
+            P[2 * e + 1] = P2[e].y;
+        }
+    } else {
+        if (nr == S) {
+#pragma unroll 4
+            for (int ii = S - 1; ii >= 1; ii--) sp_back_step<D>(rows(ii), false, A, pi, P, d);
+        } else {
+#pragma unroll 1
+            for (int ii = nr - 1; ii >= 1; ii--) sp_back_step<D>(rows(ii), false, A, pi, P, d);
+        }
     }
     sp_back_step<D>(rows(0), t0, A, pi, P, d);
 }
@@ -156,10 +271,81 @@ __device__ __forceinline__ void mp_chain_start(const float* row, const float* LA
 #pragma unroll
         for (int k = 0; k < D; k++) X[i * D + k] = LA[i * D + k] + w[k];
 }
+// mp_back_step (t > 0, even D) on packed pairs along j: P2[k*H + jj] = (P(k,2jj), P(k,2jj+1)),
+// LA2[i*D + k] = (LA(i,k), LA(i,k)).  The D^2 + D^3 adds run as FADD2 with the same operands and order
+// as the scalar step (LA + (w + P)), so the results are bit-identical; the maxima stay scalar.
+template <int D>
+__device__ __forceinline__ void mp_back_step2(const float* row, const float2* LA2, float2* P2, float& chk) {
+    constexpr int H = D / 2;
+    float v[D];
+    ld_row<D>(row, v);
+    float m = vmax<D>(v);
+    if (!(m > neg_inf())) m = 0.0f;
+    float w[D];
+#pragma unroll
+    for (int k = 0; k < D; k++) w[k] = v[k] - m;
+    chk += vsum<D>(w);
+    float2 W2[D * H];
+#pragma unroll
+    for (int k = 0; k < D; k++) {
+        const float2 wk = make_float2(w[k], w[k]);
+#pragma unroll
+        for (int jj = 0; jj < H; jj++) W2[k * H + jj] = __fadd2_rn(wk, P2[k * H + jj]);
+    }
+#pragma unroll
+    for (int i = 0; i < D; i++) {
+#pragma unroll
+        for (int jj = 0; jj < H; jj++) {
+            float sx[D], sy[D];
+#pragma unroll
+            for (int k = 0; k < D; k++) {
+                const float2 s = __fadd2_rn(LA2[i * D + k], W2[k * H + jj]);
+                sx[k] = s.x;
+                sy[k] = s.y;
+            }
+            P2[i * H + jj] = make_float2(vmax<D>(sx), vmax<D>(sy));
+        }
+    }
+}
 // Max-product slice fold, two interleaved chains for full slices (as sp_fold_back, Def. 5).
 template <int D, int S, class RS>
 __device__ __forceinline__ void mp_fold_back(const RS rows, int nr, bool t0, const float* LA, const float* LP,
                                              float* P, float& chk) {
+    if constexpr (D % 2 == 0) {
+        if (nr == S) {
+            constexpr int H = D / 2, HS = S / 2;
+            float2 LA2[D * D];
+#pragma unroll
+            for (int e = 0; e < D * D; e++) LA2[e] = make_float2(LA[e], LA[e]);
+            float X[D * D], Y[D * D];
+            mp_chain_start<D>(rows(S - 1), LA, X, chk);
+            mp_chain_start<D>(rows(HS - 1), LA, Y, chk);
+            float2 X2[D * H], Y2[D * H];
+#pragma unroll
+            for (int e = 0; e < D * H; e++) {
+                X2[e] = make_float2(X[2 * e], X[2 * e + 1]);
+                Y2[e] = make_float2(Y[2 * e], Y[2 * e + 1]);
+            }
+#pragma unroll 2
+            for (int q = 1; q < HS - 1; q++) {
+                mp_back_step2<D>(rows(S - 1 - q), LA2, X2, chk);
+                mp_back_step2<D>(rows(HS - 1 - q), LA2, Y2, chk);
+            }
+            mp_back_step2<D>(rows(HS), LA2, X2, chk);
+#pragma unroll
+            for (int e = 0; e < D * H; e++) {
+                X[2 * e] = X2[e].x;
+                X[2 * e + 1] = X2[e].y;
+                Y[2 * e] = Y2[e].x;
+                Y[2 * e + 1] = Y2[e].y;
+            }
+            mp_back_step<D>(rows(0), t0, LA, LP, Y, chk);
+            float XP[D * D];
+            mat_op<D, true>(X, P, XP);
+            mat_op<D, true>(Y, XP, P);
+            return;
+        }
+    }
     if (nr == S) {
         constexpr int H = S / 2;
         float X[D * D], Y[D * D];
@@ -246,6 +432,33 @@ __device__ __forceinline__ int sp_alpha_slice(const RS src, float* rows, float* 
     return zero_i;
 }
 
+// Backward potential at the end of the slice BEFORE a slice, from the one at this slice's end: the
+// backward recursion b <- A (l_t o b) (Thm. 2 / Alg. 1 backward) over this slice's raw rows, right to
+// left, renormalised by powers of two like sp_beta_step.  l_t = exp(ll_t - m_t): any per-step scale is
+// free (b is only ever used normalised).
+template <int D, class RS>
+__device__ __forceinline__ void sp_beta_presweep(const RS src, int nr, const float* A, float* b) {
+#pragma unroll 4
+    for (int i = nr - 1; i >= 0; i--) {
+        float v[D];
+        ld_row<D>(src(i), v);
+        const float m = vmax<D>(v);
+        const float c0 = (m > -FLT_MAX) ? -m * kLog2e : 0.0f;
+        float w[D], bn[D];
+#pragma unroll
+        for (int j = 0; j < D; j++) w[j] = ex2(fmaf(v[j], kLog2e, c0)) * b[j];
+#pragma unroll
+        for (int r = 0; r < D; r++) {
+            float acc = A[r * D] * w[0];
+#pragma unroll
+            for (int j = 1; j < D; j++) acc = fmaf(A[r * D + j], w[j], acc);
+            bn[r] = acc;
+        }
+        const float sc = pow2_inv(vmax<D>(bn));
+#pragma unroll
+        for (int r = 0; r < D; r++) b[r] = bn[r] * sc;
+    }
+}
 // Backward pass over one slice from the backward potential at its last step, combined with Eq. 14
 // (smoothed_t = alpha_t beta_t / Z_t, written over the l rows).
 template <int D>
@@ -373,12 +586,31 @@ __device__ __forceinline__ uint64_t vit_fwd_slice(const RS rows, int nr, bool t0
             if (!(m > neg_inf())) m = 0.0f;
             float Vh[D];
             uint32_t sel = 0;
+            const bool first = t0 && i == 0;
+            // scores V(k) + LA(k, j): FADD2 over column pairs (even D; same operands, bit-identical)
+            float scs[D][D];  // [j][k]
+            if (D % 2 == 0 && !first) {
+#pragma unroll
+                for (int k = 0; k < D; k++) {
+                    const float2 vk = make_float2(V[k], V[k]);
+#pragma unroll
+                    for (int jj = 0; jj < D / 2; jj++) {
+                        const float2 s2 = __fadd2_rn(vk, make_float2(LA[k * D + 2 * jj], LA[k * D + 2 * jj + 1]));
+                        scs[2 * jj][k] = s2.x;
+                        scs[2 * jj + 1][k] = s2.y;
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < D; j++)
+#pragma unroll
+                    for (int k = 0; k < D; k++) scs[j][k] = V[k] + (first ? LP[j] : LA[k * D + j]);
+            }
 #pragma unroll
             for (int j = 0; j < D; j++) {
-                const bool first = t0 && i == 0;
                 float sc[D];
 #pragma unroll
-                for (int k = 0; k < D; k++) sc[k] = V[k] + (first ? LP[j] : LA[k * D + j]);
+                for (int k = 0; k < D; k++) sc[k] = scs[j][k];
                 // the max by a 2-input tree keeps the V recursion's critical path short; the argmax
                 // (smallest index attaining it: DESIGN.md reading 5) hangs off it
                 float best;
@@ -539,6 +771,11 @@ __global__ void __launch_bounds__(stream_nt(D)) hmm_stream_kernel(const SParams 
         return rem <= 0 ? 0 : (rem < S ? (int)rem : S);
     };
     auto warp_full = [&](int k) -> bool { return wbase + 31 * n + (int64_t)k * S + S <= T; };
+    // The warp holding the end of the sequence: bit j of `fullmask(k)` = lane j's slice k is full (one
+    // ballot per slice).  Its full slices take the same 16-B copies as a full warp; only the one
+    // partial lane slice of the sequence takes the element-wise path.
+    const int my_nfull = (int)((a1 > a0 ? a1 - a0 : 0) / S);
+    auto fullmask = [&](int k) -> uint32_t { return __ballot_sync(0xffffffffu, my_nfull > k); };
     // async load of slice k of the warp's lanes into ring stage st (one cp.async group per call)
     auto coop_load = [&](int k, int st) {
         uint8_t* sbase = ring + (size_t)st * NT * PITCH + (size_t)warp * 32 * PITCH;
@@ -569,17 +806,22 @@ __global__ void __launch_bounds__(stream_nt(D)) hmm_stream_kernel(const SParams 
                     src += (int64_t)LPI * n * D;
                     dst += LPI * PITCH;
                 }
-            } else {  // the warp holding the end of the sequence: zero-filling copies, no branches
-                int64_t rem64 = (T - (wbase + (int64_t)j0 * n + (int64_t)k * S)) * D - ch * 4;  // floats left
-                int rem = (int)(rem64 < -(1 << 30) ? -(1 << 30) : (rem64 > (1 << 30) ? (1 << 30) : rem64));
-                const int step = LPI * (int)n * D;
+            } else {  // the warp holding the end of the sequence (lanes past the end load nothing)
+                const int jp = __popc(fullmask(k));  // lanes [0, jp) full; lane jp's slice may be partial
+                const int nv = (jp - j0 + LPI - 1) / LPI;  // this thread's chunks in full lane slices
 #pragma unroll
                 for (int it = 0; it < CPL; it++) {
-                    const int f = rem < 0 ? 0 : (rem > 4 ? 4 : rem);
-                    cp_async16_zfill(dst, f > 0 ? src : ll, 4u * f);
-                    src += (int64_t)step;
+                    if (it < nv) cp_async16(dst, src);
+                    src += (int64_t)LPI * n * D;
                     dst += LPI * PITCH;
-                    rem -= step;
+                }
+                if (jp < 32 && ((jp - j0) % LPI) == 0 && jp >= j0) {
+                    const int64_t rem64 = (T - (wbase + (int64_t)jp * n + (int64_t)k * S)) * D - ch * 4;
+                    if (rem64 > 0) {
+                        const int f = rem64 > 4 ? 4 : (int)rem64;
+                        cp_async16_zfill(sbase + (size_t)jp * PITCH + ch * 16,
+                                         ll + (wbase + (int64_t)jp * n + (int64_t)k * S) * D + ch * 4, 4u * f);
+                    }
                 }
             }
             done = true;
@@ -616,25 +858,22 @@ __global__ void __launch_bounds__(stream_nt(D)) hmm_stream_kernel(const SParams 
                     dst += (int64_t)LPI * n * D;
                     src += LPI * PITCH;
                 }
-            } else {
-                int64_t rem64 = (T - (wbase + (int64_t)j0 * n + (int64_t)k * S)) * D - ch * 4;
-                int rem = (int)(rem64 < -(1 << 30) ? -(1 << 30) : (rem64 > (1 << 30) ? (1 << 30) : rem64));
-                const int step = LPI * (int)n * D;
-                const int rem0 = rem;
+            } else {  // the warp holding the end of the sequence: full lane slices as above
+                const int jp = __popc(fullmask(k));  // lanes [0, jp) full; lane jp's slice may be partial
+                const int nv = (jp - j0 + LPI - 1) / LPI;
 #pragma unroll
-                for (int it = 0; it < CPL; it++) {  // whole 16-B chunks: predicated stores only
-                    if (rem >= 4) __stcs(reinterpret_cast<float4*>(dst), *reinterpret_cast<const float4*>(src));
-                    dst += (int64_t)step;
+                for (int it = 0; it < CPL; it++) {
+                    if (it < nv) __stcs(reinterpret_cast<float4*>(dst), *reinterpret_cast<const float4*>(src));
+                    dst += (int64_t)LPI * n * D;
                     src += LPI * PITCH;
-                    rem -= step;
                 }
-                // the one chunk of the sequence that ends inside 16 B (T*D not a multiple of 4)
-                if (rem0 > 0) {
-                    const int it = rem0 / step, r = rem0 - it * step;
-                    if (it < CPL && r > 0 && r < 4) {
-                        float* d2 = g + (wbase + (int64_t)(j0 + it * LPI) * n + (int64_t)k * S) * D + ch * 4;
-                        const float* s2 = reinterpret_cast<const float*>(sbase + (size_t)(j0 + it * LPI) * PITCH + ch * 16);
-                        for (int f = 0; f < r; f++) d2[f] = s2[f];
+                if (jp < 32 && ((jp - j0) % LPI) == 0 && jp >= j0) {
+                    const int64_t rem64 = (T - (wbase + (int64_t)jp * n + (int64_t)k * S)) * D - ch * 4;
+                    if (rem64 > 0) {
+                        float* d2 = g + (wbase + (int64_t)jp * n + (int64_t)k * S) * D + ch * 4;
+                        const float* s2 = reinterpret_cast<const float*>(sbase + (size_t)jp * PITCH + ch * 16);
+                        if (rem64 >= 4) __stcs(reinterpret_cast<float4*>(d2), *reinterpret_cast<const float4*>(s2));
+                        else for (int f = 0; f < (int)rem64; f++) d2[f] = s2[f];
                     }
                 }
             }
@@ -689,12 +928,20 @@ __global__ void __launch_bounds__(stream_nt(D)) hmm_stream_kernel(const SParams 
             if (it + 2 < K) coop_load(k - 2, (it + 2) % 3); else cp_async_commit();
             const int nr = slice_rows(k);
             if constexpr (!MP) {
+#if HMM_QPAIR
+                // Q_k for odd k < K-1 only (pass 2 derives the even slices' backward potential from the
+                // next slice's rows): 2 B/step of Q written here and read back in pass 2 instead of 4
+                if ((k & 1) && k < K - 1) {
+                    const int qi = k >> 1;
+#else
                 if (nr > 0) {  // Q_k = product of the slices right of k (normalised), warp-contiguous
+                    const int qi = k;
+#endif
                     const float s = pow2_inv(vmax_tree<D * D>(P));
 #pragma unroll
                     for (int e = 0; e < D * D; e++) P[e] *= s;
                     dexp = 0.0f;
-                    float* q = qdst + (((size_t)c * K + k) * NT + tid) * (QB / 4);
+                    float* q = qdst + (((size_t)c * K + qi) * NT + tid) * (QB / 4);
                     if constexpr ((D * D) % 4 == 0) {
 #pragma unroll
                         for (int e = 0; e < D * D; e += 4)
@@ -858,6 +1105,69 @@ __global__ void __launch_bounds__(stream_nt(D)) hmm_stream_kernel(const SParams 
             for (int e = 0; e < (STATS ? D * D : 1); e++) xi_l[e] = 0.0;
 #pragma unroll
             for (int e = 0; e < (STATS ? D : 1); e++) g_l[e] = 0.0;
+#if HMM_QPAIR
+            // Even slices (except the lane's last) have no stored Q: their backward potential comes
+            // from a backward pre-sweep over the next slice's rows, which are resident (stage 1)
+            // together with the slice (stage 0); odd slices reuse the potential computed for that
+            // pre-sweep.  Q_{2i+1} lives in slot i.
+            const int KQ = (K - 1) / 2;
+            coop_load(0, 0);
+            if (K > 1) coop_load(1, 1); else cp_async_commit();
+            if (KQ > 0) issue_q(0);
+            float bnext[D];
+#pragma unroll
+            for (int d = 0; d < D; d++) bnext[d] = cout_[d];
+            for (int k = 0; k < K; k++) {
+                const int st = k & 1;
+                const int nr = slice_rows(k);
+                float beta[D];
+                if (st == 0) {
+                    cp_async_wait<0>();  // slices k and k+1 resident
+                    __syncwarp();
+                    const int nr1 = (k + 1 < K) ? slice_rows(k + 1) : 0;
+#pragma unroll
+                    for (int d = 0; d < D; d++) bnext[d] = cout_[d];
+                    if (k + 1 < K - 1) {  // Q_{k+1} (the product of the slices right of k+1)
+                        mbar_wait(&qbar[warp], qphase);
+                        qphase ^= 1u;
+                        if (k + 2 < K && slice_rows(k + 2) > 0) {
+                            float Q[D * D];
+                            const float* qs = reinterpret_cast<const float*>(qbuf + ((size_t)warp * 32 + lane) * QB);
+#pragma unroll
+                            for (int e = 0; e < D * D; e++) Q[e] = qs[e];
+                            mat_vec<D>(Q, cout_, bnext);
+                        }
+                        __syncwarp();  // every lane has read its Q
+                        if ((k >> 1) + 1 < KQ) issue_q((k >> 1) + 1);
+                    }
+#pragma unroll
+                    for (int d = 0; d < D; d++) beta[d] = bnext[d];
+                    if (nr1 > 0) sp_beta_presweep<D>(rsrc(1, nr1), nr1, A, beta);
+                } else {
+#pragma unroll
+                    for (int d = 0; d < D; d++) beta[d] = bnext[d];
+                }
+                if (nr > 0) {
+                    float* rows = slot(st);
+                    float aprev[D];
+#pragma unroll
+                    for (int d = 0; d < D; d++) aprev[d] = alpha[d];
+                    const int zi = sp_alpha_slice<D, S>(rsrc(st, nr), rows, frows, nr, lane_t0 && k == 0, A, pv, alpha,
+                                                        rprod, rexp, msum);
+                    const int64_t r0 = a0 + (int64_t)k * S;
+                    if (zi >= 0 && tb + r0 + zi < zero_t) zero_t = tb + r0 + zi;
+                    if constexpr (STATS)
+                        sp_beta_slice_stats<D, S>(rows, frows, nr, A, beta, aprev, lane_t0 && k == 0, xi_l, g_l);
+                    else
+                        sp_beta_slice<D, S>(rows, frows, nr, A, beta);
+                }
+                __syncwarp();
+                if (p.smoothed) coop_store(k, stage_base(st), p.smoothed);
+                if (p.filtered) coop_store(k, stage_base(2), p.filtered);
+                __syncwarp();
+                if (k + 2 < K) coop_load(k + 2, st); else cp_async_commit();
+            }
+#else
             coop_load(0, 0);
             issue_q(0);
             for (int k = 0; k < K; k++) {
@@ -897,6 +1207,7 @@ __global__ void __launch_bounds__(stream_nt(D)) hmm_stream_kernel(const SParams 
                 if (p.filtered) coop_store(k, stage_base(2), p.filtered);
                 __syncwarp();
             }
+#endif
             if (nsl > 0) acc += log((double)vsum<D>(alpha)) - log((double)rprod) - (double)rexp * (double)kLn2 + msum;
             if constexpr (STATS) {  // fixed-order CTA sums of the lanes' fp64 partials -> workspace
                 double* cst = reinterpret_cast<double*>(p.ws + p.ws_stats) + (size_t)c * (D * D + D);

@@ -8,7 +8,11 @@
 #include "../../paper_2102_05743_b200/csrc/hmm_device.cuh"
 using namespace hmm;
 
-constexpr int NT = 256, S = 16, SB = S * 16, PITCH = SB + 16;
+#ifndef NT_
+#define NT_ 256
+#define S_ 16
+#endif
+constexpr int NT = NT_, S = S_, SB = S * 16, PITCH = SB + 16;
 
 __global__ void __launch_bounds__(NT) passA(const float4* ll, int64_t T, int64_t n, float* sink, int NS) {
     extern __shared__ __align__(128) uint8_t sm[];
