@@ -30,9 +30,6 @@
 #include "hmm_plan.h"
 #include "hmm_small_ops.cuh"
 
-#ifndef HMM_QPAIR
-#define HMM_QPAIR 0
-#endif
 #ifndef HMM_SP_TWO_CHAIN
 #define HMM_SP_TWO_CHAIN 1
 #endif
@@ -163,7 +160,7 @@ __device__ __forceinline__ void sp_chain_start2(const float* row, const float2* 
 template <int D, int S, class RS>
 __device__ __forceinline__ void sp_fold_back(const RS rows, int nr, bool t0, const float* A, const float* pi,
                                              float* P, float& d) {
-    if constexpr (D % 2 == 0) {
+    if constexpr (D % 2 == 0 && D <= 4) {  // (D = 6, 8: the packed operands would spill)
         constexpr int H = D / 2;
         float2 A2[D * D], P2[D * H];
 #pragma unroll
@@ -311,7 +308,7 @@ __device__ __forceinline__ void mp_back_step2(const float* row, const float2* LA
 template <int D, int S, class RS>
 __device__ __forceinline__ void mp_fold_back(const RS rows, int nr, bool t0, const float* LA, const float* LP,
                                              float* P, float& chk) {
-    if constexpr (D % 2 == 0) {
+    if constexpr (D % 2 == 0 && D <= 4) {  // (D = 6, 8: the packed operands would spill)
         if (nr == S) {
             constexpr int H = D / 2, HS = S / 2;
             float2 LA2[D * D];
@@ -432,33 +429,6 @@ __device__ __forceinline__ int sp_alpha_slice(const RS src, float* rows, float* 
     return zero_i;
 }
 
-// Backward potential at the end of the slice BEFORE a slice, from the one at this slice's end: the
-// backward recursion b <- A (l_t o b) (Thm. 2 / Alg. 1 backward) over this slice's raw rows, right to
-// left, renormalised by powers of two like sp_beta_step.  l_t = exp(ll_t - m_t): any per-step scale is
-// free (b is only ever used normalised).
-template <int D, class RS>
-__device__ __forceinline__ void sp_beta_presweep(const RS src, int nr, const float* A, float* b) {
-#pragma unroll 4
-    for (int i = nr - 1; i >= 0; i--) {
-        float v[D];
-        ld_row<D>(src(i), v);
-        const float m = vmax<D>(v);
-        const float c0 = (m > -FLT_MAX) ? -m * kLog2e : 0.0f;
-        float w[D], bn[D];
-#pragma unroll
-        for (int j = 0; j < D; j++) w[j] = ex2(fmaf(v[j], kLog2e, c0)) * b[j];
-#pragma unroll
-        for (int r = 0; r < D; r++) {
-            float acc = A[r * D] * w[0];
-#pragma unroll
-            for (int j = 1; j < D; j++) acc = fmaf(A[r * D + j], w[j], acc);
-            bn[r] = acc;
-        }
-        const float sc = pow2_inv(vmax<D>(bn));
-#pragma unroll
-        for (int r = 0; r < D; r++) b[r] = bn[r] * sc;
-    }
-}
 // Backward pass over one slice from the backward potential at its last step, combined with Eq. 14
 // (smoothed_t = alpha_t beta_t / Z_t, written over the l rows).
 template <int D>
@@ -589,7 +559,7 @@ __device__ __forceinline__ uint64_t vit_fwd_slice(const RS rows, int nr, bool t0
             const bool first = t0 && i == 0;
             // scores V(k) + LA(k, j): FADD2 over column pairs (even D; same operands, bit-identical)
             float scs[D][D];  // [j][k]
-            if (D % 2 == 0 && !first) {
+            if (D % 2 == 0 && D <= 4 && !first) {
 #pragma unroll
                 for (int k = 0; k < D; k++) {
                     const float2 vk = make_float2(V[k], V[k]);
@@ -928,15 +898,8 @@ __global__ void __launch_bounds__(stream_nt(D)) hmm_stream_kernel(const SParams 
             if (it + 2 < K) coop_load(k - 2, (it + 2) % 3); else cp_async_commit();
             const int nr = slice_rows(k);
             if constexpr (!MP) {
-#if HMM_QPAIR
-                // Q_k for odd k < K-1 only (pass 2 derives the even slices' backward potential from the
-                // next slice's rows): 2 B/step of Q written here and read back in pass 2 instead of 4
-                if ((k & 1) && k < K - 1) {
-                    const int qi = k >> 1;
-#else
                 if (nr > 0) {  // Q_k = product of the slices right of k (normalised), warp-contiguous
                     const int qi = k;
-#endif
                     const float s = pow2_inv(vmax_tree<D * D>(P));
 #pragma unroll
                     for (int e = 0; e < D * D; e++) P[e] *= s;
@@ -1105,69 +1068,6 @@ __global__ void __launch_bounds__(stream_nt(D)) hmm_stream_kernel(const SParams 
             for (int e = 0; e < (STATS ? D * D : 1); e++) xi_l[e] = 0.0;
 #pragma unroll
             for (int e = 0; e < (STATS ? D : 1); e++) g_l[e] = 0.0;
-#if HMM_QPAIR
-            // Even slices (except the lane's last) have no stored Q: their backward potential comes
-            // from a backward pre-sweep over the next slice's rows, which are resident (stage 1)
-            // together with the slice (stage 0); odd slices reuse the potential computed for that
-            // pre-sweep.  Q_{2i+1} lives in slot i.
-            const int KQ = (K - 1) / 2;
-            coop_load(0, 0);
-            if (K > 1) coop_load(1, 1); else cp_async_commit();
-            if (KQ > 0) issue_q(0);
-            float bnext[D];
-#pragma unroll
-            for (int d = 0; d < D; d++) bnext[d] = cout_[d];
-            for (int k = 0; k < K; k++) {
-                const int st = k & 1;
-                const int nr = slice_rows(k);
-                float beta[D];
-                if (st == 0) {
-                    cp_async_wait<0>();  // slices k and k+1 resident
-                    __syncwarp();
-                    const int nr1 = (k + 1 < K) ? slice_rows(k + 1) : 0;
-#pragma unroll
-                    for (int d = 0; d < D; d++) bnext[d] = cout_[d];
-                    if (k + 1 < K - 1) {  // Q_{k+1} (the product of the slices right of k+1)
-                        mbar_wait(&qbar[warp], qphase);
-                        qphase ^= 1u;
-                        if (k + 2 < K && slice_rows(k + 2) > 0) {
-                            float Q[D * D];
-                            const float* qs = reinterpret_cast<const float*>(qbuf + ((size_t)warp * 32 + lane) * QB);
-#pragma unroll
-                            for (int e = 0; e < D * D; e++) Q[e] = qs[e];
-                            mat_vec<D>(Q, cout_, bnext);
-                        }
-                        __syncwarp();  // every lane has read its Q
-                        if ((k >> 1) + 1 < KQ) issue_q((k >> 1) + 1);
-                    }
-#pragma unroll
-                    for (int d = 0; d < D; d++) beta[d] = bnext[d];
-                    if (nr1 > 0) sp_beta_presweep<D>(rsrc(1, nr1), nr1, A, beta);
-                } else {
-#pragma unroll
-                    for (int d = 0; d < D; d++) beta[d] = bnext[d];
-                }
-                if (nr > 0) {
-                    float* rows = slot(st);
-                    float aprev[D];
-#pragma unroll
-                    for (int d = 0; d < D; d++) aprev[d] = alpha[d];
-                    const int zi = sp_alpha_slice<D, S>(rsrc(st, nr), rows, frows, nr, lane_t0 && k == 0, A, pv, alpha,
-                                                        rprod, rexp, msum);
-                    const int64_t r0 = a0 + (int64_t)k * S;
-                    if (zi >= 0 && tb + r0 + zi < zero_t) zero_t = tb + r0 + zi;
-                    if constexpr (STATS)
-                        sp_beta_slice_stats<D, S>(rows, frows, nr, A, beta, aprev, lane_t0 && k == 0, xi_l, g_l);
-                    else
-                        sp_beta_slice<D, S>(rows, frows, nr, A, beta);
-                }
-                __syncwarp();
-                if (p.smoothed) coop_store(k, stage_base(st), p.smoothed);
-                if (p.filtered) coop_store(k, stage_base(2), p.filtered);
-                __syncwarp();
-                if (k + 2 < K) coop_load(k + 2, st); else cp_async_commit();
-            }
-#else
             coop_load(0, 0);
             issue_q(0);
             for (int k = 0; k < K; k++) {
@@ -1207,7 +1107,6 @@ __global__ void __launch_bounds__(stream_nt(D)) hmm_stream_kernel(const SParams 
                 if (p.filtered) coop_store(k, stage_base(2), p.filtered);
                 __syncwarp();
             }
-#endif
             if (nsl > 0) acc += log((double)vsum<D>(alpha)) - log((double)rprod) - (double)rexp * (double)kLn2 + msum;
             if constexpr (STATS) {  // fixed-order CTA sums of the lanes' fp64 partials -> workspace
                 double* cst = reinterpret_cast<double*>(p.ws + p.ws_stats) + (size_t)c * (D * D + D);
@@ -1351,7 +1250,8 @@ __global__ void __launch_bounds__(stream_nt(D)) hmm_stream_kernel(const SParams 
             constexpr int SBS = U * BPS;                                   // backpointer bytes per lane per stage
             constexpr int PPITCH = U * S * 4 + 16;                         // path slot pitch
             static_assert(U >= 1 && NS3 * SBS + PPITCH <= 3 * PITCH, "pass-3 staging exceeds the ring");
-            constexpr int NCU = SBS / 8;                                   // 8-B chunks per lane per stage
+            constexpr int CB = (BPS % 16 == 0) ? 16 : 8;                   // copy chunk (never straddles a slice)
+            constexpr int NCU = SBS / CB;                                  // chunks per lane per stage
             constexpr int PCU = U * S / 4;                                 // 16-B path chunks per lane
             const int KU = (K + U - 1) / U;
             uint8_t* bring = ring;                              // [NS3][NT][SBS]
@@ -1361,11 +1261,14 @@ __global__ void __launch_bounds__(stream_nt(D)) hmm_stream_kernel(const SParams 
                 uint8_t* sbase = bring + ((size_t)sb * NT + warp * 32) * SBS;
 #pragma unroll
                 for (int it = 0; it < NCU; it++) {
+                    // whole chunks: the backpointer buffer holds T + S steps, so a chunk that starts before
+                    // the sequence end may read past it (those steps are never used)
                     const int q = lane + 32 * it, j = q / NCU, rem = q - j * NCU;
-                    const int64_t so = (int64_t)u * U * S + (8 * rem) / BPB;   // step offset inside the lane
+                    const int64_t so = (int64_t)u * U * S + (CB * rem) / BPB;  // step offset inside the lane
                     const bool ok = u >= 0 && so < n && (int64_t)j * n + so < lane_end_w;
-                    const uint8_t* src = ok ? bpg + (size_t)(wbase + (int64_t)j * n + (int64_t)u * U * S) * BPB + 8 * rem : bpg;
-                    cp_async8_zfill(sbase + (size_t)j * SBS + 8 * rem, src, ok ? 8u : 0u);
+                    const uint8_t* src = ok ? bpg + (size_t)(wbase + (int64_t)j * n + (int64_t)u * U * S) * BPB + CB * rem : bpg;
+                    if constexpr (CB == 16) cp_async16_zfill(sbase + (size_t)j * SBS + 16 * rem, src, ok ? 16u : 0u);
+                    else cp_async8_zfill(sbase + (size_t)j * SBS + 8 * rem, src, ok ? 8u : 0u);
                 }
                 cp_async_commit();
             };
@@ -1381,6 +1284,32 @@ __global__ void __launch_bounds__(stream_nt(D)) hmm_stream_kernel(const SParams 
                 __syncwarp();
                 int32_t* ps = reinterpret_cast<int32_t*>(pbuf + (size_t)tid * PPITCH);
                 const uint8_t* bsl = bring + ((size_t)sb * NT + tid) * SBS;
+                if constexpr (U * BPW <= 32 && BPW % 4 == 0 && BPS % 16 == 0) {
+                    // all U slices' words up front (16-B LDS): the backtrack chain never waits on SMEM
+                    uint32_t cw[U][BPW];
+#pragma unroll
+                    for (int kk = 0; kk < U; kk++)
+#pragma unroll
+                        for (int i = 0; i < BPW; i += 4) {
+                            const uint4 v = *reinterpret_cast<const uint4*>(bsl + kk * BPS + 4 * i);
+                            cw[kk][i] = v.x;
+                            cw[kk][i + 1] = v.y;
+                            cw[kk][i + 2] = v.z;
+                            cw[kk][i + 3] = v.w;
+                        }
+#pragma unroll
+                    for (int kk = U - 1; kk >= 0; kk--) {
+                        const int k = u * U + kk;
+                        const int nr = (k < K) ? slice_rows(k) : 0;
+                        if (nr > 0) {
+                            int32_t out[S];
+                            x = vit_back_slice<D, S>(cw[kk], nr, x, out);
+#pragma unroll
+                            for (int i = 0; i < S; i += 4)
+                                *reinterpret_cast<int4*>(ps + kk * S + i) = make_int4(out[i], out[i + 1], out[i + 2], out[i + 3]);
+                        }
+                    }
+                } else {
 #pragma unroll 1
                 for (int kk = U - 1; kk >= 0; kk--) {
                     const int k = u * U + kk;
@@ -1400,6 +1329,7 @@ __global__ void __launch_bounds__(stream_nt(D)) hmm_stream_kernel(const SParams 
                         for (int i = 0; i < S; i += 4)
                             *reinterpret_cast<int4*>(ps + kk * S + i) = make_int4(out[i], out[i + 1], out[i + 2], out[i + 3]);
                     }
+                }
                 }
                 __syncwarp();
                 // coalesced path stores of the super-slice: 16-B chunks, the sequence's last chunk by words
