@@ -19,6 +19,8 @@ template<int OP> __global__ void kern(float* out, float a, float b) {
       if (OP == 6) x[i] = x[i] * a + b;                         // FFMA imm-ish (const operands)
       if (OP == 7) x[i] = fmaxf(x[i], x[(i+1)&7]) - a;          // FMNMX + FADD
       if (OP == 8) x[i] = x[i] + x[(i+1)&7];                    // FADD
+      if (OP == 10) { y[i] = __fadd2_rn(y[i], y[(i+1)&7]); x[i] = fmaxf(x[i], x[(i+1)&7]); } // FADD2 || FMNMX
+      if (OP == 11) x[i] = fmaxf(x[i], x[(i+1)&7]);             // FMNMX only
       if (OP == 9) { float r; asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(x[i]), "f"(x[(i+1)&7]), "f"(x[(i+3)&7])); x[i] = r; } // FMNMX3 only
     }
   }
@@ -47,6 +49,7 @@ int main() {
   run<0>("FFMA", 1); run<1>("FFMA2", 2); run<2>("FMNMX3+FADD", 2); run<3>("DFMA", 1);
   run<4>("EX2+FMUL", 2); run<5>("FADD2", 2); run<6>("FFMA-c", 1);
   run<7>("FMNMX+FADD", 2); run<8>("FADD", 1); run<9>("FMNMX3", 1);
+  run<10>("FADD2||FMNMX", 3); run<11>("FMNMX", 1);
   cudaDeviceProp p; cudaGetDeviceProperties(&p, 0);
   printf("SMs %d smemPerBlockOptin %zu smemPerSM %zu L2 %d regsPerSM %d clock %d kHz memclk %d kHz busw %d\n",
          p.multiProcessorCount, p.sharedMemPerBlockOptin, p.sharedMemPerMultiprocessor, p.l2CacheSize,
