@@ -18,4 +18,4 @@ ws = W.ge_symbols(T, 5)
 lp, la, lb, y = (torch.from_numpy(np.ascontiguousarray(x)).to(dev) for x in (ws.log_pi, ws.log_A, ws.log_B, ws.y))
 ts = timeit(lambda: H.smooth_symbols(lp, la, lb, y))
 tv = timeit(lambda: H.viterbi_symbols(lp, la, lb, y))
-print(f"GE symbols T=1e8: smoother {ts:.3f} ms ({T/ts/1e9*1e3:.3e} steps/s), viterbi {tv:.3f} ms")
+print(f"GE symbols T=1e8: smoother {ts:.3f} ms ({T/ts*1e3:.3e} steps/s), viterbi {tv:.3f} ms")
