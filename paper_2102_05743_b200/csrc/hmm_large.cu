@@ -156,6 +156,17 @@ __global__ void __launch_bounds__(256) lg_leaf_kernel(const LgParams p) {
             for (int k = 0; k < DP; k++) Acol[c][k] = lg_A(p, k, j, MP);
             pv[c] = lg_pi(p, j, MP);
         }
+        constexpr bool PK = (CPL == 1);           // packed row pairs (DP = 16, 32; see the loop)
+        constexpr bool PC = (CPL == 2 && MP);     // packed column pairs (max-product, DP = 64)
+        float2 A2[(PK || PC) ? DP : 1];
+        if constexpr (PK) {
+    #pragma unroll
+            for (int k = 0; k < DP; k++) A2[k] = make_float2(Acol[0][k], Acol[0][k]);
+        }
+        if constexpr (PC) {
+    #pragma unroll
+            for (int k = 0; k < DP; k++) A2[k] = make_float2(Acol[0][k], Acol[1][k]);
+        }
         const float* ll = p.log_lik + (size_t)b * T * p.D;
         bool bad = false;
         float s = MP ? 0.0f : 1.0f;  // pending normalisation (scale / offset) from the previous step
@@ -182,6 +193,65 @@ __global__ void __launch_bounds__(256) lg_leaf_kernel(const LgParams p) {
                 } else {
                     l[c] = ex2((v[c] - m) * kLog2e);
                 }
+            }
+            if constexpr (PK) {
+                // DP = 16, one column per lane: P kept with row pairs interleaved, element (r, j) at
+                // Pm[(r/2)*2DP + 2j + r%2], so one LDS.128 yields (P(r,k), P(r+1,k)) and (P(r,k+1),
+                // P(r+1,k+1)) and each FFMA2 / FADD2 updates two rows of the lane's column with the
+                // duplicated A(k, j): the same multiply-adds as the scalar loop in half the issue slots
+                // (the max-product adds keep their operands, so its values are bit-identical).
+                constexpr int NRP = DP / 2;
+                if (i == 0) {
+                    if (act) {
+    #pragma unroll
+                        for (int rp = 0; rp < NRP; rp++) {
+                            const float a0 = (t == 0) ? pv[0] : Acol[0][2 * rp];
+                            const float a1 = (t == 0) ? pv[0] : Acol[0][2 * rp + 1];
+                            *reinterpret_cast<float2*>(Pm + rp * 2 * DP + 2 * cl) =
+                                MP ? make_float2(a0 + l[0], a1 + l[0]) : make_float2(a0 * l[0], a1 * l[0]);
+                        }
+                    }
+                    __syncwarp();
+                } else {
+                    float2 acc[NRP];
+    #pragma unroll
+                    for (int rp = 0; rp < NRP; rp++) acc[rp] = MP ? make_float2(neg_inf(), neg_inf()) : make_float2(0.0f, 0.0f);
+    #pragma unroll
+                    for (int rp = 0; rp < NRP; rp++) {
+    #pragma unroll
+                        for (int k = 0; k < DP; k += 2) {
+                            const float4 x = *reinterpret_cast<const float4*>(Pm + rp * 2 * DP + 2 * k);
+                            if constexpr (MP) {
+                                const float2 s0 = __fadd2_rn(make_float2(x.x, x.y), A2[k]);
+                                const float2 s1 = __fadd2_rn(make_float2(x.z, x.w), A2[k + 1]);
+                                acc[rp] = make_float2(max3(acc[rp].x, s0.x, s1.x), max3(acc[rp].y, s0.y, s1.y));
+                            } else {
+                                acc[rp] = __ffma2_rn(make_float2(x.x, x.y), A2[k], acc[rp]);
+                                acc[rp] = __ffma2_rn(make_float2(x.z, x.w), A2[k + 1], acc[rp]);
+                            }
+                        }
+                    }
+                    __syncwarp();
+                    float mx = MP ? neg_inf() : 0.0f;
+                    if (act) {
+                        const float f = MP ? (l[0] - s) : (l[0] * s);
+                        const float2 f2 = make_float2(f, f);
+    #pragma unroll
+                        for (int rp = 0; rp < NRP; rp++) {
+                            const float2 val = MP ? __fadd2_rn(acc[rp], f2) : __fmul2_rn(acc[rp], f2);
+                            *reinterpret_cast<float2*>(Pm + rp * 2 * DP + 2 * cl) = val;
+                            mx = max3(mx, val.x, val.y);
+                        }
+                    }
+                    __syncwarp();
+                    mx = grp_max<LPL>(mx);
+                    if constexpr (MP) {
+                        s = (mx > neg_inf()) ? mx : 0.0f;
+                    } else {
+                        s = pow2_inv(mx);
+                    }
+                }
+                continue;
             }
             if (i == 0) {
                 if (act) {
@@ -212,7 +282,18 @@ __global__ void __launch_bounds__(256) lg_leaf_kernel(const LgParams p) {
                             const float4 x = *reinterpret_cast<const float4*>(Pm + (r0 + rr) * DP + k4);
     #pragma unroll
                             for (int c = 0; c < CPL; c++) {
-                                if constexpr (MP) {
+                                if constexpr (PC) {
+                                    // the lane's two columns as one FADD2 per k (scalar P(r,k) broadcast),
+                                    // maxima by FMNMX3: same sums as the scalar form, bit-identical
+                                    if (c == 0) {
+                                        const float2 s0 = __fadd2_rn(make_float2(x.x, x.x), A2[k4]);
+                                        const float2 s1 = __fadd2_rn(make_float2(x.y, x.y), A2[k4 + 1]);
+                                        const float2 s2 = __fadd2_rn(make_float2(x.z, x.z), A2[k4 + 2]);
+                                        const float2 s3 = __fadd2_rn(make_float2(x.w, x.w), A2[k4 + 3]);
+                                        acc[rr][0] = max3(max3(acc[rr][0], s0.x, s1.x), s2.x, s3.x);
+                                        acc[rr][1] = max3(max3(acc[rr][1], s0.y, s1.y), s2.y, s3.y);
+                                    }
+                                } else if constexpr (MP) {
                                     acc[rr][c] = fmaxf(acc[rr][c], max3(x.x + Acol[c][k4], x.y + Acol[c][k4 + 1],
                                                                         fmaxf(x.z + Acol[c][k4 + 2], x.w + Acol[c][k4 + 3])));
                                 } else {
@@ -243,6 +324,21 @@ __global__ void __launch_bounds__(256) lg_leaf_kernel(const LgParams p) {
                 } else {
                     s = pow2_inv(mx);
                 }
+            }
+        }
+        if constexpr (PK) {  // back to row-major (each lane moves its own column)
+            if (nmax > 0) {
+                float colv[DP];
+    #pragma unroll
+                for (int rp = 0; rp < DP / 2; rp++) {
+                    const float2 v2 = *reinterpret_cast<const float2*>(Pm + rp * 2 * DP + 2 * cl);
+                    colv[2 * rp] = v2.x;
+                    colv[2 * rp + 1] = v2.y;
+                }
+                __syncwarp();
+    #pragma unroll
+                for (int r = 0; r < DP; r++) Pm[r * DP + cl] = colv[r];
+                __syncwarp();
             }
         }
         // final normalisation and NaN check, then write the leaf aggregate (reductions warp-uniform: the
@@ -538,15 +634,24 @@ __global__ void __launch_bounds__(256) lg_sweep_kernel(const LgParams p) {
         int rexp = 0;
         double msum = 0.0;
         float* filt = p.filtered;
+        // the log-likelihood row of step i+1 is loaded during step i: the serial per-step chain never
+        // waits on global memory
+        auto ld_ll = [&](int i, float* v) {
+#pragma unroll
+            for (int c = 0; c < CPL; c++) {
+                const int j = cl * CPL + c;
+                v[c] = (i >= 0 && i < n && j < D) ? __ldg(ll + (t0 + i) * D + j) : neg_inf();
+            }
+        };
+        float vnext[CPL];
+        ld_ll(0, vnext);
         for (int i = 0; i < nmax; i++) {
             const bool act = i < n;
             const int64_t t = t0 + i;
             float v[CPL], l[CPL], ah[CPL];
 #pragma unroll
-            for (int c = 0; c < CPL; c++) {
-                const int j = cl * CPL + c;
-                v[c] = (act && j < D) ? __ldg(ll + t * D + j) : neg_inf();
-            }
+            for (int c = 0; c < CPL; c++) v[c] = vnext[c];
+            ld_ll(i + 1, vnext);
             float m = v[0];
 #pragma unroll
             for (int c = 1; c < CPL; c++) m = fmaxf(m, v[c]);
@@ -615,16 +720,32 @@ __global__ void __launch_bounds__(256) lg_sweep_kernel(const LgParams p) {
         float bt[CPL];
 #pragma unroll
         for (int c = 0; c < CPL; c++) bt[c] = lsuf[lidx * DP + cl * CPL + c];
-        for (int i = nmax - 1; i >= 0; i--) {
-            const bool act = i < n;
-            const int64_t t = t0 + i;
-            float g[CPL];
-            float z = 0.0f;
+        // filtered row of step i and log-likelihood row of step i loaded one iteration ahead
+        auto ld_f = [&](int i, float* a) {
 #pragma unroll
             for (int c = 0; c < CPL; c++) {
                 const int j = cl * CPL + c;
-                const float a = (act && j < D) ? filt[((size_t)b * T + t) * D + j] : 0.0f;
-                g[c] = a * bt[c];
+                a[c] = (i >= 0 && i < n && j < D) ? filt[((size_t)b * T + t0 + i) * D + j] : 0.0f;
+            }
+        };
+        float fnext[CPL], lnext[CPL];
+        ld_f(nmax - 1, fnext);
+        ld_ll(nmax - 1, lnext);
+        for (int i = nmax - 1; i >= 0; i--) {
+            const bool act = i < n;
+            const int64_t t = t0 + i;
+            float g[CPL], fa[CPL], lv[CPL];
+#pragma unroll
+            for (int c = 0; c < CPL; c++) {
+                fa[c] = fnext[c];
+                lv[c] = lnext[c];
+            }
+            ld_f(i - 1, fnext);
+            if (i > 0) ld_ll(i - 1, lnext);
+            float z = 0.0f;
+#pragma unroll
+            for (int c = 0; c < CPL; c++) {
+                g[c] = fa[c] * bt[c];
                 z += g[c];
             }
             z = grp_sum<LPL>(z);
@@ -637,10 +758,7 @@ __global__ void __launch_bounds__(256) lg_sweep_kernel(const LgParams p) {
             if (i > 0) {
                 float v[CPL];
 #pragma unroll
-                for (int c = 0; c < CPL; c++) {
-                    const int j = cl * CPL + c;
-                    v[c] = (act && j < D) ? __ldg(ll + t * D + j) : neg_inf();
-                }
+                for (int c = 0; c < CPL; c++) v[c] = lv[c];
                 float m = v[0];
 #pragma unroll
                 for (int c = 1; c < CPL; c++) m = fmaxf(m, v[c]);
@@ -697,15 +815,22 @@ __global__ void __launch_bounds__(256) lg_sweep_kernel(const LgParams p) {
         float V[CPL];
 #pragma unroll
         for (int c = 0; c < CPL; c++) V[c] = vv[cl * CPL + c];
+        auto ld_llv = [&](int i, float* v) {  // row of step i, loaded one step ahead (as the smoother)
+#pragma unroll
+            for (int c = 0; c < CPL; c++) {
+                const int j = cl * CPL + c;
+                v[c] = (i >= 0 && i < n && j < D) ? __ldg(ll + (t0 + i) * D + j) : neg_inf();
+            }
+        };
+        float vnext[CPL];
+        ld_llv(0, vnext);
         for (int i = 0; i < nmax; i++) {
             const bool act = i < n;
             const int64_t t = t0 + i;
             float v[CPL];
 #pragma unroll
-            for (int c = 0; c < CPL; c++) {
-                const int j = cl * CPL + c;
-                v[c] = (act && j < D) ? __ldg(ll + t * D + j) : neg_inf();
-            }
+            for (int c = 0; c < CPL; c++) v[c] = vnext[c];
+            ld_llv(i + 1, vnext);
             float m = v[0];
 #pragma unroll
             for (int c = 1; c < CPL; c++) m = fmaxf(m, v[c]);
