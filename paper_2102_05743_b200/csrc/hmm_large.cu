@@ -843,6 +843,28 @@ __global__ void __launch_bounds__(256) lg_sweep_kernel(const LgParams p) {
                 best[c] = neg_inf();
                 arg[c] = 0;
             }
+            if constexpr (CPL == 1) {
+                // scores from 16-B broadcast reads, the max by a FMNMX3 tree, then the smallest
+                // index attaining it (reading 5) by independent compares: no serial
+                // compare-select chain through the DP candidates
+                float sc[DP];
+#pragma unroll
+                for (int k4 = 0; k4 < DP; k4 += 4) {
+                    const float4 x = *reinterpret_cast<const float4*>(vv + k4);
+                    sc[k4] = x.x + ((t == 0) ? lpv[0] : LAc[0][k4]);
+                    sc[k4 + 1] = x.y + ((t == 0) ? lpv[0] : LAc[0][k4 + 1]);
+                    sc[k4 + 2] = x.z + ((t == 0) ? lpv[0] : LAc[0][k4 + 2]);
+                    sc[k4 + 3] = x.w + ((t == 0) ? lpv[0] : LAc[0][k4 + 3]);
+                }
+                const float bm = vmax_tree<DP>(sc);
+                int a = 0;
+#pragma unroll
+                for (int k = DP - 1; k >= 0; k--) a = (sc[k] == bm) ? k : a;
+                if (bm > neg_inf()) {
+                    best[0] = bm;
+                    arg[0] = a;
+                }
+            } else {
 #pragma unroll
             for (int k = 0; k < DP; k++) {
                 const float vk = vv[k];
@@ -854,6 +876,7 @@ __global__ void __launch_bounds__(256) lg_sweep_kernel(const LgParams p) {
                         arg[c] = k;
                     }
                 }
+            }
             }
             float o = neg_inf(), Vn[CPL];
 #pragma unroll
