@@ -208,7 +208,9 @@ bool make_large_plan(int D, int op, int64_t T, int64_t B, LgPlan& P, bool allow_
     // leaf kernel runs 2 leaf pairs per SM, so it wants ~4 leaves per SM
     // (tensor-core leaves: 2 leaf pairs per SM per wave; 2 waves so the sweep kernel, NLB leaves
     // per CTA, still covers every SM)
-    const int64_t target = P.tc ? (int64_t)di.sms * 8 : (int64_t)di.sms * 2 * NLB;
+    // (DP = 64 on CUDA cores: one 256-thread CTA per SM (214 registers), so two waves of blocks buy no
+    // balance and only double the serial block-root chains of the carry / resolve kernels: one wave)
+    const int64_t target = P.tc ? (int64_t)di.sms * 8 : (int64_t)di.sms * (P.DP == 64 ? 1 : 2) * NLB;
     int64_t SL = cdiv(T * B, target);
     // many sequences (one block each): fill every block's NLB leaf slots -- the leaf chains are
     // latency-bound, so idle slots cost throughput directly
