@@ -14,3 +14,5 @@ python tools/time_configs.py big > $OUT/configs.txt 2>&1
 python tools/stream_phases.py > $OUT/phases.txt 2>&1
 python tools/dist_rank_timing.py > $OUT/dist_rank_timing.txt 2>&1
 python tools/time_symbols.py > $OUT/symbols.txt 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file $OUT/config3_launches.csv python tools/run_config3.py > /dev/null 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file $OUT/config4_launches.csv python tools/run_config4.py > /dev/null 2>&1
