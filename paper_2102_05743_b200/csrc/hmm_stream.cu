@@ -153,10 +153,11 @@ __device__ __forceinline__ void sp_chain_start2(const float* row, const float2* 
     for (int e = 0; e < D * H; e++) mx[e] = fmaxf(X2[e].x, X2[e].y);
     d = exp_offset(vmax2_tree<D * H>(mx));
 }
-// One slice, right to left (sum-product).  Unlike the max-product fold below, the sum-product step is
-// issue-bound rather than latency-bound at 8 warps/SM (ncu: 66% issue-active, `wait` stalls 0.34 per
-// issue), so the two-chain split would only add its combine/normalise instructions (~7%): one chain.
-// Even D runs the packed-pair step for every step but the sequence's first.
+// One slice, right to left (sum-product).  D = 2, 4 run the packed-pair steps; full slices that do not
+// start the sequence are folded as two chains (as the max-product fold below): with the packed step the
+// issue slots are no longer the limit, and the 2x ILP took the T=1e8 smoother from 1.36 to 1.32 ms
+// (with scalar steps the fold was issue-bound and the combine only added work).  Other slices, and
+// odd D / D > 4, keep one chain.  HMM_SP_TWO_CHAIN=0 builds the one-chain packed fold for comparison.
 template <int D, int S, class RS>
 __device__ __forceinline__ void sp_fold_back(const RS rows, int nr, bool t0, const float* A, const float* pi,
                                              float* P, float& d) {
