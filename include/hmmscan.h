@@ -191,6 +191,27 @@ hmm_status_t hmm_viterbi_dist_finish(int D, int64_t T_local, int64_t t_base, con
                                      void* stream);
 
 /*
+ * Split-phase scalar plumbing for a step that runs the smoother and Viterbi on the same partition with
+ * merged collectives (paper_2102_05743_b200.dist.smooth_viterbi_dist), replacing a few dozen tiny
+ * host-launched tensor ops per step by two launches.  All pointers are device memory; one thread does the
+ * work, stream-ordered; HMM_ERR_INVALID_VALUE for a NULL pointer or world < 1.
+ *   hmm_dist_pack: one rank's record as 8 doubles, packed8 = {the 16-byte Viterbi rank record
+ *     (hmm_viterbi_dist_forward's record_out, bit-copied into doubles 0-1), log_z_partial,
+ *     log_prob_partial, the four info codes (smoother reduce, smoother finish, Viterbi reduce, Viterbi
+ *     forward) as doubles (exact)}.  The caller all-gathers packed8 into gathered[world][8], rank order.
+ *   hmm_dist_combine: from gathered: records_all (16*world bytes, rank order, the input of
+ *     hmm_viterbi_dist_finish), log_z = sum of the log_z partials and log_prob = sum of the log_prob
+ *     partials, each added in rank order starting from 0.0 (log Z; Eq. 16-17), and the
+ *     global info / vinfo: -1 if any rank reported -1 (bad input), else the smallest positive code (the
+ *     first impossible global step + 1), else 0.
+ */
+hmm_status_t hmm_dist_pack(const void* record16, const double* log_z_partial, const double* log_prob_partial,
+                           const int32_t* s_info_reduce, const int32_t* s_info_finish, const int32_t* v_info_reduce,
+                           const int32_t* v_info_forward, double* packed8, void* stream);
+hmm_status_t hmm_dist_combine(int world, const double* gathered, void* records_all, double* log_z,
+                              double* log_prob, int32_t* info, int32_t* vinfo, void* stream);
+
+/*
  * Profiling / introspection (not part of the compute path).
  *   hmm_debug_set_timers: for calls made later from the calling host thread, CTA phase timestamps
  *     (%globaltimer, ns) are written to device_buf[(b*G + c)*16 + i] (NULL disables).

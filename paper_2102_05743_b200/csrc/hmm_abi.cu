@@ -406,9 +406,68 @@ hmm_status_t run_symbols(int op, int D, int V, int64_t T, const float* log_pi, c
     return e == cudaSuccess ? HMM_SUCCESS : HMM_ERR_CUDA;
 }
 
+// Split-phase scalar plumbing (hmm_dist_pack / hmm_dist_combine): one thread each.
+__global__ void dist_pack_kernel(const uint64_t* rec, const double* lz, const double* lp, const int32_t* a,
+                                 const int32_t* b, const int32_t* c, const int32_t* d, double* out) {
+    out[0] = __longlong_as_double((long long)rec[0]);
+    out[1] = __longlong_as_double((long long)rec[1]);
+    out[2] = lz[0];
+    out[3] = lp[0];
+    out[4] = (double)a[0];
+    out[5] = (double)b[0];
+    out[6] = (double)c[0];
+    out[7] = (double)d[0];
+}
+__device__ int32_t combine_codes(const double* g, int world, int c0) {
+    bool bad = false;
+    int32_t first = INT32_MAX;
+    for (int r = 0; r < world; r++)
+        for (int c = c0; c < c0 + 2; c++) {
+            const int32_t v = (int32_t)g[(size_t)r * 8 + c];
+            if (v == -1) bad = true;
+            else if (v > 0 && v < first) first = v;
+        }
+    return bad ? -1 : (first == INT32_MAX ? 0 : first);
+}
+__global__ void dist_combine_kernel(int world, const double* g, uint64_t* rec_all, double* lz, double* lp,
+                                    int32_t* info, int32_t* vinfo) {
+    double z = 0.0, q = 0.0;
+    for (int r = 0; r < world; r++) {  // rank order
+        rec_all[2 * r] = (uint64_t)__double_as_longlong(g[(size_t)r * 8]);
+        rec_all[2 * r + 1] = (uint64_t)__double_as_longlong(g[(size_t)r * 8 + 1]);
+        z += g[(size_t)r * 8 + 2];
+        q += g[(size_t)r * 8 + 3];
+    }
+    lz[0] = z;
+    lp[0] = q;
+    info[0] = combine_codes(g, world, 4);
+    vinfo[0] = combine_codes(g, world, 6);
+}
+
 }  // namespace
 
 extern "C" {
+
+hmm_status_t hmm_dist_pack(const void* record16, const double* log_z_partial, const double* log_prob_partial,
+                           const int32_t* s_info_reduce, const int32_t* s_info_finish, const int32_t* v_info_reduce,
+                           const int32_t* v_info_forward, double* packed8, void* stream) {
+    if (!record16 || !log_z_partial || !log_prob_partial || !s_info_reduce || !s_info_finish || !v_info_reduce ||
+        !v_info_forward || !packed8)
+        return HMM_ERR_INVALID_VALUE;
+    dist_pack_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const uint64_t*>(record16), log_z_partial, log_prob_partial, s_info_reduce, s_info_finish,
+        v_info_reduce, v_info_forward, packed8);
+    return cudaGetLastError() == cudaSuccess ? HMM_SUCCESS : HMM_ERR_CUDA;
+}
+
+hmm_status_t hmm_dist_combine(int world, const double* gathered, void* records_all, double* log_z,
+                              double* log_prob, int32_t* info, int32_t* vinfo, void* stream) {
+    if (world < 1 || !gathered || !records_all || !log_z || !log_prob || !info || !vinfo)
+        return HMM_ERR_INVALID_VALUE;
+    dist_combine_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(
+        world, gathered, static_cast<uint64_t*>(records_all), log_z, log_prob, info, vinfo);
+    return cudaGetLastError() == cudaSuccess ? HMM_SUCCESS : HMM_ERR_CUDA;
+}
 
 const char* hmm_status_string(hmm_status_t status) {
     switch (status) {

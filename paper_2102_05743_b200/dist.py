@@ -51,11 +51,32 @@ class LibBackend:
         L.hmm_viterbi_dist_reduce.argtypes = [i32, i64, i64, p, p, p, p, p, p, sz, p]
         L.hmm_viterbi_dist_forward.argtypes = [i32, i64, i64, p, p, p, p, i32, i32, p, p, p, p, sz, p]
         L.hmm_viterbi_dist_finish.argtypes = [i32, i64, i64, p, p, p, p, i32, i32, p, p, p, sz, p]
+        L.hmm_dist_pack.argtypes = [p, p, p, p, p, p, p, p, p]
+        L.hmm_dist_combine.argtypes = [i32, p, p, p, p, p, p, p]
         for f in ("hmm_smooth_dist_reduce", "hmm_smooth_dist_finish", "hmm_viterbi_dist_reduce",
-                  "hmm_viterbi_dist_forward", "hmm_viterbi_dist_finish"):
+                  "hmm_viterbi_dist_forward", "hmm_viterbi_dist_finish", "hmm_dist_pack", "hmm_dist_combine"):
             getattr(L, f).restype = i32
         self.L = L
         self._ws = {}
+
+    def pack(self, rec, lzp, lpp, s_i1, s_i2, v_i1, v_i2):
+        """One rank's 8-double record for the second merged all-gather (hmm_dist_pack)."""
+        out = torch.empty(8, dtype=torch.float64, device=rec.device)
+        _check(self.L.hmm_dist_pack(_ptr(rec), _ptr(lzp), _ptr(lpp), _ptr(s_i1), _ptr(s_i2), _ptr(v_i1), _ptr(v_i2),
+                                    _ptr(out), _stream(None)), "hmm_dist_pack")
+        return out
+
+    def combine(self, g, world):
+        """Records in rank order, log Z, log_prob and the global info codes from the gathered records."""
+        dev = g.device
+        rec_all = torch.empty(16 * world, dtype=torch.uint8, device=dev)
+        lz = torch.empty(1, dtype=torch.float64, device=dev)
+        lp = torch.empty(1, dtype=torch.float64, device=dev)
+        info = torch.empty(1, dtype=torch.int32, device=dev)
+        vinfo = torch.empty(1, dtype=torch.int32, device=dev)
+        _check(self.L.hmm_dist_combine(world, _ptr(g), _ptr(rec_all), _ptr(lz), _ptr(lp), _ptr(info), _ptr(vinfo),
+                                       _stream(None)), "hmm_dist_combine")
+        return rec_all, lz, lp, info, vinfo
 
     def agg_bytes(self, D):
         return int(self.L.hmm_dist_agg_bytes(D))
@@ -205,6 +226,12 @@ def smooth_viterbi_dist(log_pi, log_A, log_lik_local, t_base: int, group=None, b
     v_all = both[:, na:].contiguous().view(-1)
     filt, sm, lzp, s_i2 = be.smooth_finish(log_pi, log_A, log_lik_local, t_base, s_all, rank, world)
     rec, lpp, v_i2 = be.viterbi_forward(log_pi, log_A, log_lik_local, t_base, v_all, rank, world)
+    if hasattr(be, "pack") and rec.is_cuda:
+        # two library launches instead of the tensor ops below (same values, bit for bit)
+        g = _all_gather(be.pack(rec, lzp, lpp, s_i1, s_i2, v_i1, v_i2), group)
+        rec_all, log_z, log_prob, info, vinfo = be.combine(g, world)
+        path, _ = be.viterbi_finish(log_pi, log_A, log_lik_local, t_base, rec_all, rank, world)
+        return filt, sm, log_z, info, path, log_prob, vinfo
     sc = torch.stack([lzp.view(()), lpp.view(()), s_i1.double().view(()), s_i2.double().view(()),
                       v_i1.double().view(()), v_i2.double().view(())])
     packed = torch.cat([rec.view(torch.float64).view(-1).to(sc.device), sc])  # 2 + 6 float64 per rank

@@ -102,3 +102,36 @@ def test_dist_info_global_step():
     assert min(i for i in info if i > 0) == 250_124
     _, _, vinfo = emulate_viterbi(wl, 4)
     assert min(i for i in vinfo if i > 0) == 250_124
+
+
+@pytest.mark.parametrize("world", [1, 3, 8])
+@pytest.mark.parametrize("codes", [(0, 0, 0, 0), (0, 17, 0, 5), (-1, 3, 0, 0), (0, 0, 9, -1)])
+def test_dist_pack_combine(world, codes):
+    """hmm_dist_pack / hmm_dist_combine against the tensor-op combination they replace: records in rank
+    order, log Z and log_prob summed in rank order from 0.0 (bit for bit), global info codes."""
+    from paper_2102_05743_b200.dist import LibBackend, _combine_info
+    be = LibBackend()
+    dev = torch.device("cuda")
+    g = torch.Generator().manual_seed(world * 31 + codes[1])
+    rows, recs, lzs, lps, infos = [], [], [], [], []
+    for r in range(world):
+        rec = torch.randint(0, 256, (16,), dtype=torch.uint8, generator=g)
+        lz = torch.randn(1, dtype=torch.float64, generator=g) * 1e6
+        lp = torch.randn(1, dtype=torch.float64, generator=g) * 1e6
+        cs = [c if r == world - 1 or c <= 0 else c + 100 * r for c in codes]  # rank 0 holds the smallest
+        ii = [torch.tensor([c], dtype=torch.int32) for c in cs]
+        rows.append(be.pack(rec.to(dev), lz.to(dev), lp.to(dev), *[t.to(dev) for t in ii]))
+        recs.append(rec); lzs.append(lz); lps.append(lp); infos.append(cs)
+    gathered = torch.cat(rows)
+    rec_all, lz, lp, info, vinfo = be.combine(gathered, world)
+    torch.cuda.synchronize()
+    assert torch.equal(rec_all.cpu(), torch.cat(recs))
+    ez, ep = torch.zeros(1, dtype=torch.float64), torch.zeros(1, dtype=torch.float64)
+    for r in range(world):
+        ez += lzs[r]
+        ep += lps[r]
+    assert float(lz[0]) == float(ez[0]) and float(lp[0]) == float(ep[0])
+    s_codes = torch.tensor([c for cs in infos for c in cs[:2]], dtype=torch.int32)
+    v_codes = torch.tensor([c for cs in infos for c in cs[2:]], dtype=torch.int32)
+    assert int(info[0]) == int(_combine_info(s_codes)[0])
+    assert int(vinfo[0]) == int(_combine_info(v_codes)[0])
