@@ -272,8 +272,9 @@ def run_multi(args, world, rank, local):
             "cpu_baseline": None,
             "e2e": {"value": Tg / (ms_e2e * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h_ll.numel() * 4),
                     "d2h_bytes_per_step": 16, "ms_per_step": ms_e2e},
-            "gpu_launches": 7 * args.steps,  # 5 phase kernels + hmm_dist_pack + hmm_dist_combine "clocks": clk.summary(),
-            "smoother_viterbi_split": "5 library launches + 2 NCCL all-gathers per step (merged collectives)",
+            "gpu_launches": 7 * args.steps, "clocks": clk.summary(),
+            "smoother_viterbi_split": "7 library launches (5 phases + hmm_dist_pack + hmm_dist_combine) + 2 NCCL "
+                                      "all-gathers per step (merged collectives)",
         }), flush=True)
     dist.destroy_process_group()
 
