@@ -36,6 +36,14 @@
  *     state sequence is consistent with the evidence and the transitions up to t (zero forward mass
  *     for the smoother, all V_t = -inf for Viterbi); -1 = a NaN or +inf input.
  *     When info != 0 the other outputs of that sequence are undefined (cuSOLVER devInfo idiom).
+ *   - Kernels whose CTAs meet at a grid barrier bound the wait (4 s): a barrier that can never
+ *     complete (a workspace left dirty by an aborted or faulted launch, or a CTA that is not resident)
+ *     traps instead of hanging the device.  The stream then reports cudaErrorLaunchFailure, the CUDA
+ *     context is unusable, and any workspace used by a failed call must be zero-filled again before
+ *     reuse (the kernels only restore the zero state on successful completion).
+ *   - Threading: any host thread may call; the per-device kernel-attribute record is mutex-guarded, so
+ *     concurrent first calls and several GPUs in one process are safe (one workspace per concurrent
+ *     call).
  */
 #ifndef HMMSCAN_H
 #define HMMSCAN_H
@@ -166,7 +174,13 @@ hmm_status_t hmm_viterbi_batched(int D, int64_t T, int64_t B, const float* log_p
  *      log_prob_partial[1]; log_prob = sum of partials over ranks.
  *   4. caller: all-gather the records -> records_all[world]
  *   5. hmm_viterbi_dist_finish  -> path of the local slice.
- * info: reduce reports bad inputs (-1); finish/forward report the first impossible GLOBAL step + 1.
+ * info: reduce reports bad inputs (-1); smoother finish / Viterbi forward report the first impossible
+ * GLOBAL step + 1; hmm_viterbi_dist_finish only backtracks and always writes info = 0.
+ * Kernel choice: every phase of a rank must run the same decomposition (later phases read the workspace
+ * layout the reduce call wrote), so it is chosen from log_lik's alignment alone: 16-B aligned log_lik
+ * selects the lane-streaming kernel, and then filtered / smoothed / path must be 16-B aligned too
+ * (HMM_ERR_INVALID_VALUE otherwise); a log_lik that is only 4-B aligned selects the chunked kernel in
+ * every phase.
  */
 size_t hmm_dist_agg_bytes(int D);
 size_t hmm_dist_record_bytes(void);
@@ -193,8 +207,12 @@ hmm_status_t hmm_viterbi_dist_finish(int D, int64_t T_local, int64_t t_base, con
 /*
  * Split-phase scalar plumbing for a step that runs the smoother and Viterbi on the same partition with
  * merged collectives (paper_2102_05743_b200.dist.smooth_viterbi_dist), replacing a few dozen tiny
- * host-launched tensor ops per step by two launches.  All pointers are device memory; one thread does the
- * work, stream-ordered; HMM_ERR_INVALID_VALUE for a NULL pointer or world < 1.
+ * host-launched tensor ops per step by two launches; the smoother-only and Viterbi-only split steps use the
+ * same pair (paper_2102_05743_b200.dist.smooth_dist / viterbi_dist).  All pointers are device memory; one
+ * thread does the work, stream-ordered.  Any INPUT of hmm_dist_pack may be NULL (it contributes zeros);
+ * any OUTPUT of hmm_dist_combine except `gathered` may be NULL (not written).  record16, packed8,
+ * gathered, records_all and the doubles must be 8-byte aligned, the int32 words 4-byte aligned:
+ * HMM_ERR_INVALID_VALUE otherwise, or for NULL packed8 / gathered, or world < 1.
  *   hmm_dist_pack: one rank's record as 8 doubles, packed8 = {the 16-byte Viterbi rank record
  *     (hmm_viterbi_dist_forward's record_out, bit-copied into doubles 0-1), log_z_partial,
  *     log_prob_partial, the four info codes (smoother reduce, smoother finish, Viterbi reduce, Viterbi

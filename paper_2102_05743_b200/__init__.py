@@ -117,10 +117,14 @@ def workspace_size(op: int, D: int, T: int, B: int = 1) -> int:
     return int(lib().hmm_workspace_size(op, D, T, B))
 
 
-def workspace(op: int, D: int, T: int, B: int = 1, device=None) -> torch.Tensor:
-    """Zero-filled device workspace (cached per device/shape; the kernels leave it zeroed)."""
+def workspace(op: int, D: int, T: int, B: int = 1, device=None, stream=None) -> torch.Tensor:
+    """Zero-filled device workspace (cached per device/shape/stream; the kernels leave it zeroed).
+
+    Calls that may run concurrently need distinct workspaces (hmmscan.h), so the cache is keyed by the
+    stream as well: two streams never share one (the grid-barrier counters would collide)."""
     device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
-    key = (device, op, D, T, B)
+    sid = None if stream is None else int(stream.cuda_stream)
+    key = (device, op, D, T, B, sid)
     ws = _ws_cache.get(key)
     if ws is None:
         n = workspace_size(op, D, T, B)
@@ -159,7 +163,7 @@ def smooth(log_pi, log_A, log_lik, want_filtered: bool = True, out=None, ws=None
         info = torch.empty(B, dtype=torch.int32, device=dev)
     else:
         filt, sm, lz, info = out
-    ws = workspace(HMM_OP_SMOOTH, D, T, B, dev) if ws is None else ws
+    ws = workspace(HMM_OP_SMOOTH, D, T, B, dev, stream) if ws is None else ws
     L = lib()
     if batched:
         st = L.hmm_smooth_batched(D, T, B, _ptr(log_pi), _ptr(log_A), _ptr(log_lik), _ptr(filt), _ptr(sm),
@@ -187,7 +191,7 @@ def smooth_stats(log_pi, log_A, log_lik, want_marginals: bool = True, stream=Non
     xi = torch.empty((D, D), dtype=torch.float64, device=dev)
     g = torch.empty(D, dtype=torch.float64, device=dev)
     info = torch.empty(1, dtype=torch.int32, device=dev)
-    ws = workspace(HMM_OP_SMOOTH_STATS, D, T, 1, dev)
+    ws = workspace(HMM_OP_SMOOTH_STATS, D, T, 1, dev, stream)
     st = lib().hmm_smooth_stats(D, T, _ptr(log_pi), _ptr(log_A), _ptr(log_lik), _ptr(filt), _ptr(sm), _ptr(lz),
                                 _ptr(xi), _ptr(g), _ptr(info), _ptr(ws), ws.numel(), _stream(stream))
     _check(st, "hmm_smooth_stats")
@@ -200,7 +204,14 @@ def _sym_inputs(log_pi, log_A, log_B, y):
             raise HmmError(f"{name} must be a CUDA tensor (no CPU path)")
     if y.dtype != torch.uint8 or y.dim() != 1 or not y.is_contiguous():
         raise HmmError("y: contiguous uint8 [T]")
+    for name, t in (("log_pi", log_pi), ("log_A", log_A), ("log_B", log_B)):
+        if t.dtype != torch.float32 or not t.is_contiguous():
+            raise HmmError(f"{name}: contiguous float32")
+    if log_B.dim() != 2:
+        raise HmmError("log_B: [D, V]")
     D, V = log_B.shape
+    if tuple(log_pi.shape) != (D,) or tuple(log_A.shape) != (D, D):
+        raise HmmError("shape mismatch: log_pi [D], log_A [D, D], log_B [D, V]")
     return D, V, y.numel()
 
 
@@ -213,7 +224,7 @@ def smooth_symbols(log_pi, log_A, log_B, y, want_filtered: bool = True, stream=N
     sm = torch.empty((T, D), dtype=torch.float32, device=dev)
     lz = torch.empty(1, dtype=torch.float64, device=dev)
     info = torch.empty(1, dtype=torch.int32, device=dev)
-    ws = workspace(HMM_OP_SMOOTH, D, T, 1, dev)
+    ws = workspace(HMM_OP_SMOOTH, D, T, 1, dev, stream)
     st = lib().hmm_smooth_symbols(D, V, T, _ptr(log_pi), _ptr(log_A), _ptr(log_B), _ptr(y), _ptr(filt), _ptr(sm),
                                   _ptr(lz), _ptr(info), _ptr(ws), ws.numel(), _stream(stream))
     _check(st, "hmm_smooth_symbols")
@@ -227,7 +238,7 @@ def viterbi_symbols(log_pi, log_A, log_B, y, stream=None):
     path = torch.empty(T, dtype=torch.int32, device=dev)
     lp = torch.empty(1, dtype=torch.float64, device=dev)
     info = torch.empty(1, dtype=torch.int32, device=dev)
-    ws = workspace(HMM_OP_VITERBI, D, T, 1, dev)
+    ws = workspace(HMM_OP_VITERBI, D, T, 1, dev, stream)
     st = lib().hmm_viterbi_symbols(D, V, T, _ptr(log_pi), _ptr(log_A), _ptr(log_B), _ptr(y), _ptr(path), _ptr(lp),
                                    _ptr(info), _ptr(ws), ws.numel(), _stream(stream))
     _check(st, "hmm_viterbi_symbols")
@@ -244,7 +255,7 @@ def viterbi(log_pi, log_A, log_lik, out=None, ws=None, stream=None):
         info = torch.empty(B, dtype=torch.int32, device=dev)
     else:
         path, lp, info = out
-    ws = workspace(HMM_OP_VITERBI, D, T, B, dev) if ws is None else ws
+    ws = workspace(HMM_OP_VITERBI, D, T, B, dev, stream) if ws is None else ws
     L = lib()
     if batched:
         st = L.hmm_viterbi_batched(D, T, B, _ptr(log_pi), _ptr(log_A), _ptr(log_lik), _ptr(path), _ptr(lp),

@@ -5,7 +5,9 @@
 
 #include <cstdint>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <utility>
 
 #include "../../include/hmmscan.h"
 #include "hmm_large.h"
@@ -20,6 +22,21 @@ int large_leaves_per_block(int DP);
 }
 
 using hmm::Plan;
+
+namespace hmm {
+cudaError_t ensure_smem_optin(const void* func, size_t smem) {
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, size_t> applied;  // (device, kernel) -> bytes set
+    int dev = 0;
+    if (cudaError_t e = cudaGetDevice(&dev); e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lock(mu);
+    size_t& have = applied[{dev, func}];
+    if (have >= smem) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) have = smem;
+    return e;
+}
+}  // namespace hmm
 
 namespace {
 
@@ -302,8 +319,17 @@ hmm_status_t run(int op, int D, int64_t T, int64_t B, const float* log_pi, const
         return HMM_ERR_INVALID_VALUE;
     if (dist && (D > 8 || B != 1 || da.world < 1 || da.rank < 0 || da.rank >= da.world || da.t_base < 0))
         return D > 8 ? HMM_ERR_UNSUPPORTED : HMM_ERR_INVALID_VALUE;
-    if (use_stream(D, T, B, dist) && al16(log_lik) && (!filtered || al16(filtered)) && (!smoothed || al16(smoothed)) &&
-        (!path || al16(path))) {
+    // The decomposition: the lane-streaming kernel needs 16-B aligned sequence buffers.  Outside the split
+    // phase a misaligned buffer just selects the resident/chunked kernel.  The split-phase calls of one
+    // rank must all run the same kernel (the finish/forward calls read the workspace layout the reduce
+    // call wrote), so there the choice depends on log_lik alone and misaligned outputs are an error.
+    const bool out16 = (!filtered || al16(filtered)) && (!smoothed || al16(smoothed)) && (!path || al16(path));
+    bool stream_path = use_stream(D, T, B, dist) && al16(log_lik);
+    if (stream_path && !out16) {
+        if (dist) return HMM_ERR_INVALID_VALUE;
+        stream_path = false;
+    }
+    if (stream_path) {
         StPlan SP;
         if (!make_stream_plan(D, op, T, SP)) return HMM_ERR_UNSUPPORTED;
         if (!ws || ws_bytes < SP.ws_total || (reinterpret_cast<uintptr_t>(ws) & 255u)) return HMM_ERR_WORKSPACE;
@@ -406,17 +432,18 @@ hmm_status_t run_symbols(int op, int D, int V, int64_t T, const float* log_pi, c
     return e == cudaSuccess ? HMM_SUCCESS : HMM_ERR_CUDA;
 }
 
-// Split-phase scalar plumbing (hmm_dist_pack / hmm_dist_combine): one thread each.
+// Split-phase scalar plumbing (hmm_dist_pack / hmm_dist_combine): one thread each.  A NULL input of
+// pack contributes zeros; a NULL output of combine is not written.
 __global__ void dist_pack_kernel(const uint64_t* rec, const double* lz, const double* lp, const int32_t* a,
                                  const int32_t* b, const int32_t* c, const int32_t* d, double* out) {
-    out[0] = __longlong_as_double((long long)rec[0]);
-    out[1] = __longlong_as_double((long long)rec[1]);
-    out[2] = lz[0];
-    out[3] = lp[0];
-    out[4] = (double)a[0];
-    out[5] = (double)b[0];
-    out[6] = (double)c[0];
-    out[7] = (double)d[0];
+    out[0] = rec ? __longlong_as_double((long long)rec[0]) : 0.0;
+    out[1] = rec ? __longlong_as_double((long long)rec[1]) : 0.0;
+    out[2] = lz ? lz[0] : 0.0;
+    out[3] = lp ? lp[0] : 0.0;
+    out[4] = a ? (double)a[0] : 0.0;
+    out[5] = b ? (double)b[0] : 0.0;
+    out[6] = c ? (double)c[0] : 0.0;
+    out[7] = d ? (double)d[0] : 0.0;
 }
 __device__ int32_t combine_codes(const double* g, int world, int c0) {
     bool bad = false;
@@ -433,15 +460,17 @@ __global__ void dist_combine_kernel(int world, const double* g, uint64_t* rec_al
                                     int32_t* info, int32_t* vinfo) {
     double z = 0.0, q = 0.0;
     for (int r = 0; r < world; r++) {  // rank order
-        rec_all[2 * r] = (uint64_t)__double_as_longlong(g[(size_t)r * 8]);
-        rec_all[2 * r + 1] = (uint64_t)__double_as_longlong(g[(size_t)r * 8 + 1]);
+        if (rec_all) {
+            rec_all[2 * r] = (uint64_t)__double_as_longlong(g[(size_t)r * 8]);
+            rec_all[2 * r + 1] = (uint64_t)__double_as_longlong(g[(size_t)r * 8 + 1]);
+        }
         z += g[(size_t)r * 8 + 2];
         q += g[(size_t)r * 8 + 3];
     }
-    lz[0] = z;
-    lp[0] = q;
-    info[0] = combine_codes(g, world, 4);
-    vinfo[0] = combine_codes(g, world, 6);
+    if (lz) lz[0] = z;
+    if (lp) lp[0] = q;
+    if (info) info[0] = combine_codes(g, world, 4);
+    if (vinfo) vinfo[0] = combine_codes(g, world, 6);
 }
 
 }  // namespace
@@ -451,8 +480,10 @@ extern "C" {
 hmm_status_t hmm_dist_pack(const void* record16, const double* log_z_partial, const double* log_prob_partial,
                            const int32_t* s_info_reduce, const int32_t* s_info_finish, const int32_t* v_info_reduce,
                            const int32_t* v_info_forward, double* packed8, void* stream) {
-    if (!record16 || !log_z_partial || !log_prob_partial || !s_info_reduce || !s_info_finish || !v_info_reduce ||
-        !v_info_forward || !packed8)
+    if (!packed8 || !al8(packed8) || (record16 && !al8(record16)) || (log_z_partial && !al8(log_z_partial)) ||
+        (log_prob_partial && !al8(log_prob_partial)) || (s_info_reduce && !al4(s_info_reduce)) ||
+        (s_info_finish && !al4(s_info_finish)) || (v_info_reduce && !al4(v_info_reduce)) ||
+        (v_info_forward && !al4(v_info_forward)))
         return HMM_ERR_INVALID_VALUE;
     dist_pack_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(
         static_cast<const uint64_t*>(record16), log_z_partial, log_prob_partial, s_info_reduce, s_info_finish,
@@ -462,7 +493,8 @@ hmm_status_t hmm_dist_pack(const void* record16, const double* log_z_partial, co
 
 hmm_status_t hmm_dist_combine(int world, const double* gathered, void* records_all, double* log_z,
                               double* log_prob, int32_t* info, int32_t* vinfo, void* stream) {
-    if (world < 1 || !gathered || !records_all || !log_z || !log_prob || !info || !vinfo)
+    if (world < 1 || !gathered || !al8(gathered) || (records_all && !al8(records_all)) || (log_z && !al8(log_z)) ||
+        (log_prob && !al8(log_prob)) || (info && !al4(info)) || (vinfo && !al4(vinfo)))
         return HMM_ERR_INVALID_VALUE;
     dist_combine_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(
         world, gathered, static_cast<uint64_t*>(records_all), log_z, log_prob, info, vinfo);

@@ -6,6 +6,11 @@
 
 namespace hmm {
 
+// Host side (hmm_abi.cu): raise `func`'s dynamic shared-memory limit to at least `smem` bytes on the
+// CURRENT device.  The attribute is per device, so the record of what was set is keyed by (device,
+// kernel) and guarded by a mutex: safe for concurrent first calls and for several GPUs in one process.
+cudaError_t ensure_smem_optin(const void* func, size_t smem);
+
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 
@@ -109,25 +114,37 @@ __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long
     return v;
 }
 
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Longest legitimate wait at a grid barrier is a few milliseconds (the slowest CTA's pass); a wait
+// beyond this bound means the counter can never reach G (a workspace left dirty by an aborted launch,
+// or CTAs that are not co-resident) and the kernel traps instead of hanging the device.
+constexpr unsigned long long kBarrierTimeoutNs = 4000000000ull;  // 4 s
+
 // Arrive-and-wait among the G CTAs of a sequence: every CTA adds 1 (release) and thread 0 spins
 // (acquire) until the counter reaches G.  The counters are reset to 0 by the last CTA of the launch
 // (after every CTA has passed every wait), so a zero-filled workspace stays valid across calls.
-// All G CTAs must be co-resident (cooperative launch).
+// All G CTAs must be co-resident (cooperative launch).  The spin is bounded (kBarrierTimeoutNs):
+// on timeout the launch traps (cudaErrorLaunchFailure on the stream, sticky for the context; the
+// caller must then re-zero the workspace, hmmscan.h "Errors").
 __device__ __forceinline__ void group_arrive_wait(unsigned long long* counter, uint32_t G) {
     __syncthreads();
     if (threadIdx.x == 0 && G > 1) {
         __threadfence();
         asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(counter) : "memory");
-        while (ld_acquire_u64(counter) < (unsigned long long)G) {
+        if (ld_acquire_u64(counter) < (unsigned long long)G) {
+            const unsigned long long t0 = global_ns();
+            uint32_t spins = 0;
+            while (ld_acquire_u64(counter) < (unsigned long long)G) {
+                if ((++spins & 1023u) == 0u && global_ns() - t0 > kBarrierTimeoutNs) __trap();
+            }
         }
     }
     __syncthreads();
-}
-
-__device__ __forceinline__ unsigned long long global_ns() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
 }
 
 // ---------------------------------------------------------------- arithmetic helpers

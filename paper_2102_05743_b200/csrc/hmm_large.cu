@@ -1013,18 +1013,11 @@ template <int DP, int OP>
 static cudaError_t lg_launch(const LgParams& p, cudaStream_t s) {
     using C = LG<DP>;
     const size_t sm1 = (size_t)C::NLB * DP * DP * 4;
-    static size_t cfg1 = 0, cfg3 = 0;
-    if (cfg1 < sm1) {
-        cudaError_t e = cudaFuncSetAttribute(lg_leaf_kernel<DP, OP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
-        if (e != cudaSuccess) return e;
-        cfg1 = sm1;
-    }
+    if (cudaError_t e = ensure_smem_optin(reinterpret_cast<const void*>(lg_leaf_kernel<DP, OP>), sm1); e != cudaSuccess)
+        return e;
     const size_t sm3 = (size_t)(3 * C::NLB + 2) * DP * 4 + (size_t)C::NLB * DP + 64;
-    if (cfg3 < sm3) {
-        cudaError_t e = cudaFuncSetAttribute(lg_sweep_kernel<DP, OP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm3);
-        if (e != cudaSuccess) return e;
-        cfg3 = sm3;
-    }
+    if (cudaError_t e = ensure_smem_optin(reinterpret_cast<const void*>(lg_sweep_kernel<DP, OP>), sm3); e != cudaSuccess)
+        return e;
     const dim3 grid((unsigned)p.NB, (unsigned)p.B);
     if (OP == 0 && DP == 64 && p.tc) {
         cudaError_t e = launch_large_tc_leaf(p, p.lik, s);
@@ -1033,12 +1026,9 @@ static cudaError_t lg_launch(const LgParams& p, cudaStream_t s) {
     lg_leaf_kernel<DP, OP><<<grid, 256, sm1, s>>>(p);
     {
         const size_t smc = (size_t)6 * DP * DP * 4;
-        static size_t cfgc = 0;
-        if (cfgc < smc) {
-            cudaError_t e = cudaFuncSetAttribute(lg_carry_kernel<DP, OP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smc);
-            if (e != cudaSuccess) return e;
-            cfgc = smc;
-        }
+        if (cudaError_t e = ensure_smem_optin(reinterpret_cast<const void*>(lg_carry_kernel<DP, OP>), smc);
+            e != cudaSuccess)
+            return e;
         lg_carry_kernel<DP, OP><<<dim3((unsigned)p.B, 2), 64, smc, s>>>(p);
     }
     lg_sweep_kernel<DP, OP><<<grid, 256, sm3, s>>>(p);

@@ -286,12 +286,8 @@ cudaError_t launch_large_tc_leaf(const LgParams& p, float* lik, cudaStream_t s) 
     const unsigned g1 = (unsigned)((rows + 7) / 8 < 148 * 16 ? (rows + 7) / 8 : 148 * 16);
     lg_lik_kernel<<<g1, 256, 0, s>>>(p, lik);
     const size_t smem = 32768 + 2 * 65536;
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(lg_leaf_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    if (cudaError_t e = ensure_smem_optin(reinterpret_cast<const void*>(lg_leaf_tc_kernel), smem); e != cudaSuccess)
+        return e;
     const int64_t nleaves = p.B * p.NL;
     lg_leaf_tc_kernel<<<(unsigned)((nleaves + 3) / 4), 256, smem, s>>>(p, lik);
     return cudaGetLastError();

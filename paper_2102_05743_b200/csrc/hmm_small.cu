@@ -509,12 +509,7 @@ __global__ void __launch_bounds__(small_nt(D)) hmm_small_kernel(const KParams p)
 template <int D, int OP>
 static cudaError_t launch_t(unsigned G, unsigned B, size_t smem, bool coop, const KParams& kp, cudaStream_t stream) {
     auto kern = hmm_small_kernel<D, OP>;
-    static size_t configured = 0;  // benign race: idempotent attribute set
-    if (configured < smem) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        configured = smem;
-    }
+    if (cudaError_t e = ensure_smem_optin(reinterpret_cast<const void*>(kern), smem); e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg;
     memset(&cfg, 0, sizeof(cfg));
     cfg.gridDim = dim3(G, B, 1);

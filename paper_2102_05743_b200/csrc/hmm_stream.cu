@@ -1403,12 +1403,7 @@ template <int D, int OP>
 static cudaError_t launch_st(unsigned G, const SParams& sp, cudaStream_t stream) {
     auto kern = hmm_stream_kernel<D, OP>;
     const size_t smem = sp.L.total;
-    static size_t configured = 0;
-    if (configured < smem) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        configured = smem;
-    }
+    if (cudaError_t e = ensure_smem_optin(reinterpret_cast<const void*>(kern), smem); e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg;
     memset(&cfg, 0, sizeof(cfg));
     cfg.gridDim = dim3(G, 1, 1);

@@ -7,6 +7,8 @@ all-gathered (NCCL over NVLink on B200s; ~W*80 bytes at D=4), and every rank run
 pass with carries folded from the gathered aggregates in rank order.  log Z / log_prob are the
 fixed-order sums of per-rank partials (a second tiny all-gather), so every rank holds bitwise-identical
 scalars.  Viterbi adds one more tiny all-gather of the rank backpointer maps (D bytes + x*).
+This module holds no arithmetic of the method: partitioning, collectives and marshalling only; the
+scalar combination (rank-order sums, info codes) runs in the library (hmm_dist_pack / hmm_dist_combine).
 
 The compute is done by ``LibBackend`` (the C ABI of libhmmscan.so).  The orchestration takes the
 backend as a parameter so its host logic can be exercised on CPU with gloo (tests/test_dist_gloo.py).
@@ -60,14 +62,16 @@ class LibBackend:
         self._ws = {}
 
     def pack(self, rec, lzp, lpp, s_i1, s_i2, v_i1, v_i2):
-        """One rank's 8-double record for the second merged all-gather (hmm_dist_pack)."""
-        out = torch.empty(8, dtype=torch.float64, device=rec.device)
+        """One rank's 8-double scalar record (hmm_dist_pack); None inputs contribute zeros."""
+        dev = next(x for x in (rec, lzp, lpp, s_i1, s_i2, v_i1, v_i2) if x is not None).device
+        out = torch.empty(8, dtype=torch.float64, device=dev)
         _check(self.L.hmm_dist_pack(_ptr(rec), _ptr(lzp), _ptr(lpp), _ptr(s_i1), _ptr(s_i2), _ptr(v_i1), _ptr(v_i2),
                                     _ptr(out), _stream(None)), "hmm_dist_pack")
         return out
 
     def combine(self, g, world):
-        """Records in rank order, log Z, log_prob and the global info codes from the gathered records."""
+        """From the gathered records (hmm_dist_combine): the Viterbi rank records in rank order, log Z and
+        log_prob (sums of the partials in rank order) and the global info codes of both operations."""
         dev = g.device
         rec_all = torch.empty(16 * world, dtype=torch.uint8, device=dev)
         lz = torch.empty(1, dtype=torch.float64, device=dev)
@@ -166,54 +170,39 @@ def _all_gather(x: torch.Tensor, group=None) -> torch.Tensor:
     return torch.cat([q.view(-1) for q in parts]).to(x.device)
 
 
-def _combine_info(infos: torch.Tensor) -> torch.Tensor:
-    """Global info from per-rank codes: -1 if any rank saw a bad input, else the smallest positive."""
-    bad = (infos == -1).any()
-    pos = torch.where(infos > 0, infos, torch.full_like(infos, torch.iinfo(torch.int32).max))
-    m = pos.min()
-    first = torch.where(m == torch.iinfo(torch.int32).max, torch.zeros_like(m), m)
-    return torch.where(bad, torch.full_like(first, -1), first).view(1)
-
-
 def smooth_dist(log_pi, log_A, log_lik_local, t_base: int, group=None, backend=None):
     """Parallel smoother over a T-partitioned sequence.  Returns (filtered, smoothed, log_z [1], info [1])
-    for the local slice; log_z and info are global and identical on every rank."""
+    for the local slice; log_z and info are global and identical on every rank (rank-order sums and
+    info combination done by the library's hmm_dist_combine)."""
     be = _backend(backend)
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     agg, info1 = be.smooth_reduce(log_pi, log_A, log_lik_local, t_base)
     agg_all = _all_gather(agg, group)                       # the method's one exchange step
     filt, sm, lzp, info2 = be.smooth_finish(log_pi, log_A, log_lik_local, t_base, agg_all, rank, world)
-    parts = _all_gather(torch.cat([lzp, torch.stack([info1.double().view(()), info2.double().view(())])]), group)
-    parts = parts.view(world, 3)
-    log_z = torch.zeros(1, dtype=torch.float64, device=parts.device)
-    for r in range(world):  # fixed rank order
-        log_z += parts[r, 0]
-    info = _combine_info(parts[:, 1:].reshape(-1).to(torch.int32))
+    g = _all_gather(be.pack(None, lzp, None, info1, info2, None, None), group)
+    _, log_z, _, info, _ = be.combine(g, world)
     return filt, sm, log_z, info
 
 
 def viterbi_dist(log_pi, log_A, log_lik_local, t_base: int, group=None, backend=None):
     """Parallel MAP path over a T-partitioned sequence.  Returns (path of the local slice, log_prob [1],
-    info [1]); log_prob and info are global."""
+    info [1]); log_prob and info are global.  Two all-gathers: the rank aggregates, then the rank records
+    (backpointer map + x*) together with the log_prob partials and info codes."""
     be = _backend(backend)
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     agg, info1 = be.viterbi_reduce(log_pi, log_A, log_lik_local, t_base)
     agg_all = _all_gather(agg, group)
     rec, lpp, info2 = be.viterbi_forward(log_pi, log_A, log_lik_local, t_base, agg_all, rank, world)
-    rec_all = _all_gather(rec, group)                      # rank backpointer maps + x*
-    path, info3 = be.viterbi_finish(log_pi, log_A, log_lik_local, t_base, rec_all, rank, world)
-    parts = _all_gather(torch.cat([lpp, torch.stack([info1.double().view(()), info2.double().view(()),
-                                                     info3.double().view(())])]), group).view(world, 4)
-    log_prob = torch.zeros(1, dtype=torch.float64, device=parts.device)
-    for r in range(world):
-        log_prob += parts[r, 0]
-    info = _combine_info(parts[:, 1:].reshape(-1).to(torch.int32))
+    g = _all_gather(be.pack(rec, None, lpp, None, None, info1, info2), group)
+    rec_all, _, log_prob, _, info = be.combine(g, world)
+    # finish only backtracks: its info is always 0 (errors are reported by reduce / forward, hmmscan.h)
+    path, _ = be.viterbi_finish(log_pi, log_A, log_lik_local, t_base, rec_all, rank, world)
     return path, log_prob, info
 
 
 def smooth_viterbi_dist(log_pi, log_A, log_lik_local, t_base: int, group=None, backend=None):
     """Smoother and MAP path of the same T-partitioned sequence with the collectives of both merged:
-    two all-gathers per call instead of five (the rank aggregates of both semirings together; then the
+    two all-gathers per call instead of four (the rank aggregates of both semirings together; then the
     Viterbi rank records together with every scalar partial).  Returns
     (filtered, smoothed, log_z [1], info [1], path, log_prob [1], vinfo [1]) for the local slice."""
     be = _backend(backend)
@@ -226,23 +215,7 @@ def smooth_viterbi_dist(log_pi, log_A, log_lik_local, t_base: int, group=None, b
     v_all = both[:, na:].contiguous().view(-1)
     filt, sm, lzp, s_i2 = be.smooth_finish(log_pi, log_A, log_lik_local, t_base, s_all, rank, world)
     rec, lpp, v_i2 = be.viterbi_forward(log_pi, log_A, log_lik_local, t_base, v_all, rank, world)
-    if hasattr(be, "pack") and rec.is_cuda:
-        # two library launches instead of the tensor ops below (same values, bit for bit)
-        g = _all_gather(be.pack(rec, lzp, lpp, s_i1, s_i2, v_i1, v_i2), group)
-        rec_all, log_z, log_prob, info, vinfo = be.combine(g, world)
-        path, _ = be.viterbi_finish(log_pi, log_A, log_lik_local, t_base, rec_all, rank, world)
-        return filt, sm, log_z, info, path, log_prob, vinfo
-    sc = torch.stack([lzp.view(()), lpp.view(()), s_i1.double().view(()), s_i2.double().view(()),
-                      v_i1.double().view(()), v_i2.double().view(())])
-    packed = torch.cat([rec.view(torch.float64).view(-1).to(sc.device), sc])  # 2 + 6 float64 per rank
-    g = _all_gather(packed, group).view(world, 8)
-    rec_all = g[:, :2].contiguous().view(-1).view(torch.uint8)
+    g = _all_gather(be.pack(rec, lzp, lpp, s_i1, s_i2, v_i1, v_i2), group)
+    rec_all, log_z, log_prob, info, vinfo = be.combine(g, world)
     path, _ = be.viterbi_finish(log_pi, log_A, log_lik_local, t_base, rec_all, rank, world)
-    log_z = torch.zeros(1, dtype=torch.float64, device=g.device)
-    log_prob = torch.zeros(1, dtype=torch.float64, device=g.device)
-    for r in range(world):  # fixed rank order
-        log_z += g[r, 2]
-        log_prob += g[r, 3]
-    info = _combine_info(g[:, 4:6].reshape(-1).to(torch.int32))
-    vinfo = _combine_info(g[:, 6:8].reshape(-1).to(torch.int32))
     return filt, sm, log_z, info, path, log_prob, vinfo

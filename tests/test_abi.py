@@ -49,7 +49,9 @@ def test_invalid_arguments_rejected_on_host(L):
 
 def test_workspace_size_invalid(L):
     assert L.hmm_workspace_size(0, 0, 10, 1) == 0
-    assert L.hmm_workspace_size(2, 4, 10, 1) == 0
+    assert L.hmm_workspace_size(3, 4, 10, 1) == 0   # no such op
+    assert L.hmm_workspace_size(2, 9, 10, 1) == 0   # statistics: D <= 8
+    assert L.hmm_workspace_size(2, 4, 10, 2) == 0   # statistics: one sequence
     assert L.hmm_workspace_size(0, 4, 0, 1) == 0
 
 

@@ -92,6 +92,36 @@ class NumpyBackend:
         rec[8:12] = np.frombuffer(np.int32(xs).tobytes(), np.uint8)
         return torch.from_numpy(rec), torch.tensor([lp_part], dtype=torch.float64), torch.zeros(1, dtype=torch.int32)
 
+    def pack(self, rec, lzp, lpp, s_i1, s_i2, v_i1, v_i2):
+        """hmm_dist_pack's record layout: 2 doubles of Viterbi record, log Z / log_prob partials, 4 codes."""
+        out = np.zeros(8)
+        if rec is not None:
+            out[:2] = rec.numpy().view(np.float64)
+        for k, x in ((2, lzp), (3, lpp), (4, s_i1), (5, s_i2), (6, v_i1), (7, v_i2)):
+            if x is not None:
+                out[k] = float(x.reshape(-1)[0])
+        return torch.from_numpy(out)
+
+    def combine(self, g, world):
+        """hmm_dist_combine: records in rank order, partial sums in rank order from 0.0, info codes."""
+        G = g.numpy().reshape(world, 8)
+        rec_all = torch.from_numpy(np.ascontiguousarray(G[:, :2]).view(np.uint8).reshape(-1).copy())
+        lz = 0.0
+        lp = 0.0
+        for r in range(world):
+            lz += G[r, 2]
+            lp += G[r, 3]
+
+        def codes(c0):
+            cs = [int(c) for c in G[:, c0:c0 + 2].reshape(-1)]
+            if -1 in cs:
+                return -1
+            pos = [c for c in cs if c > 0]
+            return min(pos) if pos else 0
+        i32 = lambda v: torch.tensor([v], dtype=torch.int32)
+        return (rec_all, torch.tensor([lz], dtype=torch.float64), torch.tensor([lp], dtype=torch.float64),
+                i32(codes(4)), i32(codes(6)))
+
     def viterbi_finish(self, lp, la, ll, t_base, rec_all, rank, world):
         recs = rec_all.numpy().reshape(world, 16)
         x = int(np.frombuffer(recs[world - 1, 8:12].tobytes(), np.int32)[0])
@@ -164,11 +194,3 @@ def test_partition_properties():
             for (a, n), (b, _) in zip(parts, parts[1:]):
                 assert a + n == b
             assert all(n >= 1 for _, n in parts)
-
-
-def test_combine_info():
-    from paper_2102_05743_b200.dist import _combine_info
-    f = lambda xs: int(_combine_info(torch.tensor(xs, dtype=torch.int32))[0])
-    assert f([0, 0, 0]) == 0
-    assert f([0, 17, 5]) == 5
-    assert f([0, -1, 5]) == -1

@@ -109,7 +109,7 @@ def test_dist_info_global_step():
 def test_dist_pack_combine(world, codes):
     """hmm_dist_pack / hmm_dist_combine against the tensor-op combination they replace: records in rank
     order, log Z and log_prob summed in rank order from 0.0 (bit for bit), global info codes."""
-    from paper_2102_05743_b200.dist import LibBackend, _combine_info
+    from paper_2102_05743_b200.dist import LibBackend
     be = LibBackend()
     dev = torch.device("cuda")
     g = torch.Generator().manual_seed(world * 31 + codes[1])
@@ -131,7 +131,54 @@ def test_dist_pack_combine(world, codes):
         ez += lzs[r]
         ep += lps[r]
     assert float(lz[0]) == float(ez[0]) and float(lp[0]) == float(ep[0])
-    s_codes = torch.tensor([c for cs in infos for c in cs[:2]], dtype=torch.int32)
-    v_codes = torch.tensor([c for cs in infos for c in cs[2:]], dtype=torch.int32)
-    assert int(info[0]) == int(_combine_info(s_codes)[0])
-    assert int(vinfo[0]) == int(_combine_info(v_codes)[0])
+    s_codes = [c for cs in infos for c in cs[:2]]
+    v_codes = [c for cs in infos for c in cs[2:]]
+    assert int(info[0]) == _expected_info(s_codes)
+    assert int(vinfo[0]) == _expected_info(v_codes)
+
+
+def _expected_info(codes):
+    """hmmscan.h: -1 if any rank reported -1, else the smallest positive code, else 0."""
+    if -1 in codes:
+        return -1
+    pos = [c for c in codes if c > 0]
+    return min(pos) if pos else 0
+
+
+def test_dist_pack_null_inputs_are_zero():
+    """hmm_dist_pack: NULL inputs contribute zeros (the smoother-only and Viterbi-only steps)."""
+    from paper_2102_05743_b200.dist import LibBackend
+    be = LibBackend()
+    dev = torch.device("cuda")
+    lz = torch.tensor([-123.5], dtype=torch.float64, device=dev)
+    i1 = torch.tensor([7], dtype=torch.int32, device=dev)
+    row = be.pack(None, lz, None, i1, None, None, None)
+    torch.cuda.synchronize()
+    assert row.cpu().tolist() == [0.0, 0.0, -123.5, 0.0, 7.0, 0.0, 0.0, 0.0]
+    rec_all, z, p, info, vinfo = be.combine(torch.cat([row, row]), 2)
+    assert float(z[0]) == -247.0 and float(p[0]) == 0.0 and int(info[0]) == 7 and int(vinfo[0]) == 0
+
+
+def test_dist_misaligned_output_rejected():
+    """Split phase: all phases of a rank run the kernel chosen from log_lik's alignment, so a finish
+    output that is not 16-B aligned is an error instead of a silent switch of kernel (hmmscan.h)."""
+    import ctypes
+    from paper_2102_05743_b200 import _ptr, _stream
+    from paper_2102_05743_b200.dist import LibBackend
+    be = LibBackend()
+    wl = W.ge(10_000, seed=3)
+    dev = torch.device("cuda")
+    lp, la = torch.from_numpy(wl.log_pi).to(dev), torch.from_numpy(wl.log_A).to(dev)
+    ll = torch.from_numpy(wl.log_lik).to(dev)
+    agg, _ = be.smooth_reduce(lp, la, ll, 0)
+    ws = be.ws(0, 4, wl.T, dev)
+    big = torch.empty(wl.T * 4 + 1, dtype=torch.float32, device=dev)
+    lzp = torch.empty(1, dtype=torch.float64, device=dev)
+    info = torch.empty(1, dtype=torch.int32, device=dev)
+    st = be.L.hmm_smooth_dist_finish(4, wl.T, 0, _ptr(lp), _ptr(la), _ptr(ll), _ptr(agg), 0, 1,
+                                     ctypes.c_void_p(big.data_ptr() + 4), _ptr(big), _ptr(lzp), _ptr(info),
+                                     _ptr(ws), ws.numel(), _stream(None))
+    assert st == 1
+    f, s, z, i = be.smooth_finish(lp, la, ll, 0, agg, 0, 1)  # the workspace is still consistent
+    torch.cuda.synchronize()
+    assert int(i[0]) == 0

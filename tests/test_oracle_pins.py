@@ -366,3 +366,14 @@ def test_symbol_workload_matches_loglik_workload():
     np.testing.assert_array_equal(oracle.symbols_loglik(ws.log_B, ws.y), wl.log_lik)
     d = W.discrete(5, 7, 1000, 2)
     assert d.y.max() < 7 and np.allclose(np.exp(d.log_B.astype(np.float64)).sum(1), 1.0, atol=1e-6)
+
+
+def test_golden_fixtures_regenerate_from_enumeration():
+    """tests/golden/ge_T5.json and spec_D2_T4.json are what tools/make_golden.py computes with
+    oracle/brute.py alone (Eqs. 1-3 by enumeration): no stored value is hand-copied."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "make_golden", os.path.join(os.path.dirname(os.path.dirname(__file__)), "tools", "make_golden.py"))
+    mg = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mg)
+    assert mg.check(mg.compute()) == []
