@@ -48,6 +48,9 @@ def _L():
         _lib.oracle_max_marginals.argtypes = [i32, i64, p, p, p, p, p]
         _lib.oracle_joint_weight.argtypes = [i32, i64, p, p, p, p]
         _lib.oracle_joint_weight.restype = ctypes.c_double
+        _lib.oracle_max_marginal_gap.argtypes = [i32, i64, p, p, p, p]
+        _lib.oracle_joint_weight_diff.argtypes = [i32, i64, p, p, p, p, p]
+        _lib.oracle_joint_weight_diff.restype = ctypes.c_double
         _lib.oracle_smooth_batched.argtypes = [i32, i64, i64, p, p, p, p, p, p, p, p, i32]
         _lib.oracle_viterbi_batched.argtypes = [i32, i64, i64, p, p, p, p, p, p, i32]
     return _lib
@@ -131,6 +134,25 @@ def max_marginals(log_pi, log_A, log_lik):
     score = np.empty((T, D)); gap = np.empty(T)
     _L().oracle_max_marginals(D, T, _p(log_pi), _p(log_A), _p(log_lik), _p(score), _p(gap))
     return score, gap
+
+
+def max_marginal_gap(log_pi, log_A, log_lik):
+    """gap [T] float32 = best - second best max-marginal score at every step (as max_marginals' gap,
+    bitwise after rounding to float32) in O(T) memory: usable at T = 1e8."""
+    log_pi, log_A, log_lik = _f32(log_pi), _f32(log_A), _f32(log_lik)
+    T, D = log_lik.shape
+    gap = np.empty(T, np.float32)
+    if _L().oracle_max_marginal_gap(D, T, _p(log_pi), _p(log_A), _p(log_lik), _p(gap)) != 0:
+        raise MemoryError("oracle_max_marginal_gap")
+    return gap
+
+
+def joint_weight_diff(log_pi, log_A, log_lik, path_a, path_b) -> float:
+    """log w(path_a) - log w(path_b) (Eq. 6), summed over the differing terms only."""
+    log_pi, log_A, log_lik = _f32(log_pi), _f32(log_A), _f32(log_lik)
+    a = np.ascontiguousarray(path_a, np.int32); b = np.ascontiguousarray(path_b, np.int32)
+    T, D = log_lik.shape
+    return _L().oracle_joint_weight_diff(D, T, _p(log_pi), _p(log_A), _p(log_lik), _p(a), _p(b))
 
 
 def joint_weight(log_pi, log_A, log_lik, path) -> float:

@@ -19,6 +19,8 @@
  *                     their sum is the max-marginal of Eq. 3; used for gap / tie analysis
  *                     and the Theorem 4 invariant.  Diagnostics, not outputs.
  *   oracle_joint_weight — log of psi_1(x_1) prod psi_t(x_{t-1},x_t) (Eq. 6).
+ *   oracle_max_marginal_gap / oracle_joint_weight_diff — the same quantities in O(T) memory / without
+ *                     cancellation, for checking full-size (T = 1e8) paths.
  *
  * Conventions: 0-based t; log_A[i*D+j] = log p(x_t=j | x_{t-1}=i);
  * log_lik[t*D+d] = log p(y_t | x_t=d); inputs are fp32, promoted to fp64 on read.
@@ -365,6 +367,101 @@ int oracle_max_marginals(int D, int64_t T, const float* log_pi, const float* log
     }
     free(f); free(b);
     return 0;
+}
+
+/* The per-step max-marginal gap of oracle_max_marginals (Lemma 3; Eq. 3) in O(T) memory
+ * for full-size checks (T = 1e8): gap32[t] = (float)(best - second best of fwd[t] + bwd[t]).  Same
+ * recursions, operand order and tie loop as oracle_max_marginals, so the values are bitwise the ones it
+ * computes; only the storage differs: the forward values are kept at every K-th step (checkpoints) and
+ * recomputed one block at a time while the backward recursion runs right to left.                       */
+int oracle_max_marginal_gap(int D, int64_t T, const float* log_pi, const float* log_A, const float* log_lik,
+                            float* gap32) {
+    const int64_t K = 4096;
+    const int64_t nb = (T + K - 1) / K;
+    double* ck = (double*)malloc(sizeof(double) * (size_t)nb * D); /* fwd at t = b*K */
+    double* fb = (double*)malloc(sizeof(double) * (size_t)K * D);  /* fwd over one block */
+    double *f = (double*)malloc(sizeof(double) * D), *fn = (double*)malloc(sizeof(double) * D);
+    double *b = (double*)malloc(sizeof(double) * D), *bn = (double*)malloc(sizeof(double) * D);
+    if (!ck || !fb || !f || !fn || !b || !bn) { free(ck); free(fb); free(f); free(fn); free(b); free(bn); return 1; }
+    /* forward: psi~f (Lemma 3), checkpointed */
+    for (int j = 0; j < D; j++) f[j] = (double)log_pi[j] + (double)log_lik[j];
+    for (int64_t t = 0; t < T; t++) {
+        if (t > 0) {
+            for (int j = 0; j < D; j++) {
+                double best = -INFINITY;
+                for (int i = 0; i < D; i++) {
+                    double s = f[i] + (double)log_A[i * D + j];
+                    if (s > best) best = s;
+                }
+                fn[j] = best + (double)log_lik[t * D + j];
+            }
+            memcpy(f, fn, sizeof(double) * D);
+        }
+        if (t % K == 0) memcpy(ck + (size_t)(t / K) * D, f, sizeof(double) * D);
+    }
+    /* backward: psi~b, one block at a time from the right, with the block's fwd recomputed */
+    for (int i = 0; i < D; i++) b[i] = 0.0;
+    for (int64_t blk = nb - 1; blk >= 0; blk--) {
+        const int64_t t0 = blk * K, t1 = (t0 + K < T) ? t0 + K : T;
+        memcpy(fb, ck + (size_t)blk * D, sizeof(double) * D);
+        for (int64_t t = t0 + 1; t < t1; t++) {
+            const double* fp = fb + (size_t)(t - 1 - t0) * D;
+            for (int j = 0; j < D; j++) {
+                double best = -INFINITY;
+                for (int i = 0; i < D; i++) {
+                    double s = fp[i] + (double)log_A[i * D + j];
+                    if (s > best) best = s;
+                }
+                fb[(size_t)(t - t0) * D + j] = best + (double)log_lik[t * D + j];
+            }
+        }
+        for (int64_t t = t1 - 1; t >= t0; t--) {
+            if (t < T - 1) {
+                for (int i = 0; i < D; i++) {
+                    double best = -INFINITY;
+                    for (int j = 0; j < D; j++) {
+                        double s = (double)log_A[i * D + j] + (double)log_lik[(t + 1) * D + j] + b[j];
+                        if (s > best) best = s;
+                    }
+                    bn[i] = best;
+                }
+                memcpy(b, bn, sizeof(double) * D);
+            }
+            double b1 = -INFINITY, b2 = -INFINITY;
+            for (int x = 0; x < D; x++) {
+                double s = fb[(size_t)(t - t0) * D + x] + b[x];
+                if (s > b1) { b2 = b1; b1 = s; } else if (s > b2) b2 = s;
+            }
+            gap32[t] = (float)((D == 1) ? INFINITY : b1 - b2);
+        }
+    }
+    free(ck); free(fb); free(f); free(fn); free(b); free(bn);
+    return 0;
+}
+
+/* Difference of the joint log-weights (Eq. 6) of two state sequences a and b,
+ * log w(a) - log w(b), summed only over the terms that differ (the prior/evidence term at t and the
+ * transition term into t, wherever a or its predecessor differs from b).  Equal to
+ * oracle_joint_weight(a) - oracle_joint_weight(b) but without cancelling two ~1e7-nat sums, so a loss of
+ * 1e-6 nats is resolvable at T = 1e8.                                                                    */
+double oracle_joint_weight_diff(int D, int64_t T, const float* log_pi, const float* log_A, const float* log_lik,
+                                const int32_t* a, const int32_t* b) {
+    double d = 0.0;
+    for (int64_t t = 0; t < T; t++) {
+        const int diff_here = a[t] != b[t];
+        const int diff_prev = t > 0 && a[t - 1] != b[t - 1];
+        if (!diff_here && !diff_prev) continue;
+        double wa, wb;
+        if (t == 0) {
+            wa = (double)log_pi[a[0]] + (double)log_lik[a[0]];
+            wb = (double)log_pi[b[0]] + (double)log_lik[b[0]];
+        } else {
+            wa = (double)log_A[a[t - 1] * D + a[t]] + (double)log_lik[t * D + a[t]];
+            wb = (double)log_A[b[t - 1] * D + b[t]] + (double)log_lik[t * D + b[t]];
+        }
+        d += wa - wb;
+    }
+    return d;
 }
 
 /* log psi_1(x_1) + sum_t log psi_t(x_{t-1}, x_t)  (Eq. 6; Eq. 16 joint). */

@@ -7,6 +7,9 @@ the MAP joint log-probability (several MAP paths are correct, reading 
 """
 from __future__ import annotations
 
+import json
+import os
+
 import numpy as np
 import torch
 
@@ -16,6 +19,15 @@ import paper_2102_05743_b200 as H
 TOL_MARG = 1e-5
 TOL_REL = 1e-6
 TAU = 1e-3
+
+
+def record(name: str, **values):
+    """Appends one JSON line of measured errors to $HMM_PARITY_LOG (if set): the numbers DESIGN.md quotes."""
+    path = os.environ.get("HMM_PARITY_LOG")
+    if path:
+        with open(path, "a") as f:
+            f.write(json.dumps({"test": name, **{k: (float(v) if isinstance(v, (np.floating, float)) else v)
+                                                 for k, v in values.items()}}) + "\n")
 
 
 def to_dev(wl):

@@ -377,3 +377,30 @@ def test_golden_fixtures_regenerate_from_enumeration():
     mg = importlib.util.module_from_spec(spec)
     spec.loader.exec_module(mg)
     assert mg.check(mg.compute()) == []
+
+
+@pytest.mark.parametrize("D,T,seed", [(4, 100_000, 1), (3, 9_000, 2), (1, 5000, 3), (8, 4097, 4), (2, 1, 5)])
+def test_max_marginal_gap_o_t_memory_is_bitwise_the_full_routine(D, T, seed):
+    """oracle.max_marginal_gap (checkpointed, O(T) memory, used at T = 1e8) returns exactly the gap of
+    oracle.max_marginals (pinned to enumeration below) rounded to float32, block boundaries included."""
+    wl = W.ge(T, seed, jitter=0.1) if D == 4 else W.random_potentials(D, T, seed)
+    _, gap = oracle.max_marginals(wl.log_pi, wl.log_A, wl.log_lik)
+    g32 = oracle.max_marginal_gap(wl.log_pi, wl.log_A, wl.log_lik)
+    assert np.array_equal(g32, gap.astype(np.float32))
+
+
+def test_joint_weight_diff_matches_difference_of_weights():
+    """Eq. 6 term-wise difference == difference of the full joint weights (small T, no cancellation issue)."""
+    rng = np.random.default_rng(7)
+    for k in range(20):
+        D, T = int(rng.integers(2, 6)), int(rng.integers(1, 300))
+        wl = W.random_potentials(D, T, 100 + k)
+        a = rng.integers(0, D, T).astype(np.int32)
+        b = a.copy()
+        flip = rng.random(T) < 0.2
+        b[flip] = rng.integers(0, D, int(flip.sum()))
+        d = oracle.joint_weight_diff(wl.log_pi, wl.log_A, wl.log_lik, a, b)
+        ref = oracle.joint_weight(wl.log_pi, wl.log_A, wl.log_lik, a) - oracle.joint_weight(wl.log_pi, wl.log_A,
+                                                                                             wl.log_lik, b)
+        assert abs(d - ref) <= 1e-9 * max(1.0, abs(ref))
+        assert oracle.joint_weight_diff(wl.log_pi, wl.log_A, wl.log_lik, a, a) == 0.0
