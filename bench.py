@@ -40,7 +40,6 @@ L2_FLUSH_BYTES = 512 << 20
 # Algorithmic work per time step (DESIGN.md §"Roofline accounting").
 SMOOTH_BYTES_PER_STEP = lambda D: 12 * D      # read log_lik (4D) + write filtered + smoothed (8D)
 VITERBI_BYTES_PER_STEP = lambda D: 4 * D + 4  # read log_lik + write int32 path
-VITERBI_ALU_PER_STEP = lambda D: D ** 3 + D * D * ((D - 1 + 1) // 2) + 2 * D * D  # leaf max-plus + sweep
 
 
 def load_peaks():
@@ -48,8 +47,9 @@ def load_peaks():
     if os.path.exists(p):
         with open(p) as f:
             d = json.load(f)
-        return dict(hbm=float(d["hbm_gbs"]), sm_mhz=float(d.get("sm_max_mhz", 1965.0)), src="measured")
-    return dict(hbm=6650.0, sm_mhz=1965.0, src="fallback")
+        return dict(hbm=float(d["hbm_gbs"]), sm_mhz=float(d.get("sm_max_mhz", 1965.0)), src="measured",
+                    bf16_tflops=d.get("bf16_tflops"))
+    return dict(hbm=6650.0, sm_mhz=1965.0, src="fallback", bf16_tflops=None)
 
 
 def ncu_traffic():
@@ -126,15 +126,34 @@ def make_workload(args, rank):
     raise SystemExit(f"unknown workload {args.workload}")
 
 
+def host_info():
+    """nproc + the CPU model (lscpu), for the cpu_baseline record."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
+
+
 def cpu_oracle_rate(wl, budget_s):
-    """The fp64 oracle as it stands, on bounded samples of the workload (1 core: it is sequential)."""
+    """The fp64 oracle as it stands, on bounded samples of the workload (1 core: it is sequential).
+
+    The sample is 8 windows of n steps spread evenly over the sequence (window k starts at k*T/8), each
+    run as its own sequence (smoother + Viterbi), cycled until the budget is spent."""
     import oracle
     T = wl.T
     n = min(T, 200_000)
-    ll = np.ascontiguousarray(wl.log_lik[:n])
+    nw = 8 if T >= 8 * n else 1
+    wins = [np.ascontiguousarray(wl.log_lik[(k * T) // nw:(k * T) // nw + n]) for k in range(nw)]
     done, t0 = 0, time.perf_counter()
     reps = 0
     while True:
+        ll = wins[reps % nw]
         oracle.smooth(wl.log_pi, wl.log_A, ll)
         oracle.viterbi(wl.log_pi, wl.log_A, ll)
         done += n
@@ -142,7 +161,99 @@ def cpu_oracle_rate(wl, budget_s):
         el = time.perf_counter() - t0
         if el >= budget_s:
             break
-    return done / el, f"first {n} steps of the workload, smoother+viterbi, {reps} reps, {el:.1f}s", 1
+    return done / el, (f"{nw} windows of {n} steps spread over the T={T:g} workload (window k at k*T/{nw}), "
+                       f"smoother+viterbi, {reps} window runs, {el:.1f}s"), 1
+
+
+def time_ops(H, wl, dev, steps, warmup, flush):
+    """Device time (ms, mean over `steps`, CUDA events on the launching stream, L2 flushed between steps
+    outside the events) of hmm_smooth and hmm_viterbi on one workload, inputs resident in HBM."""
+    import torch
+    lp = torch.from_numpy(wl.log_pi).to(dev)
+    la = torch.from_numpy(wl.log_A).to(dev)
+    ll = torch.from_numpy(wl.log_lik).to(dev)
+    batched = ll.dim() == 3
+    B = ll.shape[0] if batched else 1
+    T, D = ll.shape[-2], ll.shape[-1]
+    out_s = (torch.empty_like(ll), torch.empty_like(ll), torch.empty(B, dtype=torch.float64, device=dev),
+             torch.empty(B, dtype=torch.int32, device=dev))
+    out_v = (torch.empty(ll.shape[:-1], dtype=torch.int32, device=dev),
+             torch.empty(B, dtype=torch.float64, device=dev), torch.empty(B, dtype=torch.int32, device=dev))
+    ws_s = H.workspace(H.HMM_OP_SMOOTH, D, T, B, dev)
+    ws_v = H.workspace(H.HMM_OP_VITERBI, D, T, B, dev)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(warmup):
+        flush()
+        H.smooth(lp, la, ll, out=out_s, ws=ws_s)
+        H.viterbi(lp, la, ll, out=out_v, ws=ws_v)
+    torch.cuda.synchronize()
+    assert int(out_s[3].abs().max().item()) == 0 and int(out_v[2].abs().max().item()) == 0
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
+    for k in range(steps):
+        flush()
+        ev[k][0].record(stream)
+        H.smooth(lp, la, ll, out=out_s, ws=ws_s)
+        ev[k][1].record(stream)
+        H.viterbi(lp, la, ll, out=out_v, ws=ws_v)
+        ev[k][2].record(stream)
+    torch.cuda.synchronize()
+    ms_s = sum(e[0].elapsed_time(e[1]) for e in ev) / steps
+    ms_v = sum(e[1].elapsed_time(e[2]) for e in ev) / steps
+    del out_s, out_v, ll
+    return ms_s, ms_v, B, T, D
+
+
+def config_lines(H, dev, steps, warmup, flush, peaks):
+    """The rest of BASELINE's metric ("at D=4 and D=64"): configs[1] (GE D=4, T=1e6), configs[2] (dense
+    D=64, T=1e5) and configs[3] (B=1024, D=16, T=4096), each smoother and Viterbi device-timed with a
+    roofline: HBM for the D=4 smoother, the FP32 pipe (effective algorithmic flops) and the
+    tensor pipe for the D>=16 sum-product, the derived FADD/FMNMX3 issue ceiling for max-plus."""
+    import workloads as W
+    clk = peaks["sm_mhz"] * 1e6
+    fp32_peak = 2 * 148 * 128 * clk / 1e12                         # TFLOP/s, FFMA
+    tf32_peak = peaks["bf16_tflops"] * 0.5 if peaks.get("bf16_tflops") else None  # guide: TF32 = BF16 / 2
+    out = {}
+    for key, wl, desc in (
+            ("configs[1]", W.ge(1_000_000, seed=1), "Gilbert-Elliott D=4, T=1e6, one sequence"),
+            ("configs[2]", W.dense(64, 100_000, seed=3), "dense Dirichlet(1) D=64, T=1e5, Gaussian emissions"),
+            ("configs[3]", W.dense_batch(1024, 16, 4096), "B=1024 sequences, D=16, T=4096, shared dense model")):
+        ms_s, ms_v, B, T, D = time_ops(H, wl, dev, steps, warmup, flush)
+        n = B * T
+        rec = {"workload": desc, "D": D, "T": T, "B": B,
+               "smoother_ms": ms_s, "viterbi_ms": ms_v,
+               "smoother_steps_per_s": n / (ms_s * 1e-3), "viterbi_steps_per_s": n / (ms_v * 1e-3),
+               "value": n / ((ms_s + ms_v) * 1e-3)}
+        vops = D ** 3 + D * D * (D - 1)  # max-plus: D^3 adds + D^2 (D-1) 2-input max comparisons per step
+        # issue ceiling (DESIGN.md §7): adds as FADD2 (2 lane-adds per lane-issue) and maxima as FMNMX3
+        # (2 comparisons per lane-issue) share 128 lane-issues/clk/SM -> clk per step per SM:
+        v_clk = (D ** 3 / 2 + D * D * (D - 1) / 2) / 128
+        v_ceiling = 148 * clk / v_clk  # steps/s
+        rec["viterbi_roofline"] = {"bound": "alu", "achieved": n / (ms_v * 1e-3), "peak": v_ceiling,
+                                   "unit": "time-steps/s", "frac": n / (ms_v * 1e-3) / v_ceiling,
+                                   "ops_per_step": vops, "ceiling": "FADD2 + FMNMX3 issue, 128 lane-issues/clk/SM"}
+        if D <= 8:  # the algorithmic 20 B/step at the HBM peak is the larger floor at small D
+            ach = VITERBI_BYTES_PER_STEP(D) * n / (ms_v * 1e-3) / 1e9
+            rec["viterbi_roofline"] = {"bound": "hbm", "achieved": ach, "peak": peaks["hbm"], "unit": "GB/s",
+                                       "frac": ach / peaks["hbm"], "bytes_per_step": VITERBI_BYTES_PER_STEP(D),
+                                       "alu_frac": n / (ms_v * 1e-3) / v_ceiling}
+        if D <= 8:
+            ach = SMOOTH_BYTES_PER_STEP(D) * n / (ms_s * 1e-3) / 1e9
+            rec["smoother_roofline"] = {"bound": "hbm", "achieved": ach, "peak": peaks["hbm"], "unit": "GB/s",
+                                        "frac": ach / peaks["hbm"], "bytes_per_step": SMOOTH_BYTES_PER_STEP(D)}
+        else:
+            flop = 2 * D ** 3 + 4 * D * D  # one semiring product per step + two D^2 sweeps
+            ach = flop * n / (ms_s * 1e-3) / 1e12
+            r = {"bound": "tensor" if D >= 33 else "fp32", "achieved": ach, "unit": "TFLOP/s",
+                 "flop_per_step": flop, "fp32_peak": fp32_peak, "frac_fp32": ach / fp32_peak}
+            if D >= 33 and tf32_peak:
+                # the contraction runs as TF32x3 (3 MMAs per product): pipe-level achieved = 3x
+                r.update({"peak": tf32_peak, "frac": ach / tf32_peak, "tensor_pipe_frac": 3 * ach / tf32_peak,
+                          "peak_source": "measured bf16 x 0.5 (TF32/BF16 nominal ratio)"})
+            else:
+                r.update({"peak": fp32_peak, "frac": ach / fp32_peak})
+            rec["smoother_roofline"] = r
+        out[key] = rec
+    return out
 
 
 def run_reference(args):
@@ -167,7 +278,7 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": desc, "D": wl.D, "T": wl.T, "B": 1},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample, **host_info()},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
@@ -292,6 +403,8 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=100_000)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the configs[1..3] sub-objects")
+    ap.add_argument("--e2e-full-steps", type=int, default=3)
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo only for single-GPU multi-process smoke runs")
     ap.add_argument("--force-dist", action="store_true",
@@ -419,7 +532,31 @@ def main():
                "h2d_bytes_per_step": int(h_ll.numel() * 4 + h_lp.numel() * 4 + h_la.numel() * 4),
                "d2h_bytes_per_step": int(h_out.numel() * 8), "ms_per_step": ms_e2e,
                "note": "PCIe-bound: the step's log_lik (16 B/step) crosses the host link every step"}
-        del h_ll, d_ll
+        # e2e_full: as e2e, plus the step's full results back to pinned host memory every step
+        # (filtered + smoothed marginals and the MAP path: what a user who needs the outputs waits for)
+        h_f = torch.empty(out_s[0].shape, dtype=torch.float32).pin_memory()
+        h_s = torch.empty(out_s[1].shape, dtype=torch.float32).pin_memory()
+        h_p = torch.empty(out_v[0].shape, dtype=torch.int32).pin_memory()
+
+        def e2e_full_step():
+            e2e_step()
+            h_f.copy_(out_s[0], non_blocking=True); h_s.copy_(out_s[1], non_blocking=True)
+            h_p.copy_(out_v[0], non_blocking=True)
+
+        nfull = max(1, min(args.steps, args.e2e_full_steps))
+        e2e_full_step()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(nfull):
+            e2e_full_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms_full = e0.elapsed_time(e1) / nfull
+        e2e["full"] = {"value": T / (ms_full * 1e-3), "unit": UNIT, "ms_per_step": ms_full, "steps": nfull,
+                       "h2d_bytes_per_step": e2e["h2d_bytes_per_step"],
+                       "d2h_bytes_per_step": int(h_out.numel() * 8 + (h_f.numel() + h_s.numel() + h_p.numel()) * 4),
+                       "note": "H2D of log_lik + smooth + viterbi + D2H of filtered, smoothed, path and scalars"}
+        del h_ll, d_ll, h_f, h_s, h_p
         # the same GE sequence through the symbol-input API: a GE user holds the
         # channel outputs y (1 B/step) and the emission matrix, not log_lik
         if args.workload == "ge":
@@ -460,22 +597,28 @@ def main():
     vi_bytes = VITERBI_BYTES_PER_STEP(D) * T
     ach_s = sm_bytes / (ms_s * 1e-3) / 1e9
     ach_v = vi_bytes / (ms_v * 1e-3) / 1e9
-    alu_peak = 148 * 128 * peaks["sm_mhz"] * 1e6 / 1e12  # T lane-op/s
-    ach_alu = VITERBI_ALU_PER_STEP(D) * T / (ms_v * 1e-3) / 1e12
     kname = lambda op: ("hmm_stream_kernel" if H.plan(op, D, T)["fused"] == 2 else "hmm_small_kernel") + f"<{D},{op}>"
     roof_s = {"kernel": kname(0) + " (smoother)", "bound": "hbm", "achieved": ach_s,
               "peak": peaks["hbm"], "unit": "GB/s", "frac": ach_s / peaks["hbm"],
               "traffic": traffic.get("smooth", {}).get("dram_bytes_per_launch"),
               "peak_source": peaks["src"], "ms_per_launch": ms_s, "algorithmic_bytes_per_launch": sm_bytes}
-    roof_v = {"kernel": kname(1) + " (viterbi)", "bound": "alu", "achieved": ach_alu,
-              "peak": alu_peak, "unit": "Tlane-op/s", "frac": ach_alu / alu_peak,
-              "hbm_achieved_gbs": ach_v, "hbm_frac": ach_v / peaks["hbm"],
-              "traffic": traffic.get("viterbi", {}).get("dram_bytes_per_launch"), "ms_per_launch": ms_v}
+    # Viterbi at D <= 8: of its two floors -- the algorithmic 20 B/step at the HBM peak and the max-plus
+    # fold's FADD2 + FMNMX3 issue ceiling (config_lines) -- the HBM one is the larger, so it is the bound.
+    v_clk = (D ** 3 / 2 + D * D * (D - 1) / 2) / 128
+    v_alu_ceiling = 148 * peaks["sm_mhz"] * 1e6 / v_clk
+    roof_v = {"kernel": kname(1) + " (viterbi)", "bound": "hbm", "achieved": ach_v,
+              "peak": peaks["hbm"], "unit": "GB/s", "frac": ach_v / peaks["hbm"],
+              "alu_frac": (T / (ms_v * 1e-3)) / v_alu_ceiling,
+              "traffic": traffic.get("viterbi", {}).get("dram_bytes_per_launch"), "ms_per_launch": ms_v,
+              "algorithmic_bytes_per_launch": vi_bytes}
     dominant = roof_s if ms_s >= ms_v else roof_v
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         v, sample, cores = cpu_oracle_rate(wl, args.cpu_budget)
-        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample}
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample, **host_info()}
+    configs = None
+    if rank == 0 and world == 1 and not args.no_configs and args.workload == "ge" and T == 100_000_000:
+        configs = config_lines(H, dev, max(10, min(args.steps, 50)), args.warmup, flush_l2, peaks)
 
     if rank == 0:
         line = {
@@ -488,6 +631,7 @@ def main():
             "viterbi_steps_per_s": T / (ms_v * 1e-3),
             "roofline": dominant, "roofline_all": [roof_s, roof_v],
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": 2 * args.steps,
+            "configs": configs,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
