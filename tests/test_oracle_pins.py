@@ -404,3 +404,80 @@ def test_joint_weight_diff_matches_difference_of_weights():
                                                                                              wl.log_lik, b)
         assert abs(d - ref) <= 1e-9 * max(1.0, abs(ref))
         assert oracle.joint_weight_diff(wl.log_pi, wl.log_A, wl.log_lik, a, a) == 0.0
+
+
+# ---------------------------------------------------------------- paper-faithful variants
+from oracle import variants  # noqa: E402
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_alg5_and_path_elements_vs_brute_force(seed):
+    """Algorithm 5 (Eq. 21 assembly) and the Def. 4 reduction both give the enumerated MAP on inputs
+    whose best sequence is unique by a margin (Theorem 4 / Corollary 1)."""
+    rng = np.random.default_rng(7000 + seed)
+    D = int(rng.integers(2, 5)); T = int(rng.integers(2, 8))
+    lp, la, ll = _rng_model(rng, D, T, normalized=bool(seed % 2))
+    bv = brute.viterbi(lp, la, ll)
+    x, w = bv["path"], bv["log_prob"]
+    if bv["gap"] < 1e-6:
+        pytest.skip("tied instance")
+    a5 = variants.viterbi_maxproduct(lp, la, ll)
+    np.testing.assert_array_equal(a5["path"], x)
+    assert abs(a5["log_prob"] - w) <= 1e-9 * max(1, abs(w))
+    assert abs(a5["path_weight"] - w) <= 1e-9 * max(1, abs(w)) and a5["coherent"]
+    pe = variants.viterbi_path_elements(lp, la, ll)
+    np.testing.assert_array_equal(pe["path"], x)
+    assert abs(pe["log_prob"] - w) <= 1e-9 * max(1, abs(w))
+
+
+def test_alg5_incoherent_under_ties_closed_form():
+    """Two MAP paths (0,1,0,1,..) and (1,0,1,0,..) tie; Eq. 21 takes the smallest index at every (tied)
+    step and assembles (0,0,...,0), whose weight is log(pi_0) + (T-1) log(eps) + sum ll: SPEC's
+    diagnostic must flag it, and the Def. 4 reduction must still return a MAP path."""
+    eps, T = 0.1, 6
+    lp = np.log(np.array([0.5, 0.5])).astype(np.float32)
+    la = np.log(np.array([[eps, 1 - eps], [1 - eps, eps]])).astype(np.float32)
+    ll = np.zeros((T, 2), np.float32)
+    a5 = variants.viterbi_maxproduct(lp, la, ll)
+    np.testing.assert_array_equal(a5["path"], np.zeros(T, np.int32))
+    map_w = float(np.float64(lp[0]) + (T - 1) * np.float64(la[0, 1]))
+    bad_w = float(np.float64(lp[0]) + (T - 1) * np.float64(la[0, 0]))
+    assert abs(a5["log_prob"] - map_w) <= 1e-12
+    assert abs(a5["path_weight"] - bad_w) <= 1e-12
+    assert not a5["coherent"] and a5["n_tied"] == T
+    pe = variants.viterbi_path_elements(lp, la, ll)
+    assert abs(pe["log_prob"] - map_w) <= 1e-12
+    assert abs(oracle.joint_weight(lp, la, ll, pe["path"]) - map_w) <= 1e-12
+
+
+def test_path_elements_vs_alg4_on_ge():
+    """Near-tie-free GE sequence (jittered, SURVEY §8(d) recipe): the Def. 4 reduction, Algorithm 5 and
+    the Algorithm 4 oracle agree on the path exactly and on the weight to 1e-9."""
+    wl = W.ge(256, seed=3, jitter=0.1)
+    v = oracle.viterbi(wl.log_pi, wl.log_A, wl.log_lik)
+    _, gap = oracle.max_marginals(wl.log_pi, wl.log_A, wl.log_lik)
+    assert gap.min() >= 1e-3
+    pe = variants.viterbi_path_elements(wl.log_pi, wl.log_A, wl.log_lik)
+    a5 = variants.viterbi_maxproduct(wl.log_pi, wl.log_A, wl.log_lik)
+    np.testing.assert_array_equal(pe["path"], v["path"])
+    np.testing.assert_array_equal(a5["path"], v["path"])
+    assert abs(pe["log_prob"] - v["log_prob"]) <= 1e-9 * abs(v["log_prob"])
+    assert abs(a5["log_prob"] - v["log_prob"]) <= 1e-9 * abs(v["log_prob"])
+
+
+def test_alg5_raw_ge_flags_ties():
+    """Raw GE observations have exact max-marginal ties: the diagnostic counts them and
+    any incoherent assembly is flagged (path weight below the MAP)."""
+    wl = W.ge(10_000, seed=0)
+    a5 = variants.viterbi_maxproduct(wl.log_pi, wl.log_A, wl.log_lik)
+    v = oracle.viterbi(wl.log_pi, wl.log_A, wl.log_lik)
+    assert a5["n_tied"] > 0
+    assert abs(a5["log_prob"] - v["log_prob"]) <= 1e-9 * abs(v["log_prob"])
+    assert a5["coherent"] == (a5["path_weight"] >= v["log_prob"] - 1e-9 * abs(v["log_prob"]))
+    assert a5["path_weight"] <= v["log_prob"] + 1e-9 * abs(v["log_prob"])
+
+
+def test_path_elements_cap():
+    wl = W.ge(variants.PATH_ELEMENT_MAX_T + 1, seed=0)
+    with pytest.raises(ValueError):
+        variants.viterbi_path_elements(wl.log_pi, wl.log_A, wl.log_lik)
