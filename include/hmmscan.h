@@ -65,7 +65,18 @@ typedef enum {
     HMM_ERR_CUDA = 4
 } hmm_status_t;
 
-typedef enum { HMM_OP_SMOOTH = 0, HMM_OP_VITERBI = 1, HMM_OP_SMOOTH_STATS = 2 } hmm_op_t;
+typedef enum {
+    HMM_OP_SMOOTH = 0,
+    HMM_OP_VITERBI = 1,
+    HMM_OP_SMOOTH_STATS = 2,
+    HMM_OP_VITERBI_MAXPRODUCT = 5, /* hmm_viterbi_maxproduct (Algorithm 5) */
+    HMM_OP_VITERBI_PATHELEM = 6    /* hmm_viterbi_path_elements (Definition 4) */
+} hmm_op_t;
+
+/* Device info codes beyond the common ones (0 ok, t+1 first impossible step, -1 NaN / +inf input). */
+#define HMM_INFO_AMBIGUOUS (-2) /* Algorithm 5: the Eq. 21 assembly is not a MAP path (ties) */
+#define HMM_INFO_NO_PATH (-3)   /* Definition 4: no sequence has nonzero weight (step not located) */
+#define HMM_PATHELEM_MAX_T 1024 /* cap of the path-element reduction */
 
 /* Human-readable name of a status code (static storage, never NULL). */
 const char* hmm_status_string(hmm_status_t status);
@@ -151,6 +162,42 @@ hmm_status_t hmm_smooth_batched(int D, int64_t T, int64_t B, const float* log_pi
 hmm_status_t hmm_viterbi_batched(int D, int64_t T, int64_t B, const float* log_pi, const float* log_A,
                                  const float* log_lik, int32_t* path, double* log_prob, int32_t* info,
                                  void* workspace, size_t workspace_bytes, void* stream);
+
+/*
+ * Paper-faithful Viterbi variants (validation modes, not the production path).
+ * 1 <= D <= 8, B sequences of equal length T sharing log_pi / log_A (layouts as the batched calls; B = 1
+ * for a single sequence).  Inputs/outputs are device pointers, 4-B aligned (doubles / int64 8-B aligned).
+ *
+ * hmm_viterbi_maxproduct — Algorithm 5: forward max-product scan -> log psi~f_k
+ * (Prop. 2), reversed scan -> log psi~b_k (Prop. 3), then
+ * x*_k = argmax_x psi~f_k(x) psi~b_k(x) (Theorem 4 / Eq. 21), smallest index on ties.
+ *   path [B*T] out: the Eq. 21 assembly.  Under exact ties it need not be ONE path.
+ *   log_prob [B] out (double): the per-step optimum max_x log psi~f_k + log psi~b_k (k = T-1), = the MAP
+ *                         joint log-probability by Theorem 4.
+ *   path_weight [B] out (double, may be NULL): Eq. 6 joint log-weight of the assembled path, fp64.
+ *   n_tied [B] out (int64, may be NULL): steps whose best and second-best max-marginal scores differ by
+ *                         <= tie_tol (nats, >= 0; 0 counts exact fp32 ties).
+ *   info [B] out: as hmm_viterbi, plus HMM_INFO_AMBIGUOUS when path_weight < log_prob - 1e-6 max(1, |log_prob|)
+ *                         (SPEC.md:297-303's coherence diagnostic: the tied steps did not assemble into a
+ *                         MAP path).
+ *   Workspace: hmm_workspace_size(HMM_OP_VITERBI_MAXPRODUCT, D, T, B), zero-filled, left zeroed.
+ *
+ * hmm_viterbi_path_elements — Definition 4: elements a~_{i:j} = (A_{i:j}, X^_{i:j})
+ * carrying the max weight and the interior path for every state pair, combined by v; the reduction
+ * a~_{0:T+1} holds the MAP weight and path (Theorem 3, Corollary 1).  Memory grows as
+ * D^2 states per step, so T <= HMM_PATHELEM_MAX_T (else HMM_ERR_INVALID_VALUE).
+ *   path [B*T] out: the MAP path (smallest x^_j at every combine on ties); log_prob [B] out (double).
+ *   info [B] out: 0, -1 (NaN / +inf input) or HMM_INFO_NO_PATH (every sequence has zero weight).
+ *   Workspace: hmm_workspace_size(HMM_OP_VITERBI_PATHELEM, D, T, B) (no zero-fill needed).
+ */
+hmm_status_t hmm_viterbi_maxproduct(int D, int64_t T, int64_t B, const float* log_pi, const float* log_A,
+                                    const float* log_lik, float tie_tol, int32_t* path, double* log_prob,
+                                    double* path_weight, int64_t* n_tied, int32_t* info, void* workspace,
+                                    size_t workspace_bytes, void* stream);
+
+hmm_status_t hmm_viterbi_path_elements(int D, int64_t T, int64_t B, const float* log_pi, const float* log_A,
+                                       const float* log_lik, int32_t* path, double* log_prob, int32_t* info,
+                                       void* workspace, size_t workspace_bytes, void* stream);
 
 /*
  * Split-phase distributed execution (one sequence partitioned along T across `world` ranks, one

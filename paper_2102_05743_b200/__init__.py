@@ -22,6 +22,9 @@ import torch
 from .build import LIB, ROOT
 
 HMM_OP_SMOOTH, HMM_OP_VITERBI, HMM_OP_SMOOTH_STATS = 0, 1, 2
+HMM_OP_VITERBI_MAXPRODUCT, HMM_OP_VITERBI_PATHELEM = 5, 6
+HMM_INFO_AMBIGUOUS, HMM_INFO_NO_PATH = -2, -3
+HMM_PATHELEM_MAX_T = 1024
 HMM_MAX_D = 64
 STATUS = {0: "HMM_SUCCESS", 1: "HMM_ERR_INVALID_VALUE", 2: "HMM_ERR_WORKSPACE", 3: "HMM_ERR_UNSUPPORTED",
           4: "HMM_ERR_CUDA"}
@@ -62,6 +65,10 @@ def lib() -> ctypes.CDLL:
         L.hmm_viterbi_symbols.restype = i32
         L.hmm_debug_force_path.argtypes = [i32]
         L.hmm_debug_force_path.restype = None
+        L.hmm_viterbi_maxproduct.argtypes = [i32, i64, i64, p, p, p, ctypes.c_float, p, p, p, p, p, p, sz, p]
+        L.hmm_viterbi_maxproduct.restype = i32
+        L.hmm_viterbi_path_elements.argtypes = [i32, i64, i64, p, p, p, p, p, p, p, sz, p]
+        L.hmm_viterbi_path_elements.restype = i32
         L.hmm_debug_plan.restype = i32
         for f in ("hmm_smooth", "hmm_viterbi", "hmm_smooth_batched", "hmm_viterbi_batched"):
             getattr(L, f).restype = i32
@@ -264,4 +271,38 @@ def viterbi(log_pi, log_A, log_lik, out=None, ws=None, stream=None):
         st = L.hmm_viterbi(D, T, _ptr(log_pi), _ptr(log_A), _ptr(log_lik), _ptr(path), _ptr(lp), _ptr(info),
                            _ptr(ws), ws.numel(), _stream(stream))
     _check(st, "hmm_viterbi")
+    return path, lp, info
+
+
+def viterbi_maxproduct(log_pi, log_A, log_lik, tie_tol: float = 0.0, stream=None):
+    """Algorithm 5: per-step argmax of the max-product forward x backward potentials
+    (Eq. 21) with SPEC's coherence diagnostic.  A validation mode; hmm_viterbi is the production path.
+    Returns (path, log_prob [B] f64, path_weight [B] f64, n_tied [B] i64, info [B] i32) on device; info is
+    HMM_INFO_AMBIGUOUS where the Eq. 21 assembly is not a MAP path."""
+    batched, B, T, D = _inputs(log_pi, log_A, log_lik)
+    dev = log_lik.device
+    path = torch.empty(log_lik.shape[:-1], dtype=torch.int32, device=dev)
+    lp = torch.empty(B, dtype=torch.float64, device=dev)
+    pw = torch.empty(B, dtype=torch.float64, device=dev)
+    nt = torch.empty(B, dtype=torch.int64, device=dev)
+    info = torch.empty(B, dtype=torch.int32, device=dev)
+    ws = workspace(HMM_OP_VITERBI_MAXPRODUCT, D, T, B, dev, stream)
+    st = lib().hmm_viterbi_maxproduct(D, T, B, _ptr(log_pi), _ptr(log_A), _ptr(log_lik), float(tie_tol), _ptr(path),
+                                      _ptr(lp), _ptr(pw), _ptr(nt), _ptr(info), _ptr(ws), ws.numel(), _stream(stream))
+    _check(st, "hmm_viterbi_maxproduct")
+    return path, lp, pw, nt, info
+
+
+def viterbi_path_elements(log_pi, log_A, log_lik, stream=None):
+    """Definition 4 path-element reduction (Corollary 1), T <= 1024.
+    Returns (path, log_prob [B] f64, info [B] i32) on device."""
+    batched, B, T, D = _inputs(log_pi, log_A, log_lik)
+    dev = log_lik.device
+    path = torch.empty(log_lik.shape[:-1], dtype=torch.int32, device=dev)
+    lp = torch.empty(B, dtype=torch.float64, device=dev)
+    info = torch.empty(B, dtype=torch.int32, device=dev)
+    ws = workspace(HMM_OP_VITERBI_PATHELEM, D, T, B, dev, stream)
+    st = lib().hmm_viterbi_path_elements(D, T, B, _ptr(log_pi), _ptr(log_A), _ptr(log_lik), _ptr(path), _ptr(lp),
+                                         _ptr(info), _ptr(ws), ws.numel(), _stream(stream))
+    _check(st, "hmm_viterbi_path_elements")
     return path, lp, info

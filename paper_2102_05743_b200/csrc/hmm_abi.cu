@@ -19,6 +19,7 @@ cudaError_t launch_small(int D, int op, unsigned G, unsigned B, size_t smem, boo
 cudaError_t launch_large(int DP, int op, const LgParams& p, cudaStream_t s);
 cudaError_t launch_stream(int D, int op, unsigned G, const SParams& sp, cudaStream_t s);
 int large_leaves_per_block(int DP);
+size_t variants_workspace_size(int op, int D, int64_t T, int64_t B);
 }
 
 using hmm::Plan;
@@ -533,6 +534,8 @@ int hmm_debug_plan(int op, int D, int64_t T, int64_t B, int64_t* out /*[8]*/) {
 }
 
 size_t hmm_workspace_size(int op, int D, int64_t T, int64_t B) {
+    if (op == HMM_OP_VITERBI_MAXPRODUCT || op == HMM_OP_VITERBI_PATHELEM)
+        return hmm::variants_workspace_size(op, D, T, B);
     if (op == 2) {  // smoother with E-step statistics (hmm_smooth_stats)
         StPlan SP;
         if (D < 1 || D > 8 || T < 1 || B != 1 || !make_stream_plan(D, 2, T, SP)) return 0;

@@ -221,6 +221,28 @@ __device__ void tree_up(float* tree, int NP) {
         __syncthreads();
     }
 }
+// matrix x column vector in either semiring: y(i) = (+)_j M(i,j) (x) v(j), normalised (pow2 / max 0)
+// [backward carry; the max-plus form serves Algorithm 5's reversed scan, Prop. 3]
+template <int D, bool MP>
+__device__ __forceinline__ void mat_vec_sr(const float* M, const float* v, float* y) {
+    if constexpr (!MP) {
+        mat_vec<D>(M, v, y);
+    } else {
+#pragma unroll
+        for (int i = 0; i < D; i++) {
+            float s[D];
+#pragma unroll
+            for (int j = 0; j < D; j++) s[j] = M[i * D + j] + v[j];
+            y[i] = vmax<D>(s);
+        }
+        const float m = vmax<D>(y);
+        if (m > neg_inf()) {
+#pragma unroll
+            for (int i = 0; i < D; i++) y[i] -= m;
+        }
+    }
+}
+
 // Down-sweep of carries.  pre(x) = (left boundary) (x) all leaves left of x's subtree,
 // suf(x) = all leaves right of x's subtree (x) (right boundary).  pre is stored in elements
 // [0, D) and suf in [D, 2D) of the node (overwriting matrices no longer needed).
@@ -258,6 +280,11 @@ __device__ void tree_down(float* tree, int NP, const float* pre_root, const floa
 #pragma unroll
                     for (int k = 0; k < D; k++) sc[k] = pre[k] + tree[(k * D + d) * NN + 2 * x];
                     pr = vmax<D>(sc);
+                    if (SUF) {
+#pragma unroll
+                        for (int j = 0; j < D; j++) sc[j] = tree[(d * D + j) * NN + 2 * x + 1] + suf[j];
+                        sl = vmax<D>(sc);
+                    }
                 } else {
                     pr = pre[0] * tree[d * NN + 2 * x];
 #pragma unroll
@@ -276,6 +303,7 @@ __device__ void tree_down(float* tree, int NP, const float* pre_root, const floa
                 }
                 if constexpr (MP) {
                     if (mp > neg_inf()) pr -= mp;
+                    if (SUF && ms > neg_inf()) sl -= ms;
                 } else {
                     pr *= pow2_inv(mp);
                     if (SUF) sl *= pow2_inv(ms);
@@ -303,7 +331,7 @@ __device__ void tree_down(float* tree, int NP, const float* pre_root, const floa
                 vec_mat<D, MP>(pre, Lm, preR);
                 if (SUF) {
                     tree_load<D>(tree, NN, 2 * x + 1, Rm);
-                    mat_vec<D>(Rm, suf, sufL);
+                    mat_vec_sr<D, MP>(Rm, suf, sufL);
                 }
 #pragma unroll
                 for (int d = 0; d < D; d++) {

@@ -3,7 +3,7 @@
 # keeps the logs in gpurun_out/sanitize/.  Usage (GPU box): bash tools/sanitize.sh [family ...]
 set -u
 out=gpurun_out/sanitize; mkdir -p "$out"
-fams=${*:-"small stream chunked large tc batched stats symbols"}
+fams=${*:-"small stream chunked large tc batched stats symbols variants"}
 for tool in memcheck racecheck synccheck; do
   for f in $fams; do
     timeout 300 compute-sanitizer --tool $tool --error-exitcode 9 --print-limit 20 \

@@ -62,6 +62,16 @@ def symbols():
     assert int(info.item()) == 0 and int(vinfo.item()) == 0
 
 
+def variants():
+    wl = W.random_potentials(4, 5001, 3, B=2)
+    lp, la, ll = (torch.from_numpy(x).cuda() for x in (wl.log_pi, wl.log_A, wl.log_lik))
+    out = H.viterbi_maxproduct(lp, la, ll)
+    pe = H.viterbi_path_elements(lp, la, ll[:, :1000].contiguous())
+    torch.cuda.synchronize()
+    assert int(out[-1].abs().max().item()) == 0 and int(pe[-1].abs().max().item()) == 0
+
+
+FAMILIES["variants"] = variants
 FAMILIES["stats"] = stats
 FAMILIES["symbols"] = symbols
 
