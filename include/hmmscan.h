@@ -70,12 +70,15 @@ typedef enum {
     HMM_OP_VITERBI = 1,
     HMM_OP_SMOOTH_STATS = 2,
     HMM_OP_VITERBI_MAXPRODUCT = 5, /* hmm_viterbi_maxproduct (Algorithm 5) */
-    HMM_OP_VITERBI_PATHELEM = 6    /* hmm_viterbi_path_elements (Definition 4) */
+    HMM_OP_VITERBI_PATHELEM = 6,   /* hmm_viterbi_path_elements (Definition 4) */
+    HMM_OP_SMOOTH_VARLEN = 7,      /* hmm_smooth_varlen (T = max_T) */
+    HMM_OP_VITERBI_VARLEN = 8      /* hmm_viterbi_varlen (T = max_T) */
 } hmm_op_t;
 
 /* Device info codes beyond the common ones (0 ok, t+1 first impossible step, -1 NaN / +inf input). */
 #define HMM_INFO_AMBIGUOUS (-2) /* Algorithm 5: the Eq. 21 assembly is not a MAP path (ties) */
 #define HMM_INFO_NO_PATH (-3)   /* Definition 4: no sequence has nonzero weight (step not located) */
+#define HMM_INFO_BAD_LENGTH (-4) /* varlen batches: offsets[b+1] - offsets[b] outside [1, max_T] */
 #define HMM_PATHELEM_MAX_T 1024 /* cap of the path-element reduction */
 
 /* Human-readable name of a status code (static storage, never NULL). */
@@ -162,6 +165,32 @@ hmm_status_t hmm_smooth_batched(int D, int64_t T, int64_t B, const float* log_pi
 hmm_status_t hmm_viterbi_batched(int D, int64_t T, int64_t B, const float* log_pi, const float* log_A,
                                  const float* log_lik, int32_t* path, double* log_prob, int32_t* info,
                                  void* workspace, size_t workspace_bytes, void* stream);
+
+/*
+ * Variable-length batches and per-sequence models (extends the batched calls).
+ * B independent sequences packed back to back: sequence b owns rows [offsets[b], offsets[b+1]) of
+ * log_lik [N*D] (N = offsets[B]) and of the outputs filtered / smoothed [N*D] and path [N]; its length
+ * T_b = offsets[b+1] - offsets[b] must lie in [1, max_T] (else info[b] = HMM_INFO_BAD_LENGTH and that
+ * sequence's outputs are undefined).  Every sequence is its own HMM (Eq. 5 potentials):
+ * its first step takes the prior, its last step the all-ones backward element a_{T:T+1} (Thm 2).
+ *   offsets [B+1] in: device int64, 8-B aligned (read on the device; the host passes only max_T).
+ *   per_sequence_model = 0: log_pi [D], log_A [D*D] shared by the batch;
+ *                      != 0: log_pi [B*D], log_A [B*D*D], one model per sequence.
+ *   log_likelihood / log_prob / info [B] out, as the batched calls.
+ * 1 <= D <= 64 (D >= 9: filtered is required, as hmm_smooth).  D <= 8 runs one CTA per sequence; D >= 9
+ * the large-D block scan planned for max_T (CUDA cores; the tensor-core leaf needs one shared A).
+ * Workspace: hmm_workspace_size(HMM_OP_SMOOTH_VARLEN / HMM_OP_VITERBI_VARLEN, D, max_T, B), zero-filled,
+ * left zeroed.
+ */
+hmm_status_t hmm_smooth_varlen(int D, int64_t B, int64_t max_T, const int64_t* offsets, const float* log_pi,
+                               const float* log_A, int per_sequence_model, const float* log_lik, float* filtered,
+                               float* smoothed, double* log_likelihood, int32_t* info, void* workspace,
+                               size_t workspace_bytes, void* stream);
+
+hmm_status_t hmm_viterbi_varlen(int D, int64_t B, int64_t max_T, const int64_t* offsets, const float* log_pi,
+                                const float* log_A, int per_sequence_model, const float* log_lik, int32_t* path,
+                                double* log_prob, int32_t* info, void* workspace, size_t workspace_bytes,
+                                void* stream);
 
 /*
  * Paper-faithful Viterbi variants (validation modes, not the production path).

@@ -23,6 +23,8 @@ from .build import LIB, ROOT
 
 HMM_OP_SMOOTH, HMM_OP_VITERBI, HMM_OP_SMOOTH_STATS = 0, 1, 2
 HMM_OP_VITERBI_MAXPRODUCT, HMM_OP_VITERBI_PATHELEM = 5, 6
+HMM_OP_SMOOTH_VARLEN, HMM_OP_VITERBI_VARLEN = 7, 8
+HMM_INFO_BAD_LENGTH = -4
 HMM_INFO_AMBIGUOUS, HMM_INFO_NO_PATH = -2, -3
 HMM_PATHELEM_MAX_T = 1024
 HMM_MAX_D = 64
@@ -69,6 +71,10 @@ def lib() -> ctypes.CDLL:
         L.hmm_viterbi_maxproduct.restype = i32
         L.hmm_viterbi_path_elements.argtypes = [i32, i64, i64, p, p, p, p, p, p, p, sz, p]
         L.hmm_viterbi_path_elements.restype = i32
+        L.hmm_smooth_varlen.argtypes = [i32, i64, i64, p, p, p, i32, p, p, p, p, p, p, sz, p]
+        L.hmm_smooth_varlen.restype = i32
+        L.hmm_viterbi_varlen.argtypes = [i32, i64, i64, p, p, p, i32, p, p, p, p, p, sz, p]
+        L.hmm_viterbi_varlen.restype = i32
         L.hmm_debug_plan.restype = i32
         for f in ("hmm_smooth", "hmm_viterbi", "hmm_smooth_batched", "hmm_viterbi_batched"):
             getattr(L, f).restype = i32
@@ -305,4 +311,60 @@ def viterbi_path_elements(log_pi, log_A, log_lik, stream=None):
     st = lib().hmm_viterbi_path_elements(D, T, B, _ptr(log_pi), _ptr(log_A), _ptr(log_lik), _ptr(path), _ptr(lp),
                                          _ptr(info), _ptr(ws), ws.numel(), _stream(stream))
     _check(st, "hmm_viterbi_path_elements")
+    return path, lp, info
+
+
+def _varlen_inputs(log_pi, log_A, log_lik, offsets, max_T):
+    for t in (log_pi, log_A, log_lik, offsets):
+        if not t.is_cuda:
+            raise HmmError("inputs must be CUDA tensors (no CPU fallback)")
+        if not t.is_contiguous():
+            raise HmmError("inputs must be contiguous")
+    for t in (log_pi, log_A, log_lik):
+        if t.dtype != torch.float32:
+            raise HmmError("log_pi, log_A, log_lik must be float32")
+    if offsets.dtype != torch.int64 or offsets.dim() != 1 or offsets.numel() < 2:
+        raise HmmError("offsets must be a 1-D int64 tensor [B+1]")
+    if log_lik.dim() != 2:
+        raise HmmError("log_lik must be packed [N, D]")
+    B, D = offsets.numel() - 1, log_lik.shape[1]
+    per_seq = log_pi.dim() == 2
+    if per_seq:
+        if tuple(log_pi.shape) != (B, D) or tuple(log_A.shape) != (B, D, D):
+            raise HmmError("per-sequence models: log_pi [B, D], log_A [B, D, D]")
+    elif tuple(log_pi.shape) != (D,) or tuple(log_A.shape) != (D, D):
+        raise HmmError("shared model: log_pi [D], log_A [D, D]")
+    if int(max_T) < 1:
+        raise HmmError("max_T must be >= 1")
+    return B, D, int(per_seq)
+
+
+def smooth_varlen(log_pi, log_A, log_lik, offsets, max_T: int, stream=None):
+    """Variable-length batch smoother: sequence b = rows [offsets[b], offsets[b+1]) of
+    the packed log_lik [N, D]; log_pi/log_A shared ([D], [D, D]) or per sequence ([B, D], [B, D, D]).
+    Returns (filtered [N, D], smoothed [N, D], log_likelihood [B] f64, info [B] i32) on device."""
+    B, D, per_seq = _varlen_inputs(log_pi, log_A, log_lik, offsets, max_T)
+    dev = log_lik.device
+    filt = torch.empty_like(log_lik)
+    sm = torch.empty_like(log_lik)
+    lz = torch.empty(B, dtype=torch.float64, device=dev)
+    info = torch.empty(B, dtype=torch.int32, device=dev)
+    ws = workspace(HMM_OP_SMOOTH_VARLEN, D, int(max_T), B, dev, stream)
+    st = lib().hmm_smooth_varlen(D, B, int(max_T), _ptr(offsets), _ptr(log_pi), _ptr(log_A), per_seq, _ptr(log_lik),
+                                 _ptr(filt), _ptr(sm), _ptr(lz), _ptr(info), _ptr(ws), ws.numel(), _stream(stream))
+    _check(st, "hmm_smooth_varlen")
+    return filt, sm, lz, info
+
+
+def viterbi_varlen(log_pi, log_A, log_lik, offsets, max_T: int, stream=None):
+    """Variable-length batch MAP paths (f4).  Returns (path [N] i32, log_prob [B] f64, info [B] i32)."""
+    B, D, per_seq = _varlen_inputs(log_pi, log_A, log_lik, offsets, max_T)
+    dev = log_lik.device
+    path = torch.empty(log_lik.shape[0], dtype=torch.int32, device=dev)
+    lp = torch.empty(B, dtype=torch.float64, device=dev)
+    info = torch.empty(B, dtype=torch.int32, device=dev)
+    ws = workspace(HMM_OP_VITERBI_VARLEN, D, int(max_T), B, dev, stream)
+    st = lib().hmm_viterbi_varlen(D, B, int(max_T), _ptr(offsets), _ptr(log_pi), _ptr(log_A), per_seq, _ptr(log_lik),
+                                  _ptr(path), _ptr(lp), _ptr(info), _ptr(ws), ws.numel(), _stream(stream))
+    _check(st, "hmm_viterbi_varlen")
     return path, lp, info

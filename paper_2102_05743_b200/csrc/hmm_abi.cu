@@ -70,7 +70,7 @@ int pow2_ceil(int x) {
 }
 
 // Work decomposition for the small-D kernels (see hmm_plan.h and DESIGN.md §"Decomposition").
-bool make_plan(int D, int op, int64_t T, int64_t B, Plan& P, bool chunked = false) {
+bool make_plan(int D, int op, int64_t T, int64_t B, Plan& P, bool chunked = false, bool one_cta = false) {
     DevInfo di;
     if (!dev_info(di)) return false;
     P = Plan{};
@@ -79,7 +79,7 @@ bool make_plan(int D, int op, int64_t T, int64_t B, Plan& P, bool chunked = fals
     const int NT = P.NT;
     const size_t smax = (size_t)di.smem_optin;
     int64_t G;
-    if (B >= di.sms) {
+    if (B >= di.sms || one_cta) {  // (variable-length batches: one CTA per sequence, f4)
         G = 1;
     } else {
         G = di.sms / B;
@@ -474,6 +474,80 @@ __global__ void dist_combine_kernel(int world, const double* g, uint64_t* rec_al
     if (vinfo) vinfo[0] = combine_codes(g, world, 6);
 }
 
+// Variable-length batches and per-sequence models.  D <= 8: the resident/chunked
+// kernel with one CTA per sequence (each CTA reads its length from the offsets); D >= 9: the large-D
+// engine planned for max_T (blocks and leaves past a sequence's end are empty = identity elements).
+bool varlen_large_plan(int D, int op, int64_t maxT, int64_t B, LgPlan& G) {
+    return make_large_plan(D, op, maxT, B, G, /*allow_tc=*/false);
+}
+hmm_status_t run_varlen(int op, int D, int64_t B, int64_t maxT, const int64_t* offsets, const float* log_pi,
+                        const float* log_A, int per_seq, const float* log_lik, float* filtered, float* smoothed,
+                        int32_t* path, double* scalar, int32_t* info, void* ws, size_t ws_bytes, void* stream) {
+    if (D < 1 || B < 1 || B > 65535 || maxT < 1 || !offsets) return HMM_ERR_INVALID_VALUE;
+    if (D > HMM_MAX_D) return HMM_ERR_UNSUPPORTED;
+    if (!log_pi || !log_A || !log_lik || !scalar || !info) return HMM_ERR_INVALID_VALUE;
+    if (op == 0 && (!smoothed || (D > 8 && !filtered))) return HMM_ERR_INVALID_VALUE;
+    if (op == 1 && !path) return HMM_ERR_INVALID_VALUE;
+    if (!al8(offsets) || !al4(log_pi) || !al4(log_A) || !al4(log_lik) || !al8(scalar) || !al4(info) ||
+        (filtered && !al4(filtered)) || (smoothed && !al4(smoothed)) || (path && !al4(path)))
+        return HMM_ERR_INVALID_VALUE;
+    const int64_t pis = per_seq ? D : 0, As = per_seq ? (int64_t)D * D : 0;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (D > 8) {
+        LgPlan G;
+        if (!varlen_large_plan(D, op, maxT, B, G)) return HMM_ERR_UNSUPPORTED;
+        if (!ws || ws_bytes < G.total || (reinterpret_cast<uintptr_t>(ws) & 255u)) return HMM_ERR_WORKSPACE;
+        uint8_t* w = static_cast<uint8_t*>(ws);
+        hmm::LgParams lp;
+        std::memset(&lp, 0, sizeof(lp));
+        lp.T = maxT; lp.B = B; lp.D = D; lp.SL = G.SL; lp.NL = G.NL; lp.NB = G.NB;
+        lp.log_pi = log_pi; lp.log_A = log_A; lp.log_lik = log_lik;
+        lp.filtered = filtered; lp.smoothed = smoothed; lp.path = path; lp.scalar_out = scalar; lp.info = info;
+        lp.ws_sync = w + G.o_sync;
+        lp.leafagg = reinterpret_cast<float*>(w + G.o_leaf);
+        lp.groot = reinterpret_cast<float*>(w + G.o_groot);
+        lp.bpre = reinterpret_cast<float*>(w + G.o_bpre);
+        lp.bsuf = reinterpret_cast<float*>(w + G.o_bsuf);
+        lp.partial = reinterpret_cast<double*>(w + G.o_part);
+        lp.bp = w + G.o_bp;
+        lp.lmap = w + G.o_lmap;
+        lp.bmap = w + G.o_bmap;
+        lp.bend = reinterpret_cast<int32_t*>(w + G.o_bend);
+        lp.xstar = reinterpret_cast<int32_t*>(w + G.o_xstar);
+        lp.tc = 0;
+        lp.offsets = offsets; lp.pi_stride = pis; lp.A_stride = As;
+        cudaError_t e = hmm::launch_large(G.DP, op, lp, s);
+        return e == cudaSuccess ? HMM_SUCCESS : HMM_ERR_CUDA;
+    }
+    Plan P;
+    if (!make_plan(D, op, maxT, B, P, false, /*one_cta=*/true)) return HMM_ERR_UNSUPPORTED;
+    if (!ws || ws_bytes < P.ws_total || (reinterpret_cast<uintptr_t>(ws) & 255u)) return HMM_ERR_WORKSPACE;
+    hmm::KParams kp;
+    std::memset(&kp, 0, sizeof(kp));
+    kp.T = maxT; kp.R = P.R; kp.S = P.S; kp.chunk = P.chunk; kp.K = P.K; kp.KP = P.KP; kp.fused = P.fused ? 1 : 0;
+    kp.log_pi = log_pi; kp.log_A = log_A; kp.log_lik = log_lik;
+    kp.filtered = filtered; kp.smoothed = smoothed; kp.path = path; kp.scalar_out = scalar; kp.info = info;
+    kp.ws = static_cast<uint8_t*>(ws);
+    kp.ws_sync = P.ws_sync; kp.ws_slots = P.ws_slots; kp.slot_bytes = P.slot_bytes;
+    kp.ws_chunk = P.ws_chunk; kp.chunk_slot = P.chunk_slot; kp.ws_bp = P.ws_bp; kp.ws_lmap = P.ws_lmap;
+    kp.L = hmm::small_smem_layout(D, op, P.chunk, P.KP, P.G);
+    kp.ws_cmap = P.ws_cmap;
+    kp.mode = hmm::HMM_MODE_FULL; kp.world = 1;
+    kp.offsets = offsets; kp.pi_stride = pis; kp.A_stride = As;
+    cudaError_t e = hmm::launch_small(D, op, (unsigned)P.G, (unsigned)P.B, P.smem, false, kp, s);
+    return e == cudaSuccess ? HMM_SUCCESS : HMM_ERR_CUDA;
+}
+
+size_t varlen_workspace_size(int op, int D, int64_t maxT, int64_t B) {
+    if (D < 1 || D > HMM_MAX_D || maxT < 1 || B < 1 || B > 65535) return 0;
+    if (D > 8) {
+        LgPlan G;
+        return varlen_large_plan(D, op, maxT, B, G) ? G.total : 0;
+    }
+    Plan P;
+    return make_plan(D, op, maxT, B, P, false, true) ? P.ws_total : 0;
+}
+
 }  // namespace
 
 extern "C" {
@@ -536,6 +610,8 @@ int hmm_debug_plan(int op, int D, int64_t T, int64_t B, int64_t* out /*[8]*/) {
 size_t hmm_workspace_size(int op, int D, int64_t T, int64_t B) {
     if (op == HMM_OP_VITERBI_MAXPRODUCT || op == HMM_OP_VITERBI_PATHELEM)
         return hmm::variants_workspace_size(op, D, T, B);
+    if (op == HMM_OP_SMOOTH_VARLEN || op == HMM_OP_VITERBI_VARLEN)
+        return varlen_workspace_size(op == HMM_OP_SMOOTH_VARLEN ? 0 : 1, D, T, B);
     if (op == 2) {  // smoother with E-step statistics (hmm_smooth_stats)
         StPlan SP;
         if (D < 1 || D > 8 || T < 1 || B != 1 || !make_stream_plan(D, 2, T, SP)) return 0;
@@ -670,3 +746,19 @@ hmm_status_t hmm_viterbi_batched(int D, int64_t T, int64_t B, const float* log_p
 }
 
 }  // extern "C"
+
+hmm_status_t hmm_smooth_varlen(int D, int64_t B, int64_t max_T, const int64_t* offsets, const float* log_pi,
+                               const float* log_A, int per_sequence_model, const float* log_lik, float* filtered,
+                               float* smoothed, double* log_likelihood, int32_t* info, void* workspace,
+                               size_t workspace_bytes, void* stream) {
+    return run_varlen(0, D, B, max_T, offsets, log_pi, log_A, per_sequence_model, log_lik, filtered, smoothed,
+                      nullptr, log_likelihood, info, workspace, workspace_bytes, stream);
+}
+
+hmm_status_t hmm_viterbi_varlen(int D, int64_t B, int64_t max_T, const int64_t* offsets, const float* log_pi,
+                                const float* log_A, int per_sequence_model, const float* log_lik, int32_t* path,
+                                double* log_prob, int32_t* info, void* workspace, size_t workspace_bytes,
+                                void* stream) {
+    return run_varlen(1, D, B, max_T, offsets, log_pi, log_A, per_sequence_model, log_lik, nullptr, nullptr, path,
+                      log_prob, info, workspace, workspace_bytes, stream);
+}

@@ -22,6 +22,7 @@
 
 #include "hmm_device.cuh"
 #include "hmm_large.h"
+#include "hmm_plan.h"
 
 namespace hmm {
 
@@ -56,14 +57,14 @@ __device__ __forceinline__ int og_global_lookup(const LgParams& p, int64_t b, in
 }
 
 // A(k, j) for the padded model (exp for sum-product, log for max-product).
-__device__ __forceinline__ float lg_A(const LgParams& p, int k, int j, bool mp) {
+__device__ __forceinline__ float lg_A(const LgParams& p, int64_t b, int k, int j, bool mp) {
     if (k >= p.D || j >= p.D) return lg_pad(mp);
-    const float la = __ldg(p.log_A + k * p.D + j);
+    const float la = __ldg(p.log_A + b * p.A_stride + k * p.D + j);
     return mp ? la : ex2(la * kLog2e);
 }
-__device__ __forceinline__ float lg_pi(const LgParams& p, int j, bool mp) {
+__device__ __forceinline__ float lg_pi(const LgParams& p, int64_t b, int j, bool mp) {
     if (j >= p.D) return lg_pad(mp);
-    const float lp = __ldg(p.log_pi + j);
+    const float lp = __ldg(p.log_pi + b * p.pi_stride + j);
     return mp ? lp : ex2(lp * kLog2e);
 }
 
@@ -135,7 +136,8 @@ __global__ void __launch_bounds__(256) lg_leaf_kernel(const LgParams p) {
     const int lidx = warp * LPW + sub;                    // leaf index inside the block
     const int64_t L = (int64_t)blk * NLB + lidx;          // leaf index inside the sequence
     float* Pm = sm + (size_t)lidx * DP * DP;
-    const int64_t T = p.T;
+    int64_t sbase, T_raw;  // packed first row / length of sequence b (varlen batches, f4)
+    const int64_t T = seq_span(p.offsets, p.T, b, sbase, T_raw);
     const int64_t t0 = L * p.SL;
     auto leaf_len = [&](int64_t LL) -> int {
         const int64_t a = LL * p.SL;
@@ -153,8 +155,8 @@ __global__ void __launch_bounds__(256) lg_leaf_kernel(const LgParams p) {
         for (int c = 0; c < CPL; c++) {
             const int j = cl * CPL + c;
     #pragma unroll
-            for (int k = 0; k < DP; k++) Acol[c][k] = lg_A(p, k, j, MP);
-            pv[c] = lg_pi(p, j, MP);
+            for (int k = 0; k < DP; k++) Acol[c][k] = lg_A(p, b, k, j, MP);
+            pv[c] = lg_pi(p, b, j, MP);
         }
         constexpr bool PK = (CPL == 1);           // packed row pairs (DP = 16, 32; see the loop)
         constexpr bool PC = (CPL == 2 && MP);     // packed column pairs (max-product, DP = 64)
@@ -167,7 +169,7 @@ __global__ void __launch_bounds__(256) lg_leaf_kernel(const LgParams p) {
     #pragma unroll
             for (int k = 0; k < DP; k++) A2[k] = make_float2(Acol[0][k], Acol[1][k]);
         }
-        const float* ll = p.log_lik + (size_t)b * T * p.D;
+        const float* ll = p.log_lik + (size_t)sbase * p.D;
         bool bad = false;
         float s = MP ? 0.0f : 1.0f;  // pending normalisation (scale / offset) from the previous step
         float chk = 0.0f;
@@ -369,11 +371,16 @@ __global__ void __launch_bounds__(256) lg_leaf_kernel(const LgParams p) {
                     dst[r * DP + cl * CPL + c] = x;
                 }
         } else {
+            // an empty leaf (past the end of a shorter sequence of a varlen batch) is the identity
+            // element; the sweep's leaf chains read it back from the workspace
+            float* dst = (L < p.NL) ? p.leafagg + ((size_t)b * p.NL + L) * DP * DP : nullptr;
             for (int r = 0; r < DP; r++)
     #pragma unroll
                 for (int c = 0; c < CPL; c++) {
                     const int j = cl * CPL + c;
-                    Pm[r * DP + j] = (r == j) ? (MP ? 0.0f : 1.0f) : lg_pad(MP);
+                    const float v = (r == j) ? (MP ? 0.0f : 1.0f) : lg_pad(MP);
+                    Pm[r * DP + j] = v;
+                    if (dst) dst[r * DP + j] = v;
                 }
         }
         if constexpr (MP) bad |= (chk != chk);
@@ -579,7 +586,8 @@ __global__ void __launch_bounds__(256) lg_sweep_kernel(const LgParams p) {
     const int sub = lane / LPL, cl = lane % LPL;
     const int lidx = warp * LPW + sub;
     const int64_t L = (int64_t)blk * NLB + lidx;
-    const int64_t T = p.T;
+    int64_t sbase, T_raw;  // packed first row / length of sequence b (varlen batches, f4)
+    const int64_t T = seq_span(p.offsets, p.T, b, sbase, T_raw);
     const int D = p.D;
     const float* leafs = p.leafagg + ((size_t)b * p.NL + (size_t)blk * NLB) * DP * DP;
     int nleaf = NLB;  // leaves of this block that exist
@@ -600,7 +608,7 @@ __global__ void __launch_bounds__(256) lg_sweep_kernel(const LgParams p) {
 #pragma unroll
     for (int o = LPL; o < 32; o <<= 1) nmax = max(nmax, __shfl_xor_sync(0xffffffffu, nmax, o));
     const int64_t t0 = L * p.SL;
-    const float* ll = p.log_lik + (size_t)b * T * D;
+    const float* ll = p.log_lik + (size_t)sbase * D;
     float* vv = vec + lidx * DP;
     uint32_t* sync = reinterpret_cast<uint32_t*>(p.ws_sync + b * 64);
     unsigned long long* zero_code = reinterpret_cast<unsigned long long*>(sync + 4);
@@ -613,8 +621,8 @@ __global__ void __launch_bounds__(256) lg_sweep_kernel(const LgParams p) {
 #pragma unroll
         for (int c = 0; c < CPL; c++) {
 #pragma unroll
-            for (int k = 0; k < DP; k++) Acol[c][k] = lg_A(p, k, cl * CPL + c, false);
-            pv[c] = lg_pi(p, cl * CPL + c, false);
+            for (int k = 0; k < DP; k++) Acol[c][k] = lg_A(p, b, k, cl * CPL + c, false);
+            pv[c] = lg_pi(p, b, cl * CPL + c, false);
         }
         float a_own[CPL];
         {
@@ -694,7 +702,7 @@ __global__ void __launch_bounds__(256) lg_sweep_kernel(const LgParams p) {
                     a_own[c] = ah[c] * r;
                     vv[cl * CPL + c] = a_own[c];
                     const int j = cl * CPL + c;
-                    if (j < D) filt[((size_t)b * T + t) * D + j] = a_own[c];
+                    if (j < D) filt[((size_t)sbase + t) * D + j] = a_own[c];
                 }
             }
             __syncwarp();
@@ -716,7 +724,7 @@ __global__ void __launch_bounds__(256) lg_sweep_kernel(const LgParams p) {
 #pragma unroll
         for (int c = 0; c < CPL; c++)
 #pragma unroll
-            for (int j = 0; j < DP; j++) Arow[c][j] = lg_A(p, cl * CPL + c, j, false);
+            for (int j = 0; j < DP; j++) Arow[c][j] = lg_A(p, b, cl * CPL + c, j, false);
         float bt[CPL];
 #pragma unroll
         for (int c = 0; c < CPL; c++) bt[c] = lsuf[lidx * DP + cl * CPL + c];
@@ -725,7 +733,7 @@ __global__ void __launch_bounds__(256) lg_sweep_kernel(const LgParams p) {
 #pragma unroll
             for (int c = 0; c < CPL; c++) {
                 const int j = cl * CPL + c;
-                a[c] = (i >= 0 && i < n && j < D) ? filt[((size_t)b * T + t0 + i) * D + j] : 0.0f;
+                a[c] = (i >= 0 && i < n && j < D) ? filt[((size_t)sbase + t0 + i) * D + j] : 0.0f;
             }
         };
         float fnext[CPL], lnext[CPL];
@@ -753,7 +761,7 @@ __global__ void __launch_bounds__(256) lg_sweep_kernel(const LgParams p) {
 #pragma unroll
             for (int c = 0; c < CPL; c++) {
                 const int j = cl * CPL + c;
-                if (act && j < D) p.smoothed[((size_t)b * T + t) * D + j] = g[c] * rz;
+                if (act && j < D) p.smoothed[((size_t)sbase + t) * D + j] = g[c] * rz;
             }
             if (i > 0) {
                 float v[CPL];
@@ -801,8 +809,8 @@ __global__ void __launch_bounds__(256) lg_sweep_kernel(const LgParams p) {
 #pragma unroll
         for (int c = 0; c < CPL; c++) {
 #pragma unroll
-            for (int k = 0; k < DP; k++) LAc[c][k] = lg_A(p, k, cl * CPL + c, true);
-            lpv[c] = lg_pi(p, cl * CPL + c, true);
+            for (int k = 0; k < DP; k++) LAc[c][k] = lg_A(p, b, k, cl * CPL + c, true);
+            lpv[c] = lg_pi(p, b, cl * CPL + c, true);
         }
         uint8_t* og = orig + lidx * DP;
 #pragma unroll
@@ -901,7 +909,7 @@ __global__ void __launch_bounds__(256) lg_sweep_kernel(const LgParams p) {
                     V[c] = Vn[c] - o;
                     vv[j] = V[c];
                     og[j] = on[c];
-                    p.bp[((size_t)b * T + t) * DP + j] = (uint8_t)arg[c];
+                    p.bp[((size_t)b * p.T + t) * DP + j] = (uint8_t)arg[c];
                 }
             }
             __syncwarp();
@@ -921,6 +929,10 @@ __global__ void __launch_bounds__(256) lg_sweep_kernel(const LgParams p) {
                 for (int c = 0; c < CPL; c++)
                     p.lmap[((size_t)b * p.NL + L) * DP + cl * CPL + c] = og[cl * CPL + c];
                 if (t0 + n == T && cl == 0) p.xstar[b] = xs;
+            } else if (L < p.NL) {  // empty leaf (varlen batch): identity map
+#pragma unroll
+                for (int c = 0; c < CPL; c++)
+                    p.lmap[((size_t)b * p.NL + L) * DP + cl * CPL + c] = (uint8_t)(cl * CPL + c);
             }
         }
         __syncthreads();
@@ -956,7 +968,8 @@ __global__ void __launch_bounds__(256) lg_backtrack_kernel(const LgParams p) {
     __shared__ int ends[NLB];
     const int64_t b = blockIdx.y;
     const int blk = blockIdx.x;
-    const int64_t T = p.T;
+    int64_t sbase, T_raw;  // packed first row / length of sequence b (varlen batches, f4)
+    const int64_t T = seq_span(p.offsets, p.T, b, sbase, T_raw);
     int nleaf = NLB;
     if ((int64_t)blk * NLB + nleaf > p.NL) nleaf = (int)(p.NL - (int64_t)blk * NLB);
     if (threadIdx.x == 0) {
@@ -976,8 +989,8 @@ __global__ void __launch_bounds__(256) lg_backtrack_kernel(const LgParams p) {
         int x = ends[q];
         for (int i = n - 1; i >= 0; i--) {
             const int64_t t = a + i;
-            p.path[(size_t)b * T + t] = x;
-            x = p.bp[((size_t)b * T + t) * DP + x];
+            p.path[(size_t)sbase + t] = x;
+            x = p.bp[((size_t)b * p.T + t) * DP + x];
         }
     }
 }
@@ -1004,6 +1017,9 @@ __global__ void lg_finalize_kernel(const LgParams p) {
         int32_t inf = 0;
         if (badf) inf = -1;
         else if (zc) inf = (int32_t)((1ull << 62) - zc + 1ull);
+        int64_t sb, raw;
+        seq_span(p.offsets, p.T, b, sb, raw);
+        if (raw < 1 || raw > p.T) inf = kInfoBadLength;
         p.info[b] = inf;
     }
 }

@@ -34,6 +34,9 @@ struct LgParams {
     // tensor-core leaf products (sum-product, DP = 64): hmm_large_tc.cu
     int tc;             // 1: leaf aggregates come from lg_leaf_tc_kernel
     float* lik;         // [B][T][64] likelihood rows exp(ll - m_t), padded with 0
+    // variable-length batches / per-sequence models (see KParams in hmm_plan.h)
+    const int64_t* offsets;
+    int64_t pi_stride, A_stride;
 };
 
 }  // namespace hmm

@@ -132,8 +132,27 @@ struct KParams {
     const uint8_t* rec_all;  // [world][16] Viterbi rank records {u64 map, i32 x*} (mode 4)
     uint8_t* rec_out;        // this rank's record (mode 3)
     size_t ws_cmap;          // per-chunk Viterbi maps persisted between modes 3 and 4
+    // variable-length batches: sequence b = packed rows [offsets[b], offsets[b+1]),
+    // 1 <= length <= T (T = the batch's max length); null = every sequence has T rows at b*T
+    const int64_t* offsets;
+    int64_t pi_stride, A_stride;  // per-sequence models: log_pi + b*pi_stride, log_A + b*A_stride (0: shared)
 };
 
+
+// Sequence b of a (possibly variable-length) batch: its length, clamped to [0, Tmax], and its first row
+// in the packed sequence buffers.  `raw` receives the unclamped length (validity is reported in info).
+__host__ __device__ __forceinline__ int64_t seq_span(const int64_t* offsets, int64_t Tmax, int64_t b, int64_t& base,
+                                                     int64_t& raw) {
+    if (!offsets) {
+        base = b * Tmax;
+        raw = Tmax;
+        return Tmax;
+    }
+    base = offsets[b];
+    raw = offsets[b + 1] - base;
+    return raw < 0 ? 0 : (raw > Tmax ? Tmax : raw);
+}
+constexpr int32_t kInfoBadLength = -4;  // HMM_INFO_BAD_LENGTH (hmmscan.h)
 
 // ---------------------------------------------------------------------------- lane streaming
 // Long single sequences (DESIGN.md §"Streaming"): lane g = c*NT + tid of the G CTAs owns the

@@ -45,7 +45,8 @@ __global__ void __launch_bounds__(small_nt(D)) hmm_small_kernel(const KParams p)
     const int warp = tid >> 5, lane = tid & 31;
     const int c = blockIdx.x, G = gridDim.x;
     const int64_t b = blockIdx.y;
-    const int64_t T = p.T;
+    int64_t sbase, T_raw;  // first packed row of sequence b, its length (varlen batches: f4)
+    const int64_t T = seq_span(p.offsets, p.T, b, sbase, T_raw);
     const int64_t cta0 = (int64_t)c * p.R;
     const int64_t cta1 = (cta0 + p.R < T) ? cta0 + p.R : T;
     const int nchunks = (int)((cta1 - cta0 + p.chunk - 1) / p.chunk);
@@ -65,7 +66,7 @@ __global__ void __launch_bounds__(small_nt(D)) hmm_small_kernel(const KParams p)
     const size_t map_off = align16((size_t)D * D * 4);
     const int sw = (int)(p.slot_bytes / 4);  // slot stride in words
     uint8_t* myslot = slots + (size_t)c * p.slot_bytes;
-    const float* ll_seq = p.log_lik + (size_t)b * T * D;
+    const float* ll_seq = p.log_lik + (size_t)sbase * D;
 
     float* tile = reinterpret_cast<float*>(smem + p.L.tile);
     float* carr = reinterpret_cast<float*>(smem + p.L.carr);
@@ -95,12 +96,12 @@ __global__ void __launch_bounds__(small_nt(D)) hmm_small_kernel(const KParams p)
     float A[D * D], pv[D];
 #pragma unroll
     for (int e = 0; e < D * D; e++) {
-        const float la = __ldg(p.log_A + e);
+        const float la = __ldg(p.log_A + b * p.A_stride + e);
         A[e] = MP ? la : ex2(la * kLog2e);
     }
 #pragma unroll
     for (int d = 0; d < D; d++) {
-        const float lp = __ldg(p.log_pi + d);
+        const float lp = __ldg(p.log_pi + b * p.pi_stride + d);
         pv[d] = MP ? lp : ex2(lp * kLog2e);
     }
 
@@ -301,13 +302,13 @@ __global__ void __launch_bounds__(small_nt(D)) hmm_small_kernel(const KParams p)
             int r0, nr;
             warp_rows(nch, r0, nr);
             if (p.filtered && nr > 0)
-                warp_store(p.filtered + ((size_t)b * T + ch0 + r0) * D, filt + (size_t)r0 * D, (int64_t)nr * D);
+                warp_store(p.filtered + ((size_t)sbase + ch0 + r0) * D, filt + (size_t)r0 * D, (int64_t)nr * D);
             if (tmr && tid == 0) tmr[15] = clock64();
             HMM_STAMP(6);
             if (ln > 0) sp_beta<D>(tile + li * D, filt + li * D, ln, A, beta);
             HMM_STAMP(7);
             if (nr > 0)
-                warp_store(p.smoothed + ((size_t)b * T + ch0 + r0) * D, tile + (size_t)r0 * D, (int64_t)nr * D);
+                warp_store(p.smoothed + ((size_t)sbase + ch0 + r0) * D, tile + (size_t)r0 * D, (int64_t)nr * D);
             warp_store_wait();
             __syncthreads();
             HMM_STAMP(8);
@@ -463,7 +464,7 @@ __global__ void __launch_bounds__(small_nt(D)) hmm_small_kernel(const KParams p)
             int r0, nr;
             warp_rows(nch, r0, nr);
             __syncwarp();
-            if (nr > 0) warp_store(p.path + (size_t)b * T + ch0 + r0, out + r0, nr);
+            if (nr > 0) warp_store(p.path + (size_t)sbase + ch0 + r0, out + r0, nr);
             warp_store_wait();
             __syncthreads();
         }
@@ -494,6 +495,7 @@ __global__ void __launch_bounds__(small_nt(D)) hmm_small_kernel(const KParams p)
             int32_t inf = 0;
             if (badf) inf = -1;
             else if (zc) inf = (int32_t)((1ull << 62) - zc + 1ull);
+            if (T_raw < 1 || T_raw > p.T) inf = kInfoBadLength;
             if (p.info) p.info[b] = inf;
             // every CTA has passed every wait of this launch: reset the arrival counters
             atomicExch(arrive1, 0ull);
