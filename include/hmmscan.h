@@ -316,8 +316,10 @@ hmm_status_t hmm_dist_combine(int world, const double* gathered, void* records_a
  *   hmm_debug_force_path: for calls made later from the calling host thread, select the
  *     decomposition: 0 automatic (default); for 1 <= D <= 8 and B == 1: 1 lane-streaming (16-B
  *     aligned buffers required, else automatic), 2 resident/chunked; for 33 <= D <= 64: 3 keeps the
- *     sum-product leaf products on the FP32 CUDA cores instead of the tensor cores.  Test and
- *     profiling use only; the results agree within the stated tolerances whichever path runs.
+ *     sum-product leaf products on the FP32 CUDA cores instead of the tensor cores; for 9 <= D <= 32:
+ *     4 forces the batch-parallel plan (one lane group per sequence running the Algorithm 1 / 4
+ *     recursions, chosen automatically for large B), 5 forbids it (block scan).  Test and profiling
+ *     use only; the results agree within the stated tolerances whichever path runs.
  */
 void hmm_debug_set_timers(unsigned long long* device_buf);
 int hmm_debug_plan(int op, int D, int64_t T, int64_t B, int64_t* out);

@@ -100,7 +100,8 @@ def plan(op: int, D: int, T: int, B: int = 1) -> dict:
 
 
 def force_path(path: int):
-    """Testing/profiling: 0 automatic, 1 lane-streaming, 2 resident/chunked (calling thread only)."""
+    """Testing/profiling (calling thread only): 0 automatic, 1 lane-streaming, 2 resident/chunked,
+    3 large-D leaves on CUDA cores (no tcgen05), 4 batch-parallel plan for 9 <= D <= 32, 5 never it."""
     lib().hmm_debug_force_path(int(path))
 
 

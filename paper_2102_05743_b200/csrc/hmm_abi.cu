@@ -20,6 +20,7 @@ cudaError_t launch_large(int DP, int op, const LgParams& p, cudaStream_t s);
 cudaError_t launch_stream(int D, int op, unsigned G, const SParams& sp, cudaStream_t s);
 int large_leaves_per_block(int DP);
 size_t variants_workspace_size(int op, int D, int64_t T, int64_t B);
+cudaError_t launch_batchseq(int DP, int op, const BSParams& p, cudaStream_t s);
 }
 
 using hmm::Plan;
@@ -205,6 +206,42 @@ bool use_stream(int D, int64_t T, int64_t B, bool dist) {
 }
 bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
+// Batch-parallel plan (hmm_batchseq.cu) for 9 <= D <= 32: one lane group per sequence running the
+// element recursions; chosen when the batch is large enough that the scan's D^3 element products cost
+// more than the recursions' per-step latency.  hmm_debug_force_path: 4 forces it,
+// 5 forbids it.
+int bs_dp(int D) { return D <= 16 ? 16 : (D <= 32 ? 32 : 0); }
+// The plan's time is T x (per-step latency of the recursion, ~190 ns) until the batch saturates the
+// issue slots; the scan's is proportional to B T D^3.  Measured crossover (tools/batchseq_crossover.py,
+// T = 4096, profiles/r2/batchseq_crossover.txt; T cancels): DP = 16 smoother B ~ 770, Viterbi ~ 550;
+// DP = 32 smoother ~ 150, Viterbi ~ 100.
+bool use_batchseq(int D, int op, int64_t B) {
+    const int DP = bs_dp(D);
+    if (D <= 8 || DP == 0) return false;
+    if (t_force_path == 4) return true;
+    if (t_force_path == 5) return false;
+    const int64_t bmin = DP == 16 ? (op == 0 ? 768 : 512) : (op == 0 ? 160 : 128);
+    return B >= bmin;
+}
+size_t bs_workspace(int op, int D, int64_t T, int64_t B) {
+    return op == 1 ? (((size_t)B * T * bs_dp(D) + 255) & ~(size_t)255) : 256;
+}
+hmm_status_t run_batchseq(int op, int D, int64_t T, int64_t B, const int64_t* offsets, int64_t pis, int64_t As,
+                          const float* log_pi, const float* log_A, const float* log_lik, float* filtered,
+                          float* smoothed, int32_t* path, double* scalar, int32_t* info, void* ws, size_t ws_bytes,
+                          void* stream) {
+    if (!ws || ws_bytes < bs_workspace(op, D, T, B) || (reinterpret_cast<uintptr_t>(ws) & 255u)) return HMM_ERR_WORKSPACE;
+    hmm::BSParams bp;
+    std::memset(&bp, 0, sizeof(bp));
+    bp.T = T; bp.B = B; bp.D = D;
+    bp.log_pi = log_pi; bp.log_A = log_A; bp.log_lik = log_lik;
+    bp.filtered = filtered; bp.smoothed = smoothed; bp.path = path; bp.scalar_out = scalar; bp.info = info;
+    bp.bp = static_cast<uint8_t*>(ws);
+    bp.offsets = offsets; bp.pi_stride = pis; bp.A_stride = As;
+    const cudaError_t e = hmm::launch_batchseq(bs_dp(D), op, bp, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? HMM_SUCCESS : HMM_ERR_CUDA;
+}
+
 // Profiling hook (hmm_debug_set_timers): per-thread, not used unless set.
 thread_local unsigned long long* t_timers = nullptr;
 
@@ -282,6 +319,9 @@ hmm_status_t run(int op, int D, int64_t T, int64_t B, const float* log_pi, const
         if (op == 1 && !path) return HMM_ERR_INVALID_VALUE;
         if (op == 0 && !filtered) return HMM_ERR_UNSUPPORTED;  // large-D smoother stages alpha in `filtered`
         if (!al4(log_pi) || !al4(log_A) || !al4(log_lik) || !al8(scalar) || !al4(info)) return HMM_ERR_INVALID_VALUE;
+        if (use_batchseq(D, op, B))
+            return run_batchseq(op, D, T, B, nullptr, 0, 0, log_pi, log_A, log_lik, filtered, smoothed, path, scalar,
+                                info, ws, ws_bytes, stream);
         LgPlan G;
         if (!make_large_plan(D, op, T, B, G)) return HMM_ERR_UNSUPPORTED;
         if (!ws || ws_bytes < G.total || (reinterpret_cast<uintptr_t>(ws) & 255u)) return HMM_ERR_WORKSPACE;
@@ -494,6 +534,9 @@ hmm_status_t run_varlen(int op, int D, int64_t B, int64_t maxT, const int64_t* o
     const int64_t pis = per_seq ? D : 0, As = per_seq ? (int64_t)D * D : 0;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (D > 8) {
+        if (use_batchseq(D, op, B))
+            return run_batchseq(op, D, maxT, B, offsets, pis, As, log_pi, log_A, log_lik, filtered, smoothed, path,
+                                scalar, info, ws, ws_bytes, stream);
         LgPlan G;
         if (!varlen_large_plan(D, op, maxT, B, G)) return HMM_ERR_UNSUPPORTED;
         if (!ws || ws_bytes < G.total || (reinterpret_cast<uintptr_t>(ws) & 255u)) return HMM_ERR_WORKSPACE;
@@ -542,7 +585,10 @@ size_t varlen_workspace_size(int op, int D, int64_t maxT, int64_t B) {
     if (D < 1 || D > HMM_MAX_D || maxT < 1 || B < 1 || B > 65535) return 0;
     if (D > 8) {
         LgPlan G;
-        return varlen_large_plan(D, op, maxT, B, G) ? G.total : 0;
+        if (!varlen_large_plan(D, op, maxT, B, G)) return 0;
+        size_t w = G.total;
+        if (bs_dp(D) && bs_workspace(op, D, maxT, B) > w) w = bs_workspace(op, D, maxT, B);
+        return w;
     }
     Plan P;
     return make_plan(D, op, maxT, B, P, false, true) ? P.ws_total : 0;
@@ -591,7 +637,7 @@ const char* hmm_version(void) { return "hmmscan 0.1 sm_100a"; }
 
 void hmm_debug_set_timers(unsigned long long* device_buf) { t_timers = device_buf; }
 
-void hmm_debug_force_path(int path) { t_force_path = (path >= 0 && path <= 3) ? path : 0; }
+void hmm_debug_force_path(int path) { t_force_path = (path >= 0 && path <= 5) ? path : 0; }
 
 int hmm_debug_plan(int op, int D, int64_t T, int64_t B, int64_t* out /*[8]*/) {
     StPlan SP;
@@ -618,10 +664,12 @@ size_t hmm_workspace_size(int op, int D, int64_t T, int64_t B) {
         return SP.ws_total;
     }
     if ((op != 0 && op != 1) || D < 1 || D > HMM_MAX_D || T < 1 || B < 1) return 0;
-    if (D > 8) {  // either leaf-product engine may run (hmm_debug_force_path): size for both
+    if (D > 8) {  // any large-D engine may run (hmm_debug_force_path): size for all of them
         LgPlan G, H2;
         if (!make_large_plan(D, op, T, B, G, true) || !make_large_plan(D, op, T, B, H2, false)) return 0;
-        return G.total > H2.total ? G.total : H2.total;
+        size_t w = G.total > H2.total ? G.total : H2.total;
+        if (bs_dp(D) && bs_workspace(op, D, T, B) > w) w = bs_workspace(op, D, T, B);
+        return w;
     }
     Plan P;
     if (!make_plan(D, op, T, B, P)) return 0;

@@ -1,0 +1,491 @@
+// hmm_batchseq.cu — batch-parallel plan for many sequences with 9 <= D <= 32 (SURVEY.md §8(a) a9,
+// BASELINE config ④: B = 1024, D = 16, T = 4096), sm_100a.
+//
+// With B sequences the batch alone fills the GPU, so the scan's per-step D x D element products
+// (D^3 work) are pure overhead: each sequence is one block-wise element spanning the whole sequence
+// ("a single computational element to a set of consecutive observations"), evaluated
+// by the element recursions themselves — Algorithm 1's forward and backward passes (PAPER.md:156-174,
+// D^2 work per step) and Algorithm 4's forward max-product pass with backpointers.
+// The planner picks this plan when B is large enough that the scan's D^3 work costs more than the
+// recursions' latency (hmm_abi.cu); the scan plans stay for small B.
+//
+// One group of DP lanes (DP = 16: half a warp, DP = 32: a warp) owns a sequence; lane j holds state j.
+// A step gathers the previous vector with DP shuffles, so every lane also sees the whole vector: the
+// exact power-of-two renormalisation (sum-product) or the max subtraction (max-product) is computed
+// redundantly from the gathered values — no reduction on the recursion's critical path — and the
+// normalised outputs of step t are produced one step later, off it.  The vector exchange goes through a
+// per-group SMEM slot (one store, __syncwarp, broadcast LDS.128 reads) and the log_lik / filtered rows
+// are staged in SMEM chunks of kBsC steps by cp.async, two chunks ahead of the one in use (the
+// per-step loads of a register prefetch did not cover the memory latency at this step rate).
+//
+//   bs_smooth   forward: a_t = s_t ((a_{t-1} A) o l_t), s_t = 2^k from max(a_{t-1}); filtered_{t-1}
+//               = a_{t-1}/sum; log Z = log sum(a_{T-1}) - sum log s_t + sum m_t (exact telescoping).
+//               backward: b_{t-1} = s (A (l_t o b_t)); smoothed_t = f_t o b_t / sum (Eq. 14), f_t the
+//               filtered row read back.
+//   bs_viterbi  forward: V~_t(j) = max_i (V~_{t-1}(i) - o_{t-1} + log A(i,j)) + w_t(j), backpointer =
+//               smallest maximising i (one byte per state per step, workspace); then the backtrack,
+//               staged through shared memory in chunks.
+#include <cfloat>
+#include <cstdint>
+#include <cstring>
+
+#include "hmm_device.cuh"
+#include "hmm_large.h"
+#include "hmm_plan.h"
+
+namespace hmm {
+
+
+constexpr int kBsThreads = 128;
+constexpr int kBsC = 32;      // steps per staged chunk
+constexpr int kBsStages = 3;  // chunk ring depth (two chunks in flight ahead of the one in use)
+constexpr int kBsChunk = 256;  // backtrack chunk (steps)
+
+template <int DP>
+__device__ __forceinline__ unsigned bs_mask() {
+    if constexpr (DP == 32) return 0xffffffffu;
+    else return 0xffffu << (16 * ((threadIdx.x >> 4) & 1));
+}
+// log2 of the exact power-of-two factor pow2_inv(m) (0 when pow2_inv returns 1)
+__device__ __forceinline__ int pow2_inv_log2(float m) {
+    const uint32_t e = (__float_as_uint(m) >> 23) & 0xffu;
+    return (e == 0u || e >= 0xfeu) ? 0 : 127 - (int)e;
+}
+// Balanced trees (depth log2 N instead of an N-deep chain: the reductions sit on the recursion's
+// critical path, and the compiler may not reassociate fp adds).
+template <int N>
+__device__ __forceinline__ float tmax(const float* v) {
+    if constexpr (N == 1) return v[0];
+    else if constexpr (N == 2) return fmaxf(v[0], v[1]);
+    else return fmaxf(tmax<N / 2>(v), tmax<N - N / 2>(v + N / 2));
+}
+template <int N>
+__device__ __forceinline__ float tsum(const float* v) {
+    if constexpr (N == 1) return v[0];
+    else if constexpr (N == 2) return v[0] + v[1];
+    else return tsum<N / 2>(v) + tsum<N - N / 2>(v + N / 2);
+}
+// smallest k with v[k] == best (best = max v): equality bits OR-ed by a tree, then the lowest set bit
+template <int N>
+__device__ __forceinline__ uint32_t eq_bits(const float* v, float best, int k0) {
+    if constexpr (N == 1) return (v[0] == best) ? (1u << k0) : 0u;
+    else return eq_bits<N / 2>(v, best, k0) | eq_bits<N - N / 2>(v + N / 2, best, k0 + N / 2);
+}
+template <int N>
+__device__ __forceinline__ int first_argmax(const float* v, float best) {
+    const uint32_t m = eq_bits<N>(v, best, 0);
+    return m ? __ffs(m) - 1 : 0;
+}
+template <int N>
+__device__ __forceinline__ void ld_vec(const float* p, float* v) {
+#pragma unroll
+    for (int i = 0; i < N; i += 4) {
+        const float4 x = *reinterpret_cast<const float4*>(p + i);
+        v[i] = x.x; v[i + 1] = x.y; v[i + 2] = x.z; v[i + 3] = x.w;
+    }
+}
+
+// One warp per sequence: lane = (state j = lane % DP, half h = lane / DP), H = 32 / DP halves (2 for
+// DP = 16: two lanes per state split every dot product and reduction, so the batch of config ④ gives
+// twice as many warps to hide the recursion's latency).  NV = DP / H values per lane.
+template <int DP> struct BsShape {
+    static constexpr int H = 32 / DP;
+    static constexpr int NV = DP / H;
+};
+
+// Per-sequence staging of rows in SMEM: chunk c = rows [c C, c C + C) of a [T][D] array, row pitch DP
+// floats, element (r, j) copied by lane (j, r % H) with 4-B cp.async (any D, any row alignment),
+// kBsStages-deep ring, one cp.async group per chunk.
+template <int DP>
+struct BsRing {
+    float* buf;  // [kBsStages][kBsC][DP]
+    const float* src;
+    int64_t T;
+    int D, j, h;
+    __device__ __forceinline__ float* stage(int64_t c) const { return buf + (size_t)(c % kBsStages) * kBsC * DP; }
+    __device__ __forceinline__ void issue(int64_t c) const {
+        if (c >= 0 && c * kBsC < T && j < D) {
+            const int64_t r0 = c * kBsC;
+            const int n = (int)((T - r0 < kBsC) ? T - r0 : kBsC);
+            float* dst = stage(c) + j;
+            const float* s = src + r0 * D + j;
+            for (int r = h; r < n; r += BsShape<DP>::H) cp_async4(dst + r * DP, s + (int64_t)r * D);
+        }
+        cp_async_commit();
+    }
+};
+
+template <int DP>
+__device__ __forceinline__ void bs_fill(float* buf, int nfl, float v) {
+    for (int e = threadIdx.x % 32; e < nfl; e += 32) buf[e] = v;
+}
+
+// Chunk preparation: row r's maximum m_r = max_{j<D} ll_r(j) (lane r, kBsC = 32 rows) and a NaN / +inf
+// flag, then every element turned into l = exp(ll - m_r) (sum-product) or w = ll - m_r (max-product);
+// padded states get l = 0 / w = -inf.  The per-step recursion then reads one value.
+template <int DP, bool MP>
+__device__ __forceinline__ bool bs_prep(float* rows, float* mrow, int n, int D, int j, int h) {
+    const int lane = threadIdx.x % 32;
+    bool bad = false;
+    if (lane < n) {
+        float v[DP];
+        ld_vec<DP>(rows + lane * DP, v);
+        float cs = 0.0f;
+#pragma unroll
+        for (int k = 0; k < DP; k++) {
+            cs += (k < D) ? v[k] : 0.0f;
+            v[k] = (k < D) ? v[k] : neg_inf();
+        }
+        const float m = tmax<DP>(v);
+        bad = (cs != cs) || (cs == INFINITY);
+        mrow[lane] = (m > -FLT_MAX) ? m : 0.0f;  // impossible step: l = 0 / w = -inf, caught downstream
+    }
+    __syncwarp();
+    for (int r = h; r < n; r += BsShape<DP>::H) {
+        const float x = rows[r * DP + j] - mrow[r];
+        rows[r * DP + j] = (j < D) ? (MP ? x : ex2(x * kLog2e)) : (MP ? neg_inf() : 0.0f);
+    }
+    __syncwarp();
+    return __any_sync(0xffffffffu, bad);
+}
+
+// Normalise n staged rows and store them coalesced to dst rows [0, n) (pitch D).  Returns the first
+// zero-mass row (or -1) and the sum of row n-1 in `last`.
+template <int DP>
+__device__ __forceinline__ int bs_flush(float* rows, int n, float* dst, int D, int j, int h, float* inv, bool& bad,
+                                        float& last) {
+    const int lane = threadIdx.x % 32;
+    float sm = 1.0f;
+    if (lane < n) {
+        float v[DP];
+        ld_vec<DP>(rows + lane * DP, v);
+        sm = tsum<DP>(v);
+        inv[lane] = (sm > 0.0f) ? rcp(sm) : 0.0f;
+    }
+    const uint32_t zmask = __ballot_sync(0xffffffffu, lane < n && !(sm > 0.0f));
+    bad |= __any_sync(0xffffffffu, sm != sm);
+    last = __shfl_sync(0xffffffffu, sm, n - 1);
+    __syncwarp();
+    if (j < D)
+        for (int r = h; r < n; r += BsShape<DP>::H) dst[(int64_t)r * D + j] = rows[r * DP + j] * inv[r];
+    __syncwarp();
+    return zmask ? __ffs(zmask) - 1 : -1;
+}
+
+template <int DP>
+__global__ void __launch_bounds__(kBsThreads) bs_smooth_kernel(const BSParams p) {
+    using S = BsShape<DP>;
+    constexpr int H = S::H, NV = S::NV;
+    constexpr int SPB = kBsThreads / 32;
+    constexpr int RING = kBsStages * kBsC * DP;
+    constexpr int OUT = (kBsC + 1) * DP;
+    constexpr int PER = 2 * RING + OUT + 2 * kBsC;
+    extern __shared__ __align__(16) float bsm[];
+    const int lane = threadIdx.x % 32, grp = threadIdx.x / 32;
+    const int j = lane % DP, h = lane / DP;
+    float* rl_buf = bsm + (size_t)grp * PER;  // log_lik chunks (turned into l in place)
+    float* rf_buf = rl_buf + RING;            // filtered chunks (backward pass)
+    float* out = rf_buf + RING;               // [1 + C][DP]: row 0 = previous step, rows 1.. = this chunk
+    float* mrow = out + OUT;                  // [C] row maxima m_t
+    float* inv = mrow + kBsC;                 // [C] row normalisers
+    const int64_t b = (int64_t)blockIdx.x * SPB + grp;
+    if (b >= p.B) return;
+    int64_t base, raw;
+    const int64_t T = seq_span(p.offsets, p.T, b, base, raw);
+    if (T < 1) {  // (varlen: invalid length)
+        if (lane == 0) { p.scalar_out[b] = 0.0; p.info[b] = kInfoBadLength; }
+        return;
+    }
+    const int D = p.D;
+    const bool act = j < D;
+    const float* la = p.log_A + b * p.A_stride;
+    float Acol[NV], Arow[NV];  // A(i, j) and A(j, i) for i in this lane's half
+#pragma unroll
+    for (int k = 0; k < NV; k++) {
+        const int i = h * NV + k;
+        Acol[k] = (act && i < D) ? ex2(__ldg(la + i * D + j) * kLog2e) : 0.0f;
+        Arow[k] = (act && i < D) ? ex2(__ldg(la + j * D + i) * kLog2e) : 0.0f;
+    }
+    const float piv = act ? ex2(__ldg(p.log_pi + b * p.pi_stride + j) * kLog2e) : 0.0f;
+    float* filt = p.filtered + base * D;
+    float* smo = p.smoothed + base * D;
+    bs_fill<DP>(rl_buf, 2 * RING + OUT, 0.0f);  // pads of the filtered ring and the staging rows stay 0
+    __syncwarp();
+    const BsRing<DP> rl{rl_buf, p.log_lik + base * D, T, D, j, h};
+    const BsRing<DP> rf{rf_buf, filt, T, D, j, h};
+    const int64_t nch = (T + kBsC - 1) / kBsC;
+    auto hsum = [&](float v) -> float { return (H == 2) ? v + __shfl_xor_sync(0xffffffffu, v, 16) : v; };
+    auto hmax = [&](float v) -> float { return (H == 2) ? fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 16)) : v; };
+
+    // ---------------- forward (Algorithm 1 forward pass): a_t = s_t ((a_{t-1} A) o l_t), staged in `out`
+    // (the staged row is also the vector exchange), normalised per chunk into filtered.
+    double msum = 0.0;
+    int es = 0;           // sum of log2 s_t
+    int64_t zero_t = -1;  // first step with zero forward mass
+    bool bad = false;
+    float lastsum = 0.0f;
+    rl.issue(0);
+    rl.issue(1);
+    for (int64_t c = 0; c < nch; c++) {
+        rl.issue(c + 2);
+        cp_async_wait<2>();
+        __syncwarp();
+        float* rows = rl.stage(c);
+        const int n = (int)((T - c * kBsC < kBsC) ? T - c * kBsC : kBsC);
+        bad |= bs_prep<DP, false>(rows, mrow, n, D, j, h);
+        for (int i = 0; i < n; i++) msum += (double)mrow[i];
+        for (int i = 0; i < n; i++) {
+            const int64_t t = c * kBsC + i;
+            const float l = rows[i * DP + j];
+            float a;
+            if (t == 0) {
+                a = piv * l;
+            } else {
+                float g[NV];
+                ld_vec<NV>(out + i * DP + h * NV, g);  // this half of a_{t-1}
+                const float mx = hmax(tmax<NV>(g));
+                const float s = pow2_inv(mx);
+                es += pow2_inv_log2(mx);
+                float c0 = 0.0f, c1 = 0.0f, c2 = 0.0f, c3 = 0.0f;
+#pragma unroll
+                for (int k = 0; k < NV; k += 4) {
+                    c0 = fmaf(g[k], Acol[k], c0);
+                    c1 = fmaf(g[k + 1], Acol[k + 1], c1);
+                    c2 = fmaf(g[k + 2], Acol[k + 2], c2);
+                    c3 = fmaf(g[k + 3], Acol[k + 3], c3);
+                }
+                a = hsum((c0 + c1) + (c2 + c3)) * (l * s);
+            }
+            if (h == 0) out[(i + 1) * DP + j] = a;
+            __syncwarp();
+        }
+        const int z = bs_flush<DP>(out + DP, n, filt + c * kBsC * D, D, j, h, inv, bad, lastsum);
+        if (z >= 0 && zero_t < 0) zero_t = c * kBsC + z;
+        if (h == 0) out[j] = out[n * DP + j];  // carry a_{t0-1} into row 0
+        __syncwarp();
+    }
+    const double logz = log((double)lastsum) - (double)es * (double)kLn2 + msum;
+    cp_async_wait<0>();
+    __syncwarp();  // the filtered rows of the sequence are complete before the backward pass stages them
+
+    // ---------------- backward (Algorithm 1 backward pass) + Eq. 14, chunks in reverse order: the staged
+    // l row of step t becomes w = l_t o b_t (the exchange for b_{t-1}); gam_t = f_t o b_t is staged in
+    // `out` and normalised per chunk into smoothed.
+    float bt = act ? 1.0f : 0.0f;  // b_{T-1} = 1 (Thm 2: a_{T:T+1} = 1)
+    rl.issue(nch - 1); rf.issue(nch - 1);
+    rl.issue(nch - 2); rf.issue(nch - 2);
+    for (int64_t c = nch - 1; c >= 0; c--) {
+        rl.issue(c - 2); rf.issue(c - 2);
+        cp_async_wait<4>();
+        __syncwarp();
+        float* rows = rl.stage(c);
+        const float* frows = rf.stage(c);
+        const int n = (int)((T - c * kBsC < kBsC) ? T - c * kBsC : kBsC);
+        bs_prep<DP, false>(rows, mrow, n, D, j, h);
+        for (int i = n - 1; i >= 0; i--) {
+            const int64_t t = c * kBsC + i;
+            if (h == 0) {
+                out[(i + 1) * DP + j] = frows[i * DP + j] * bt;  // gam_t (unnormalised)
+                rows[i * DP + j] *= bt;                           // w = l_t o b_t (pads: 0)
+            }
+            __syncwarp();
+            if (t > 0) {  // b_{t-1} = A (l_t o b_t), renormalised by an exact power of two
+                float g[NV];
+                ld_vec<NV>(rows + i * DP + h * NV, g);
+                const float s = pow2_inv(hmax(tmax<NV>(g)));
+                float c0 = 0.0f, c1 = 0.0f, c2 = 0.0f, c3 = 0.0f;
+#pragma unroll
+                for (int k = 0; k < NV; k += 4) {
+                    c0 = fmaf(Arow[k], g[k], c0);
+                    c1 = fmaf(Arow[k + 1], g[k + 1], c1);
+                    c2 = fmaf(Arow[k + 2], g[k + 2], c2);
+                    c3 = fmaf(Arow[k + 3], g[k + 3], c3);
+                }
+                bt = hsum((c0 + c1) + (c2 + c3)) * s;
+            }
+        }
+        __syncwarp();
+        bool dummy = false;
+        float dl;
+        bs_flush<DP>(out + DP, n, smo + c * kBsC * D, D, j, h, inv, dummy, dl);
+    }
+    cp_async_wait<0>();
+    if (lane == 0) {
+        p.scalar_out[b] = logz;
+        int32_t inf = 0;
+        if (bad || logz != logz) inf = -1;
+        else if (zero_t >= 0) inf = (int32_t)(zero_t + 1);
+        if (raw < 1 || raw > p.T) inf = kInfoBadLength;
+        p.info[b] = inf;
+    }
+}
+
+template <int DP>
+__global__ void __launch_bounds__(kBsThreads) bs_viterbi_kernel(const BSParams p) {
+    using S = BsShape<DP>;
+    constexpr int H = S::H, NV = S::NV;
+    constexpr int SPB = kBsThreads / 32;
+    constexpr int RING = kBsStages * kBsC * DP;
+    constexpr int PER = RING + 2 * DP + kBsC + kBsChunk + kBsChunk * DP / 4;
+    extern __shared__ __align__(16) float bsm[];
+    const int lane = threadIdx.x % 32, grp = threadIdx.x / 32;
+    const int j = lane % DP, h = lane / DP;
+    float* rl_buf = bsm + (size_t)grp * PER;
+    float* xbuf = rl_buf + RING;                                     // [2][DP]
+    float* mrow = xbuf + 2 * DP;                                     // [C]
+    int32_t* spath = reinterpret_cast<int32_t*>(mrow + kBsC);        // [kBsChunk]
+    uint8_t* sbp = reinterpret_cast<uint8_t*>(spath + kBsChunk);     // [kBsChunk][DP]
+    const int64_t b = (int64_t)blockIdx.x * SPB + grp;
+    if (b >= p.B) return;
+    int64_t base, raw;
+    const int64_t T = seq_span(p.offsets, p.T, b, base, raw);
+    if (T < 1) {
+        if (lane == 0) { p.scalar_out[b] = 0.0; p.info[b] = kInfoBadLength; }
+        return;
+    }
+    const int D = p.D;
+    const bool act = j < D;
+    const float* la = p.log_A + b * p.A_stride;
+    float LA[NV];  // log A(i, j) for i in this lane's half
+#pragma unroll
+    for (int k = 0; k < NV; k++) {
+        const int i = h * NV + k;
+        LA[k] = (act && i < D) ? __ldg(la + i * D + j) : neg_inf();
+    }
+    const float lpv = act ? __ldg(p.log_pi + b * p.pi_stride + j) : neg_inf();
+    uint8_t* bp = p.bp + (size_t)b * p.T * DP;
+    bs_fill<DP>(rl_buf, RING + 2 * DP, neg_inf());
+    __syncwarp();
+    const BsRing<DP> rl{rl_buf, p.log_lik + base * D, T, D, j, h};
+    const int64_t nch = (T + kBsC - 1) / kBsC;
+
+    // ---------------- forward max-product pass with backpointers (Algorithm 4 lines 3-6)
+    double c = 0.0;  // accumulated offset: V_t = V~_t + c
+    int64_t zero_t = -1;
+    bool bad = false;
+    float V = neg_inf();
+    int par = 0;
+    rl.issue(0);
+    rl.issue(1);
+    for (int64_t ch = 0; ch < nch; ch++) {
+        rl.issue(ch + 2);
+        cp_async_wait<2>();
+        __syncwarp();
+        float* rows = rl.stage(ch);
+        const int n = (int)((T - ch * kBsC < kBsC) ? T - ch * kBsC : kBsC);
+        bad |= bs_prep<DP, true>(rows, mrow, n, D, j, h);
+        for (int i = 0; i < n; i++) {
+            const int64_t t = ch * kBsC + i;
+            const float w = rows[i * DP + j];
+            const float m = mrow[i];
+            if (t == 0) {
+                V = lpv + w;
+                c = (double)m;
+            } else {
+                float* xb = xbuf + par * DP;
+                par ^= 1;
+                if (h == 0) xb[j] = V;
+                __syncwarp();
+                float g[NV];
+                ld_vec<NV>(xb + h * NV, g);
+                float o = tmax<NV>(g);
+                if (H == 2) o = fmaxf(o, __shfl_xor_sync(0xffffffffu, o, 16));
+                if (!(o > neg_inf())) {
+                    if (zero_t < 0) zero_t = t - 1;
+                    o = 0.0f;
+                }
+                float sc[NV];
+#pragma unroll
+                for (int k = 0; k < NV; k++) sc[k] = (g[k] - o) + LA[k];
+                float best = tmax<NV>(sc);
+                int arg = first_argmax<NV>(sc, best) + h * NV;
+                if (H == 2) {  // the lower half wins ties (smallest index)
+                    const float bo = __shfl_xor_sync(0xffffffffu, best, 16);
+                    const int ao = __shfl_xor_sync(0xffffffffu, arg, 16);
+                    const float bl = h ? bo : best, bh = h ? best : bo;
+                    const int al = h ? ao : arg, ah = h ? arg : ao;
+                    best = fmaxf(bl, bh);
+                    arg = (bl == best) ? al : ah;
+                }
+                if (h == 0 && act) bp[t * DP + j] = (uint8_t)arg;
+                V = best + w;
+                c += (double)o + (double)m;
+            }
+        }
+        __syncwarp();
+    }
+    cp_async_wait<0>();
+    // x*_{T-1} = smallest argmax of V_{T-1}; log_prob = max V_{T-1}
+    int xs;
+    {
+        float* xb = xbuf + par * DP;
+        if (h == 0) xb[j] = V;
+        __syncwarp();
+        float g[DP];
+        ld_vec<DP>(xb, g);
+        float o = tmax<DP>(g);
+        xs = first_argmax<DP>(g, o);
+        if (!(o > neg_inf())) {
+            if (zero_t < 0) zero_t = T - 1;
+            o = 0.0f;
+            xs = 0;
+        }
+        c += (double)o;
+    }
+    __syncwarp();  // the backpointer stores are visible to all lanes
+    // ---------------- backtrack (Algorithm 4 lines 8-10), chunks of the backpointers staged in SMEM
+    int x = xs;
+    for (int64_t e = T; e > 0; e -= kBsChunk) {
+        const int64_t s0 = (e - kBsChunk > 0) ? e - kBsChunk : 0;
+        const int n = (int)(e - s0);
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(bp + s0 * DP);
+        uint32_t* dst = reinterpret_cast<uint32_t*>(sbp);
+        for (int q = lane; q < n * DP / 4; q += 32) dst[q] = src[q];
+        __syncwarp();
+        if (lane == 0) {
+            for (int i = n - 1; i >= 0; i--) {
+                spath[i] = x;
+                if (s0 + i > 0) x = sbp[i * DP + x];
+            }
+        }
+        __syncwarp();
+        for (int i = lane; i < n; i += 32) p.path[base + s0 + i] = spath[i];
+        __syncwarp();
+    }
+    if (lane == 0) {
+        p.scalar_out[b] = c;
+        int32_t inf = 0;
+        if (bad || c != c) inf = -1;
+        else if (zero_t >= 0) inf = (int32_t)(zero_t + 1);
+        if (raw < 1 || raw > p.T) inf = kInfoBadLength;
+        p.info[b] = inf;
+    }
+}
+
+size_t bs_smem(int DP, int op) {
+    const size_t ring = (size_t)kBsStages * kBsC * DP;
+    const size_t per = op == 0 ? 2 * ring + (size_t)(kBsC + 1) * DP + 2 * kBsC
+                               : ring + 2 * DP + kBsC + kBsChunk + (size_t)kBsChunk * DP / 4;
+    return per * 4 * (kBsThreads / 32);
+}
+
+cudaError_t launch_batchseq(int DP, int op, const BSParams& p, cudaStream_t s) {
+    const unsigned spb = kBsThreads / 32;  // one warp per sequence
+    const unsigned grid = (unsigned)((p.B + spb - 1) / spb);
+    const size_t sm = bs_smem(DP, op);
+    const void* k = nullptr;
+    if (DP == 16) k = op == 0 ? (const void*)bs_smooth_kernel<16> : (const void*)bs_viterbi_kernel<16>;
+    else if (DP == 32) k = op == 0 ? (const void*)bs_smooth_kernel<32> : (const void*)bs_viterbi_kernel<32>;
+    else return cudaErrorInvalidValue;
+    if (cudaError_t e = ensure_smem_optin(k, sm); e != cudaSuccess) return e;
+    if (DP == 16) {
+        if (op == 0) bs_smooth_kernel<16><<<grid, kBsThreads, sm, s>>>(p);
+        else bs_viterbi_kernel<16><<<grid, kBsThreads, sm, s>>>(p);
+    } else {
+        if (op == 0) bs_smooth_kernel<32><<<grid, kBsThreads, sm, s>>>(p);
+        else bs_viterbi_kernel<32><<<grid, kBsThreads, sm, s>>>(p);
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace hmm

@@ -39,4 +39,21 @@ struct LgParams {
     int64_t pi_stride, A_stride;
 };
 
+// Batch-parallel plan (hmm_batchseq.cu): one lane group per sequence, 9 <= D <= 32.
+struct BSParams {
+    int64_t T, B;
+    int D;
+    const float* log_pi;
+    const float* log_A;
+    const float* log_lik;
+    float* filtered;
+    float* smoothed;
+    int32_t* path;
+    double* scalar_out;
+    int32_t* info;
+    uint8_t* bp;  // [B][T][DP] Viterbi backpointers (workspace)
+    const int64_t* offsets;
+    int64_t pi_stride, A_stride;
+};
+
 }  // namespace hmm

@@ -1,0 +1,108 @@
+"""GPU parity of the batch-parallel plan for 9 <= D <= 32 (hmm_batchseq.cu): one lane
+group per sequence runs Algorithm 1's forward/backward passes and Algorithm 4's max-product pass with
+backpointers (the sequence is one block-wise element).
+Forced with hmm_debug_force_path(4) on small batches, compared with the fp64 oracle per sequence and
+with the block-scan plan (force 5) on the same inputs."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import workloads as W
+import paper_2102_05743_b200 as H
+from parity import TAU, TOL_MARG, TOL_REL, rel, check_smooth, check_viterbi
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(autouse=True, scope="module")
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    H.lib()
+
+
+def _run(wl, force):
+    d = torch.device("cuda")
+    lp, la, ll = (torch.from_numpy(np.ascontiguousarray(x)).to(d) for x in (wl.log_pi, wl.log_A, wl.log_lik))
+    H.force_path(force)
+    try:
+        f, s, lz, info = H.smooth(lp, la, ll)
+        p, q, vinfo = H.viterbi(lp, la, ll)
+        torch.cuda.synchronize()
+    finally:
+        H.force_path(0)
+    return [x.cpu().numpy() for x in (f, s, lz, info)], [x.cpu().numpy() for x in (p, q, vinfo)]
+
+
+@pytest.mark.parametrize("D", [9, 12, 16, 17, 25, 32])
+@pytest.mark.parametrize("T", [1, 2, 7, 1000, 4099])
+def test_batchseq_vs_oracle(D, T):
+    wl = W.dense_batch(5, D, T, model_seed=77 + D, seed0=31 * T)
+    wl.log_lik = wl.log_lik + W.random_potentials(D, T, seed=D, B=5, sigma=0.1).log_lik  # near-tie-free
+    s, v = _run(wl, 4)
+    for b in range(5):
+        check_smooth(wl, *s, b=b)
+        check_viterbi(wl, *v, b=b)
+
+
+@pytest.mark.parametrize("D", [16, 32])
+def test_batchseq_unnormalised_and_scan_agree(D):
+    wl = W.random_potentials(D, 3000, seed=4, B=3)
+    s4, v4 = _run(wl, 4)
+    s5, v5 = _run(wl, 5)
+    for b in range(3):
+        check_smooth(wl, *s4, b=b)
+        check_viterbi(wl, *v4, b=b)
+    assert float(np.abs(s4[1] - s5[1]).max()) <= 2 * TOL_MARG
+    assert float(np.max(np.abs(s4[2] - s5[2]) / np.abs(s5[2]))) <= 2 * TOL_REL
+
+
+def test_batchseq_info_codes():
+    wl = W.random_potentials(16, 2000, seed=9, B=4)
+    wl.log_lik[1, 777, :] = -np.inf
+    wl.log_lik[2, 5, 3] = np.nan
+    s, v = _run(wl, 4)
+    assert s[3].tolist() == [0, 778, -1, 0]
+    assert v[2].tolist() == [0, 778, -1, 0]
+
+
+def test_batchseq_is_the_auto_plan_for_config4_shape():
+    """B = 1024, D = 16: the planner takes the batch-parallel plan (config ④) — checked by comparing the
+    automatic result bitwise with the forced plan."""
+    wl = W.dense_batch(1024, 16, 256)
+    a, av = _run(wl, 0)
+    f, fv = _run(wl, 4)
+    np.testing.assert_array_equal(a[1], f[1])
+    np.testing.assert_array_equal(av[0], fv[0])
+    for b in (0, 100, 1023):
+        check_smooth(wl, *a, b=b)
+
+
+def test_batchseq_varlen_per_sequence_models():
+    rng = np.random.default_rng(2)
+    B, D = 200, 32
+    lengths = rng.integers(1, 1500, size=B)
+    models, lls = [], []
+    for b in range(B):
+        w = W.dense(D, int(lengths[b]), seed=b, model_seed=5000 + b)
+        models.append((w.log_pi, w.log_A)); lls.append(w.log_lik)
+    off = np.zeros(B + 1, np.int64); off[1:] = np.cumsum(lengths)
+    d = torch.device("cuda")
+    lp = torch.from_numpy(np.stack([m[0] for m in models])).to(d)
+    la = torch.from_numpy(np.stack([m[1] for m in models])).to(d)
+    ll = torch.from_numpy(np.concatenate(lls)).to(d)
+    o = torch.from_numpy(off).to(d)
+    f, s, lz, info = H.smooth_varlen(lp, la, ll, o, int(lengths.max()))   # D = 32, B >= 160: batch-parallel
+    p, q, vinfo = H.viterbi_varlen(lp, la, ll, o, int(lengths.max()))
+    torch.cuda.synchronize()
+    s, lz, p, q = s.cpu().numpy(), lz.cpu().numpy(), p.cpu().numpy(), q.cpu().numpy()
+    assert (info.cpu().numpy() == 0).all() and (vinfo.cpu().numpy() == 0).all()
+    for b in range(0, B, 13):
+        a, e = off[b], off[b + 1]
+        or_ = oracle.smooth(*models[b], lls[b])
+        assert float(np.abs(s[a:e] - or_["smoothed"]).max()) <= TOL_MARG
+        assert rel(float(lz[b]), or_["log_z"]) <= TOL_REL
+        v = oracle.viterbi(*models[b], lls[b])
+        assert rel(float(q[b]), v["log_prob"]) <= TOL_REL
+        assert rel(oracle.joint_weight(*models[b], lls[b], p[a:e]), v["log_prob"]) <= TOL_REL
