@@ -41,11 +41,18 @@ for r in data:
         "warp_instructions": f("smsp__inst_executed.sum"),
         "sm_ghz": f("sm__cycles_elapsed.avg.per_second"),
         "top_stalls_per_issue": top,
+        "pipe_active_pct": {h.split("__")[1].split(".")[0]: f(h) for h in hdr
+                            if ("pipe_tensor" in h or "pipe_fma_cycles" in h or "pipe_alu_cycles" in h
+                                or "pipe_fmaheavy_cycles" in h or "pipe_xu" in h)
+                            and h.endswith("pct_of_peak_sustained_active")},
     }
     if T:
         s["dram_bytes_per_step"] = (rd + wr) / T
         s["warp_instructions_per_step"] = s["warp_instructions"] / T
-    key = "smooth" if ", 0>" in name or "<4, 0>" in name else ("viterbi" if ", 1>" in name else name)
+    if "hmm_stream_kernel" in name:
+        key = "smooth" if ", 0>" in name else ("viterbi" if ", 1>" in name else name)
+    else:
+        key = name
     res[key] = s
     print(json.dumps(s, indent=1))
 if out:
