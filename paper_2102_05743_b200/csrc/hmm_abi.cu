@@ -250,7 +250,9 @@ struct LgPlan {
     int DP = 0;
     bool tc = false;  // sum-product leaf products on the tensor cores (DP = 64)
     int64_t SL = 0, NL = 0, NB = 0;
-    size_t o_sync, o_leaf, o_groot, o_bpre, o_bsuf, o_part, o_bp, o_lmap, o_bmap, o_bend, o_xstar, o_lik, total;
+    int64_t KG = 0, NG = 1;  // two-level carry: KG block roots per group, NG groups (NG = 1: one level)
+    size_t o_sync, o_leaf, o_groot, o_bpre, o_bsuf, o_part, o_bp, o_lmap, o_bmap, o_bend, o_xstar, o_lik;
+    size_t o_gprod, o_gpre, o_gsuf, total;
 };
 
 bool make_large_plan(int D, int op, int64_t T, int64_t B, LgPlan& P, bool allow_tc = true) {
@@ -276,6 +278,16 @@ bool make_large_plan(int D, int op, int64_t T, int64_t B, LgPlan& P, bool allow_
     P.SL = SL;
     P.NL = cdiv(T, SL);
     P.NB = cdiv(P.NL, NLB);
+    // The block-root carry chain is serial (~1 us per root at DP = 64): beyond 24 roots it runs in two
+    // levels, ~sqrt(NB / 2) roots per group (hmm_large.cu lg_group_kernel).
+    P.KG = P.NB;
+    P.NG = 1;
+    if (P.NB > 24) {  // group product ~2.5 us per root, chain steps ~0.9 us: KG ~ sqrt(NB / 2)
+        int64_t kg = 6;
+        while (2 * kg * kg < P.NB) kg++;
+        P.KG = kg;
+        P.NG = cdiv(P.NB, kg);
+    }
     const size_t DP2 = (size_t)P.DP * P.DP;
     size_t off = 0;
     auto take = [&](size_t bytes) { size_t o = off; off = (off + bytes + 255) & ~(size_t)255; return o; };
@@ -291,6 +303,9 @@ bool make_large_plan(int D, int op, int64_t T, int64_t B, LgPlan& P, bool allow_
     P.o_bend = take(op == 1 ? (size_t)B * P.NB * 4 : 0);
     P.o_xstar = take((size_t)B * 4);
     P.o_lik = take(P.tc ? (size_t)B * T * 64 * 4 : 0);
+    P.o_gprod = take(P.NG > 1 ? (size_t)B * P.NG * DP2 * 4 : 0);
+    P.o_gpre = take(P.NG > 1 ? (size_t)B * P.NG * P.DP * 4 : 0);
+    P.o_gsuf = take(P.NG > 1 ? (size_t)B * P.NG * P.DP * 4 : 0);
     P.total = off;
     return true;
 }
@@ -342,6 +357,10 @@ hmm_status_t run(int op, int D, int64_t T, int64_t B, const float* log_pi, const
         lp.bmap = w + G.o_bmap;
         lp.bend = reinterpret_cast<int32_t*>(w + G.o_bend);
         lp.xstar = reinterpret_cast<int32_t*>(w + G.o_xstar);
+        lp.KG = G.KG; lp.NG = G.NG;
+        lp.gprod = reinterpret_cast<float*>(w + G.o_gprod);
+        lp.gpre = reinterpret_cast<float*>(w + G.o_gpre);
+        lp.gsuf = reinterpret_cast<float*>(w + G.o_gsuf);
         lp.tc = G.tc ? 1 : 0;
         lp.lik = reinterpret_cast<float*>(w + G.o_lik);
         cudaError_t e = hmm::launch_large(G.DP, op, lp, static_cast<cudaStream_t>(stream));
@@ -557,6 +576,10 @@ hmm_status_t run_varlen(int op, int D, int64_t B, int64_t maxT, const int64_t* o
         lp.bmap = w + G.o_bmap;
         lp.bend = reinterpret_cast<int32_t*>(w + G.o_bend);
         lp.xstar = reinterpret_cast<int32_t*>(w + G.o_xstar);
+        lp.KG = G.KG; lp.NG = G.NG;
+        lp.gprod = reinterpret_cast<float*>(w + G.o_gprod);
+        lp.gpre = reinterpret_cast<float*>(w + G.o_gpre);
+        lp.gsuf = reinterpret_cast<float*>(w + G.o_gsuf);
         lp.tc = 0;
         lp.offsets = offsets; lp.pi_stride = pis; lp.A_stride = As;
         cudaError_t e = hmm::launch_large(G.DP, op, lp, s);

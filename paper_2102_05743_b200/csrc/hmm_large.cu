@@ -497,21 +497,37 @@ __device__ void lg_chain_bwd(const float* mats, int64_t nm, const float* w0, flo
 // sum-product only).  The chain is serial, so the roots stream through an NS-deep cp.async ring
 // (16-B chunks XOR-swizzled by row: both the column reads of the forward step and the row reads of
 // the backward step are bank-conflict-free) and every step is pure SMEM math on 64 threads.
+// Carry chain arguments: the chain runs over `roots` (n per sequence, `rstride` floats apart per
+// sequence); CTA (x = b * ng + g, y = dir) covers roots [g gs, min((g+1) gs, n)) starting from the entering
+// vector init_pre[b][g] / init_suf[b][g] (null: the boundary vector: 1 / 0 for max-plus), and writes the
+// carry entering every root to out_pre / out_suf ([b][root][DP]).
+struct LgChain {
+    const float* roots;
+    int64_t n, rstride, gs, ng;
+    const float* init_pre;
+    const float* init_suf;
+    float* out_pre;
+    float* out_suf;
+};
+
 template <int DP, int OP>
-__global__ void __launch_bounds__(64) lg_carry_kernel(const LgParams p) {
+__global__ void __launch_bounds__(64) lg_carry_kernel(const LgParams p, const LgChain ch) {
     constexpr bool MP = (OP == 1);
     constexpr int NS = 6;                 // ring depth (roots in flight)
     constexpr int CH = DP / 4;            // 16-B chunks per row
     extern __shared__ __align__(16) float ring[];  // [NS][DP*DP]
     __shared__ float vec[DP];
     __shared__ float red[2];
-    const int64_t b = blockIdx.x;
+    const int64_t b = blockIdx.x / ch.ng, g = blockIdx.x % ch.ng;
     const bool fwd = blockIdx.y == 0;
     if (!fwd && MP) return;
     const int tid = threadIdx.x, lane = tid & 31;
-    const int64_t NB = p.NB;
-    const float* roots = p.groot + (size_t)b * NB * DP * DP;
-    float* out = (fwd ? p.bpre : p.bsuf) + (size_t)b * NB * DP;
+    const int64_t lo = g * ch.gs, hi = (lo + ch.gs < ch.n) ? lo + ch.gs : ch.n;
+    const int64_t NB = hi - lo;
+    if (NB <= 0) return;
+    const float* roots = ch.roots + (size_t)b * ch.rstride + (size_t)lo * DP * DP;
+    float* out = (fwd ? ch.out_pre : ch.out_suf) + ((size_t)b * ch.n + lo) * DP;
+    const float* init = fwd ? ch.init_pre : ch.init_suf;
     auto sw = [&](int r, int c) -> int { return r * DP + ((c ^ (r & (CH - 1))) << 2); };  // chunk c of row r
     auto load = [&](int64_t i, int st) {
         if (i >= 0 && i < NB) {
@@ -524,7 +540,8 @@ __global__ void __launch_bounds__(64) lg_carry_kernel(const LgParams p) {
         }
         cp_async_commit();
     };
-    for (int j = tid; j < DP; j += 64) vec[j] = MP ? 0.0f : 1.0f;
+    for (int j = tid; j < DP; j += 64)
+        vec[j] = init ? init[((size_t)b * ch.ng + g) * DP + j] : (MP ? 0.0f : 1.0f);
     for (int s = 0; s < NS - 1; s++) load(fwd ? s : NB - 1 - s, s);
     __syncthreads();
     for (int64_t it = 0; it < NB; it++) {
@@ -566,6 +583,82 @@ __global__ void __launch_bounds__(64) lg_carry_kernel(const LgParams p) {
         if (tid < DP) vec[tid] = MP ? ((m > neg_inf()) ? y - m : y) : y * pow2_inv(m);
         // (the next iteration's barrier orders these writes before the reads)
     }
+}
+
+// Group products for the two-level carry (long root chains): group g of a sequence = block roots
+// [g KG, min((g+1) KG, NB)), multiplied in order (Def. 3 matrix product / Def. 5 max-plus product) and
+// renormalised after every product; one CTA of 256 threads per group, thread = 4 x 4 output tile,
+// roots double-buffered through SMEM by cp.async.  The carry chain then runs over NB / KG group
+// products, and the per-block carries inside a group from the group's carry.
+template <int DP, int OP>
+__global__ void __launch_bounds__(256) lg_group_kernel(const LgParams p, int64_t KG, int64_t NG, float* gprod) {
+    constexpr bool MP = (OP == 1);
+    constexpr int TR = DP / 16;  // output rows per thread (DP = 64: 4; 32: 2; 16: 1)
+    extern __shared__ __align__(16) float gsm[];  // C [DP][DP], R[2][DP][DP]
+    __shared__ float gred[8];
+    float* C = gsm;
+    const int64_t b = blockIdx.y, g = blockIdx.x;
+    const int64_t lo = g * KG, hi = (lo + KG < p.NB) ? lo + KG : p.NB;
+    const int tid = threadIdx.x;
+    const int r0 = (tid / 16) * TR, c0 = (tid % 16) * (DP / 16);
+    constexpr int TC = DP / 16;  // output columns per thread
+    const float* roots = p.groot + (size_t)b * p.NB * DP * DP;
+    auto load = [&](int64_t i, float* dst) {
+        if (i < hi) {
+            const float* src = roots + (size_t)i * DP * DP;
+            for (int q = tid; q < DP * DP / 4; q += 256) cp_async16(dst + 4 * q, src + 4 * q);
+        }
+        cp_async_commit();
+    };
+    load(lo, C);
+    load(lo + 1, gsm + DP * DP);
+    for (int64_t i = lo + 1; i < hi; i++) {
+        float* R = gsm + (size_t)(1 + ((i - lo - 1) & 1)) * DP * DP;
+        load(i + 1, gsm + (size_t)(1 + ((i - lo) & 1)) * DP * DP);
+        cp_async_wait<1>();
+        __syncthreads();
+        float acc[TR][TC];
+#pragma unroll
+        for (int r = 0; r < TR; r++)
+#pragma unroll
+            for (int c = 0; c < TC; c++) acc[r][c] = MP ? neg_inf() : 0.0f;
+#pragma unroll 8
+        for (int k = 0; k < DP; k++) {
+            float a[TR], bb[TC];
+#pragma unroll
+            for (int r = 0; r < TR; r++) a[r] = C[(r0 + r) * DP + k];
+#pragma unroll
+            for (int c = 0; c < TC; c++) bb[c] = R[k * DP + c0 + c];
+#pragma unroll
+            for (int r = 0; r < TR; r++)
+#pragma unroll
+                for (int c = 0; c < TC; c++)
+                    acc[r][c] = MP ? fmaxf(acc[r][c], a[r] + bb[c]) : fmaf(a[r], bb[c], acc[r][c]);
+        }
+        float m = acc[0][0];
+#pragma unroll
+        for (int r = 0; r < TR; r++)
+#pragma unroll
+            for (int c = 0; c < TC; c++) m = fmaxf(m, acc[r][c]);
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if ((tid & 31) == 0) gred[tid >> 5] = m;
+        __syncthreads();  // every thread has read C and R; the warp maxima are in place
+        m = gred[0];
+#pragma unroll
+        for (int w = 1; w < 8; w++) m = fmaxf(m, gred[w]);
+        const float sc = MP ? 0.0f : pow2_inv(m);
+#pragma unroll
+        for (int r = 0; r < TR; r++)
+#pragma unroll
+            for (int c = 0; c < TC; c++)
+                C[(r0 + r) * DP + c0 + c] = MP ? ((m > neg_inf()) ? acc[r][c] - m : acc[r][c]) : acc[r][c] * sc;
+        __syncthreads();
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+    float* dst = gprod + ((size_t)b * NG + g) * DP * DP;
+    for (int q = tid; q < DP * DP; q += 256) dst[q] = C[q];
 }
 
 // ------------------------------------------------------------------------------------------- K3
@@ -950,22 +1043,44 @@ __global__ void __launch_bounds__(256) lg_sweep_kernel(const LgParams p) {
 
 // ------------------------------------------------------------------------------------------- K4/K5
 __global__ void lg_resolve_kernel(const LgParams p, int DP) {
-    // one CTA per sequence: end state of every block = (F_{blk+1} o ... o F_{NB-1})(x*)
+    // one CTA per sequence: end state of every block = (F_{blk+1} o ... o F_{NB-1})(x*).  The block maps
+    // are staged in SMEM (coalesced, chunks of up to 32 KB from the end), so the serial composition runs
+    // on SMEM latency instead of one dependent global load per block.
+    __shared__ uint8_t smaps[32768];
+    __shared__ int xs;
     const int64_t b = blockIdx.x;
-    if (threadIdx.x != 0) return;
-    int x = p.xstar[b];
-    if (x < 0 || x >= DP) x = 0;
-    for (int64_t blk = p.NB - 1; blk >= 0; blk--) {
-        p.bend[b * p.NB + blk] = x;
-        x = p.bmap[((size_t)b * p.NB + blk) * DP + x];
+    const uint8_t* src = p.bmap + (size_t)b * p.NB * DP;
+    const int64_t cb = 32768 / DP;  // blocks per chunk
+    if (threadIdx.x == 0) {
+        int x = p.xstar[b];
+        xs = (x < 0 || x >= DP) ? 0 : x;
+    }
+    for (int64_t hi = p.NB; hi > 0; hi -= cb) {
+        const int64_t lo = hi - cb > 0 ? hi - cb : 0;
+        __syncthreads();
+        for (int64_t q = threadIdx.x; q < (hi - lo) * DP; q += blockDim.x) smaps[q] = src[lo * DP + q];
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int x = xs;
+            for (int64_t blk = hi - 1; blk >= lo; blk--) {
+                p.bend[b * p.NB + blk] = x;
+                x = smaps[(blk - lo) * DP + x];
+            }
+            xs = x;
+        }
     }
 }
 
 template <int DP>
 __global__ void __launch_bounds__(256) lg_backtrack_kernel(const LgParams p) {
+    // one thread per leaf backtracks through its backpointers (Alg. 4 lines 8-10) from the leaf's end
+    // state; the block's backpointer rows are staged in SMEM in chunks of 32 KB (from the end of the
+    // block's range), so each step of the serial walk is an SMEM load, not a dependent global one.
     using C = LG<DP>;
     constexpr int NLB = C::NLB;
+    constexpr int CHS = 32768 / DP;  // steps per chunk
     __shared__ int ends[NLB];
+    __shared__ __align__(16) uint8_t sbp[CHS * DP];
     const int64_t b = blockIdx.y;
     const int blk = blockIdx.x;
     int64_t sbase, T_raw;  // packed first row / length of sequence b (varlen batches, f4)
@@ -980,17 +1095,25 @@ __global__ void __launch_bounds__(256) lg_backtrack_kernel(const LgParams p) {
         }
     }
     __syncthreads();
-    // one thread per leaf backtracks through its backpointers
     const int q = threadIdx.x;
-    if (q < nleaf) {
-        const int64_t L = (int64_t)blk * NLB + q;
-        const int64_t a = L * p.SL;
-        const int n = (int)((T - a < p.SL) ? T - a : p.SL);
-        int x = ends[q];
-        for (int i = n - 1; i >= 0; i--) {
-            const int64_t t = a + i;
+    const int64_t la = ((int64_t)blk * NLB + q) * p.SL;                      // this thread's leaf
+    const int64_t lb = (q < nleaf) ? ((la + p.SL < T) ? la + p.SL : T) : la;
+    int x = (q < nleaf) ? ends[q] : 0;
+    const int64_t r0 = (int64_t)blk * NLB * p.SL;                             // the block's steps
+    int64_t r1 = r0 + (int64_t)nleaf * p.SL;
+    if (r1 > T) r1 = T;
+    const uint8_t* bpg = p.bp + (size_t)b * p.T * DP;
+    for (int64_t c1 = r1; c1 > r0; c1 -= CHS) {
+        const int64_t c0 = (c1 - CHS > r0) ? c1 - CHS : r0;
+        __syncthreads();
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(bpg + c0 * DP);
+        uint32_t* dst = reinterpret_cast<uint32_t*>(sbp);
+        for (int64_t w = threadIdx.x; w < (c1 - c0) * DP / 4; w += blockDim.x) dst[w] = src[w];
+        __syncthreads();
+        const int64_t hi = (lb < c1) ? lb : c1, lo = (la > c0) ? la : c0;
+        for (int64_t t = hi - 1; t >= lo; t--) {
             p.path[(size_t)sbase + t] = x;
-            x = p.bp[((size_t)b * p.T + t) * DP + x];
+            x = sbp[(t - c0) * DP + x];
         }
     }
 }
@@ -1045,11 +1168,24 @@ static cudaError_t lg_launch(const LgParams& p, cudaStream_t s) {
         if (cudaError_t e = ensure_smem_optin(reinterpret_cast<const void*>(lg_carry_kernel<DP, OP>), smc);
             e != cudaSuccess)
             return e;
-        lg_carry_kernel<DP, OP><<<dim3((unsigned)p.B, 2), 64, smc, s>>>(p);
+        if (p.NG <= 1) {  // one level: the chain over the NB block roots
+            const LgChain ch{p.groot, p.NB, p.NB * DP * DP, p.NB, 1, nullptr, nullptr, p.bpre, p.bsuf};
+            lg_carry_kernel<DP, OP><<<dim3((unsigned)p.B, 2), 64, smc, s>>>(p, ch);
+        } else {  // two levels: group products, the chain over them, then the chains inside the groups
+            const size_t smg = (size_t)3 * DP * DP * 4;
+            if (cudaError_t e = ensure_smem_optin(reinterpret_cast<const void*>(lg_group_kernel<DP, OP>), smg);
+                e != cudaSuccess)
+                return e;
+            lg_group_kernel<DP, OP><<<dim3((unsigned)p.NG, (unsigned)p.B), 256, smg, s>>>(p, p.KG, p.NG, p.gprod);
+            const LgChain top{p.gprod, p.NG, p.NG * DP * DP, p.NG, 1, nullptr, nullptr, p.gpre, p.gsuf};
+            lg_carry_kernel<DP, OP><<<dim3((unsigned)p.B, 2), 64, smc, s>>>(p, top);
+            const LgChain low{p.groot, p.NB, p.NB * DP * DP, p.KG, p.NG, p.gpre, p.gsuf, p.bpre, p.bsuf};
+            lg_carry_kernel<DP, OP><<<dim3((unsigned)(p.B * p.NG), 2), 64, smc, s>>>(p, low);
+        }
     }
     lg_sweep_kernel<DP, OP><<<grid, 256, sm3, s>>>(p);
     if (OP == 1) {
-        lg_resolve_kernel<<<(unsigned)p.B, 32, 0, s>>>(p, DP);
+        lg_resolve_kernel<<<(unsigned)p.B, 256, 0, s>>>(p, DP);
         lg_backtrack_kernel<DP><<<grid, 256, 0, s>>>(p);
     }
     lg_finalize_kernel<<<(unsigned)p.B, 256, 0, s>>>(p);

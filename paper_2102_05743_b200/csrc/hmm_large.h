@@ -37,6 +37,11 @@ struct LgParams {
     // variable-length batches / per-sequence models (see KParams in hmm_plan.h)
     const int64_t* offsets;
     int64_t pi_stride, A_stride;
+    // two-level carry (NG > 1): KG block roots per group, group products and their carries
+    int64_t KG, NG;
+    float* gprod;  // [B][NG][DP*DP]
+    float* gpre;   // [B][NG][DP]
+    float* gsuf;   // [B][NG][DP]
 };
 
 // Batch-parallel plan (hmm_batchseq.cu): one lane group per sequence, 9 <= D <= 32.
