@@ -768,19 +768,24 @@ __global__ void __launch_bounds__(256) lg_sweep_kernel(const LgParams p) {
 #pragma unroll
                 for (int c = 0; c < CPL; c++) ah[c] = pv[c] * l[c];
             } else {
+                // four partial sums per output: the recursion is latency-bound, and a single
+                // DP-long FMA chain per output was its critical path
+                float q[CPL][4];
+#pragma unroll
+                for (int c = 0; c < CPL; c++) q[c][0] = q[c][1] = q[c][2] = q[c][3] = 0.0f;
 #pragma unroll
                 for (int k4 = 0; k4 < DP; k4 += 4) {
                     const float4 x = *reinterpret_cast<const float4*>(vv + k4);
 #pragma unroll
                     for (int c = 0; c < CPL; c++) {
-                        ah[c] = fmaf(x.x, Acol[c][k4], ah[c]);
-                        ah[c] = fmaf(x.y, Acol[c][k4 + 1], ah[c]);
-                        ah[c] = fmaf(x.z, Acol[c][k4 + 2], ah[c]);
-                        ah[c] = fmaf(x.w, Acol[c][k4 + 3], ah[c]);
+                        q[c][0] = fmaf(x.x, Acol[c][k4], q[c][0]);
+                        q[c][1] = fmaf(x.y, Acol[c][k4 + 1], q[c][1]);
+                        q[c][2] = fmaf(x.z, Acol[c][k4 + 2], q[c][2]);
+                        q[c][3] = fmaf(x.w, Acol[c][k4 + 3], q[c][3]);
                     }
                 }
 #pragma unroll
-                for (int c = 0; c < CPL; c++) ah[c] *= l[c];
+                for (int c = 0; c < CPL; c++) ah[c] = ((q[c][0] + q[c][1]) + (q[c][2] + q[c][3])) * l[c];
             }
             float cs = 0.0f;
 #pragma unroll
@@ -871,20 +876,22 @@ __global__ void __launch_bounds__(256) lg_sweep_kernel(const LgParams p) {
                     for (int c = 0; c < CPL; c++) vv[cl * CPL + c] = ex2((v[c] - m) * kLog2e) * bt[c];
                 }
                 __syncwarp();
-                float y[CPL];
+                float y[CPL], q[CPL][4];
 #pragma unroll
-                for (int c = 0; c < CPL; c++) y[c] = 0.0f;
+                for (int c = 0; c < CPL; c++) q[c][0] = q[c][1] = q[c][2] = q[c][3] = 0.0f;
 #pragma unroll
                 for (int k4 = 0; k4 < DP; k4 += 4) {
                     const float4 x = *reinterpret_cast<const float4*>(vv + k4);
 #pragma unroll
                     for (int c = 0; c < CPL; c++) {
-                        y[c] = fmaf(Arow[c][k4], x.x, y[c]);
-                        y[c] = fmaf(Arow[c][k4 + 1], x.y, y[c]);
-                        y[c] = fmaf(Arow[c][k4 + 2], x.z, y[c]);
-                        y[c] = fmaf(Arow[c][k4 + 3], x.w, y[c]);
+                        q[c][0] = fmaf(Arow[c][k4], x.x, q[c][0]);
+                        q[c][1] = fmaf(Arow[c][k4 + 1], x.y, q[c][1]);
+                        q[c][2] = fmaf(Arow[c][k4 + 2], x.z, q[c][2]);
+                        q[c][3] = fmaf(Arow[c][k4 + 3], x.w, q[c][3]);
                     }
                 }
+#pragma unroll
+                for (int c = 0; c < CPL; c++) y[c] = (q[c][0] + q[c][1]) + (q[c][2] + q[c][3]);
                 float mx = y[0];
 #pragma unroll
                 for (int c = 1; c < CPL; c++) mx = fmaxf(mx, y[c]);
@@ -967,17 +974,17 @@ __global__ void __launch_bounds__(256) lg_sweep_kernel(const LgParams p) {
                 }
             } else {
 #pragma unroll
-            for (int k = 0; k < DP; k++) {
-                const float vk = vv[k];
+                for (int k = 0; k < DP; k++) {
+                    const float vk = vv[k];
 #pragma unroll
-                for (int c = 0; c < CPL; c++) {
-                    const float sc = vk + ((t == 0) ? lpv[c] : LAc[c][k]);
-                    if (sc > best[c]) {
-                        best[c] = sc;
-                        arg[c] = k;
+                    for (int c = 0; c < CPL; c++) {
+                        const float sc = vk + ((t == 0) ? lpv[c] : LAc[c][k]);
+                        if (sc > best[c]) {
+                            best[c] = sc;
+                            arg[c] = k;
+                        }
                     }
                 }
-            }
             }
             float o = neg_inf(), Vn[CPL];
 #pragma unroll
