@@ -145,3 +145,13 @@ def test_varlen_impossible_step_per_sequence():
     res = _run(4, models, lls, off, True)
     f, s, lz, info, path, lpr, vinfo = res
     assert info.tolist() == [0, 124, 0] and vinfo.tolist() == [0, 124, 0]
+
+
+@pytest.mark.parametrize("D", [2, 4, 8])
+def test_varlen_long_sequences_chunked(D):
+    """D <= 8 runs one CTA per sequence: a long member (T = 400 003) takes the chunked resident plan
+    (many chunks per CTA, chunk roots and backpointers in the workspace) next to short members."""
+    lengths = [400_003, 17, 65_537, 1]
+    models, lls, off = _batch(D, lengths, seed=40 + D, per_seq=True)
+    res = _run(D, models, lls, off, True)
+    _check(models, lls, off, res, True)
