@@ -472,11 +472,17 @@ def main():
     with ClockSampler(local) as clk:
         for k in range(args.steps):
             flush_l2()
+            torch.cuda.nvtx.range_push(f"step{k}")  # NVTX ranges for nsys / ncu timelines
             ev[k][0].record(stream)
+            torch.cuda.nvtx.range_push("hmm_smooth")
             H.smooth(lp, la, ll, out=out_s, ws=ws_s)
+            torch.cuda.nvtx.range_pop()
             ev[k][1].record(stream)
+            torch.cuda.nvtx.range_push("hmm_viterbi")
             H.viterbi(lp, la, ll, out=out_v, ws=ws_v)
+            torch.cuda.nvtx.range_pop()
             ev[k][2].record(stream)
+            torch.cuda.nvtx.range_pop()
         torch.cuda.synchronize()
         # keep sampling a little longer on very short regions
         if len(clk.samples) < 5:

@@ -25,6 +25,19 @@ from . import HmmError, _check, _ptr, _stream, lib
 RECORD_BYTES = 16
 
 
+class _nvtx:
+    """NVTX range around a phase (visible in nsys / ncu timelines; a host-side marker, no device work)."""
+
+    def __init__(self, name):
+        self.name = name
+
+    def __enter__(self):
+        torch.cuda.nvtx.range_push(self.name)
+
+    def __exit__(self, *a):
+        torch.cuda.nvtx.range_pop()
+
+
 def partition(T: int, world: int, rank: int, align: int = 8) -> tuple[int, int]:
     """Contiguous slices with boundaries on multiples of `align` (16-B aligned slices for the bulk
     copies); if that would leave a rank empty, an unaligned equal split.  Returns (t_base, T_local)."""
@@ -207,15 +220,20 @@ def smooth_viterbi_dist(log_pi, log_A, log_lik_local, t_base: int, group=None, b
     (filtered, smoothed, log_z [1], info [1], path, log_prob [1], vinfo [1]) for the local slice."""
     be = _backend(backend)
     rank, world = dist.get_rank(group), dist.get_world_size(group)
-    s_agg, s_i1 = be.smooth_reduce(log_pi, log_A, log_lik_local, t_base)
-    v_agg, v_i1 = be.viterbi_reduce(log_pi, log_A, log_lik_local, t_base)
+    with _nvtx("hmm.reduce"):
+        s_agg, s_i1 = be.smooth_reduce(log_pi, log_A, log_lik_local, t_base)
+        v_agg, v_i1 = be.viterbi_reduce(log_pi, log_A, log_lik_local, t_base)
     na = s_agg.numel()
-    both = _all_gather(torch.cat([s_agg.view(-1), v_agg.view(-1)]), group).view(world, 2 * na)
+    with _nvtx("hmm.allgather.aggregates"):
+        both = _all_gather(torch.cat([s_agg.view(-1), v_agg.view(-1)]), group).view(world, 2 * na)
     s_all = both[:, :na].contiguous().view(-1)
     v_all = both[:, na:].contiguous().view(-1)
-    filt, sm, lzp, s_i2 = be.smooth_finish(log_pi, log_A, log_lik_local, t_base, s_all, rank, world)
-    rec, lpp, v_i2 = be.viterbi_forward(log_pi, log_A, log_lik_local, t_base, v_all, rank, world)
-    g = _all_gather(be.pack(rec, lzp, lpp, s_i1, s_i2, v_i1, v_i2), group)
-    rec_all, log_z, log_prob, info, vinfo = be.combine(g, world)
-    path, _ = be.viterbi_finish(log_pi, log_A, log_lik_local, t_base, rec_all, rank, world)
+    with _nvtx("hmm.finish"):
+        filt, sm, lzp, s_i2 = be.smooth_finish(log_pi, log_A, log_lik_local, t_base, s_all, rank, world)
+        rec, lpp, v_i2 = be.viterbi_forward(log_pi, log_A, log_lik_local, t_base, v_all, rank, world)
+    with _nvtx("hmm.allgather.records"):
+        g = _all_gather(be.pack(rec, lzp, lpp, s_i1, s_i2, v_i1, v_i2), group)
+        rec_all, log_z, log_prob, info, vinfo = be.combine(g, world)
+    with _nvtx("hmm.backtrack"):
+        path, _ = be.viterbi_finish(log_pi, log_A, log_lik_local, t_base, rec_all, rank, world)
     return filt, sm, log_z, info, path, log_prob, vinfo
