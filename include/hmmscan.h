@@ -235,7 +235,9 @@ hmm_status_t hmm_viterbi_path_elements(int D, int64_t T, int64_t B, const float*
  * the phases the CALLER all-gathers small fixed-size blobs (e.g. torch.distributed
  * all_gather_into_tensor over NCCL/NVLink) into rank order.  All phases of one rank must use the same
  * workspace (hmm_dist_workspace_size bytes, zero-filled once), on the same stream, in order.
- * Supported for 1 <= D <= 8 and a single sequence.
+ * Supported for a single sequence: the smoother for 1 <= D <= 64, the Viterbi for 1 <= D <= 8 (its rank
+ * records are 16-byte maps; D > 8 -> HMM_ERR_UNSUPPORTED).  hmm_dist_agg_bytes(D) is align16(D*D*4) for
+ * D <= 8 and DP*DP*4 (DP = 16, 32 or 64, the padded state count) for D > 8.
  *
  * Smoother (Algorithm 3 across ranks; the rank aggregate is the ordered product of the rank's
  * elements, Def. 3 / PAPER.md:281-290):

@@ -252,7 +252,7 @@ struct LgPlan {
     int64_t SL = 0, NL = 0, NB = 0;
     int64_t KG = 0, NG = 1;  // two-level carry: KG block roots per group, NG groups (NG = 1: one level)
     size_t o_sync, o_leaf, o_groot, o_bpre, o_bsuf, o_part, o_bp, o_lmap, o_bmap, o_bend, o_xstar, o_lik;
-    size_t o_gprod, o_gpre, o_gsuf, total;
+    size_t o_gprod, o_gpre, o_gsuf, o_rcar, total;
 };
 
 bool make_large_plan(int D, int op, int64_t T, int64_t B, LgPlan& P, bool allow_tc = true) {
@@ -306,6 +306,7 @@ bool make_large_plan(int D, int op, int64_t T, int64_t B, LgPlan& P, bool allow_
     P.o_gprod = take(P.NG > 1 ? (size_t)B * P.NG * DP2 * 4 : 0);
     P.o_gpre = take(P.NG > 1 ? (size_t)B * P.NG * P.DP * 4 : 0);
     P.o_gsuf = take(P.NG > 1 ? (size_t)B * P.NG * P.DP * 4 : 0);
+    P.o_rcar = take((size_t)2 * P.DP * 4);  // split-phase rank carries
     P.total = off;
     return true;
 }
@@ -327,14 +328,23 @@ hmm_status_t run(int op, int D, int64_t T, int64_t B, const float* log_pi, const
                  size_t ws_bytes, void* stream, const DistArgs& da = DistArgs()) {
     if (D < 1 || T < 1 || B < 1 || B > 65535) return HMM_ERR_INVALID_VALUE;
     if (D > HMM_MAX_D) return HMM_ERR_UNSUPPORTED;
-    if (D > 8 && da.mode != hmm::HMM_MODE_FULL) return HMM_ERR_UNSUPPORTED;  // split phase: D <= 8
+    // split phase at D > 8: the smoother on one sequence (reduce / finish); the Viterbi records are D <= 8
+    if (D > 8 && da.mode != hmm::HMM_MODE_FULL &&
+        (op != 0 || B != 1 || (da.mode != hmm::HMM_MODE_REDUCE && da.mode != hmm::HMM_MODE_SFINISH)))
+        return HMM_ERR_UNSUPPORTED;
     if (D > 8) {
-        if (!log_pi || !log_A || !log_lik || !scalar || !info) return HMM_ERR_INVALID_VALUE;
-        if (op == 0 && !smoothed) return HMM_ERR_INVALID_VALUE;
+        const bool ldist = da.mode != hmm::HMM_MODE_FULL;
+        const bool lreduce = da.mode == hmm::HMM_MODE_REDUCE;
+        if (!log_pi || !log_A || !log_lik || (!lreduce && !scalar) || !info) return HMM_ERR_INVALID_VALUE;
+        if (op == 0 && !lreduce && !smoothed) return HMM_ERR_INVALID_VALUE;
         if (op == 1 && !path) return HMM_ERR_INVALID_VALUE;
-        if (op == 0 && !filtered) return HMM_ERR_UNSUPPORTED;  // large-D smoother stages alpha in `filtered`
-        if (!al4(log_pi) || !al4(log_A) || !al4(log_lik) || !al8(scalar) || !al4(info)) return HMM_ERR_INVALID_VALUE;
-        if (use_batchseq(D, op, B))
+        if (op == 0 && !lreduce && !filtered) return HMM_ERR_UNSUPPORTED;  // large-D smoother stages alpha in `filtered`
+        if (!al4(log_pi) || !al4(log_A) || !al4(log_lik) || (scalar && !al8(scalar)) || !al4(info))
+            return HMM_ERR_INVALID_VALUE;
+        if (ldist && (da.world < 1 || da.rank < 0 || da.rank >= da.world || da.t_base < 0 ||
+                      (lreduce && !da.agg_out) || (!lreduce && !da.agg_all)))
+            return HMM_ERR_INVALID_VALUE;
+        if (!ldist && use_batchseq(D, op, B))
             return run_batchseq(op, D, T, B, nullptr, 0, 0, log_pi, log_A, log_lik, filtered, smoothed, path, scalar,
                                 info, ws, ws_bytes, stream);
         LgPlan G;
@@ -361,6 +371,9 @@ hmm_status_t run(int op, int D, int64_t T, int64_t B, const float* log_pi, const
         lp.gprod = reinterpret_cast<float*>(w + G.o_gprod);
         lp.gpre = reinterpret_cast<float*>(w + G.o_gpre);
         lp.gsuf = reinterpret_cast<float*>(w + G.o_gsuf);
+        lp.rcar = reinterpret_cast<float*>(w + G.o_rcar);
+        lp.mode = da.mode; lp.t_base = da.t_base; lp.rank = da.rank; lp.world = da.world;
+        lp.agg_all = da.agg_all; lp.agg_out = da.agg_out;
         lp.tc = G.tc ? 1 : 0;
         lp.lik = reinterpret_cast<float*>(w + G.o_lik);
         cudaError_t e = hmm::launch_large(G.DP, op, lp, static_cast<cudaStream_t>(stream));
@@ -737,12 +750,21 @@ hmm_status_t hmm_viterbi(int D, int64_t T, const float* log_pi, const float* log
                workspace_bytes, stream);
 }
 
-size_t hmm_dist_agg_bytes(int D) { return (D < 1 || D > 8) ? 0 : hmm::align16((size_t)D * D * 4); }
+size_t hmm_dist_agg_bytes(int D) {
+    if (D < 1 || D > HMM_MAX_D) return 0;
+    if (D <= 8) return hmm::align16((size_t)D * D * 4);
+    const size_t DP = D <= 16 ? 16 : (D <= 32 ? 32 : 64);  // large-D aggregates: padded DP x DP floats
+    return DP * DP * 4;
+}
 
 size_t hmm_dist_record_bytes(void) { return 16; }
 
 size_t hmm_dist_workspace_size(int op, int D, int64_t T_local) {
-    if ((op != 0 && op != 1) || D < 1 || D > 8 || T_local < 1) return 0;
+    if ((op != 0 && op != 1) || D < 1 || D > HMM_MAX_D || T_local < 1) return 0;
+    if (D > 8) {  // split phase at D > 8: smoother only
+        LgPlan G;
+        return (op == 0 && make_large_plan(D, 0, T_local, 1, G)) ? G.total : 0;
+    }
     Plan P;
     if (!make_plan(D, op, T_local, 1, P, true)) return 0;
     size_t w = P.ws_total;

@@ -207,8 +207,8 @@ __global__ void __launch_bounds__(256) lg_leaf_kernel(const LgParams p) {
                     if (act) {
     #pragma unroll
                         for (int rp = 0; rp < NRP; rp++) {
-                            const float a0 = (t == 0) ? pv[0] : Acol[0][2 * rp];
-                            const float a1 = (t == 0) ? pv[0] : Acol[0][2 * rp + 1];
+                            const float a0 = (p.t_base + t == 0) ? pv[0] : Acol[0][2 * rp];
+                            const float a1 = (p.t_base + t == 0) ? pv[0] : Acol[0][2 * rp + 1];
                             *reinterpret_cast<float2*>(Pm + rp * 2 * DP + 2 * cl) =
                                 MP ? make_float2(a0 + l[0], a1 + l[0]) : make_float2(a0 * l[0], a1 * l[0]);
                         }
@@ -261,7 +261,7 @@ __global__ void __launch_bounds__(256) lg_leaf_kernel(const LgParams p) {
                     for (int r = 0; r < DP; r++)
     #pragma unroll
                         for (int c = 0; c < CPL; c++) {
-                            const float a = (t == 0) ? pv[c] : Acol[c][r];
+                            const float a = (p.t_base + t == 0) ? pv[c] : Acol[c][r];
                             Pm[r * DP + cl * CPL + c] = MP ? a + l[c] : a * l[c];
                         }
                 }
@@ -591,18 +591,19 @@ __global__ void __launch_bounds__(64) lg_carry_kernel(const LgParams p, const Lg
 // roots double-buffered through SMEM by cp.async.  The carry chain then runs over NB / KG group
 // products, and the per-block carries inside a group from the group's carry.
 template <int DP, int OP>
-__global__ void __launch_bounds__(256) lg_group_kernel(const LgParams p, int64_t KG, int64_t NG, float* gprod) {
+__global__ void __launch_bounds__(256) lg_group_kernel(const LgParams p, const float* groot, int64_t NR, int64_t KG,
+                                                       int64_t NG, float* gprod) {
     constexpr bool MP = (OP == 1);
     constexpr int TR = DP / 16;  // output rows per thread (DP = 64: 4; 32: 2; 16: 1)
     extern __shared__ __align__(16) float gsm[];  // C [DP][DP], R[2][DP][DP]
     __shared__ float gred[8];
     float* C = gsm;
     const int64_t b = blockIdx.y, g = blockIdx.x;
-    const int64_t lo = g * KG, hi = (lo + KG < p.NB) ? lo + KG : p.NB;
+    const int64_t lo = g * KG, hi = (lo + KG < NR) ? lo + KG : NR;
     const int tid = threadIdx.x;
     const int r0 = (tid / 16) * TR, c0 = (tid % 16) * (DP / 16);
     constexpr int TC = DP / 16;  // output columns per thread
-    const float* roots = p.groot + (size_t)b * p.NB * DP * DP;
+    const float* roots = groot + (size_t)b * NR * DP * DP;
     auto load = [&](int64_t i, float* dst) {
         if (i < hi) {
             const float* src = roots + (size_t)i * DP * DP;
@@ -764,7 +765,7 @@ __global__ void __launch_bounds__(256) lg_sweep_kernel(const LgParams p) {
                 l[c] = ex2((v[c] - m) * kLog2e);
                 ah[c] = 0.0f;
             }
-            if (t == 0) {
+            if (p.t_base + t == 0) {
 #pragma unroll
                 for (int c = 0; c < CPL; c++) ah[c] = pv[c] * l[c];
             } else {
@@ -791,7 +792,7 @@ __global__ void __launch_bounds__(256) lg_sweep_kernel(const LgParams p) {
 #pragma unroll
             for (int c = 0; c < CPL; c++) cs += ah[c];
             cs = grp_sum<LPL>(cs);
-            if (act && !(cs > 0.0f) && t < zero_t) zero_t = t;
+            if (act && !(cs > 0.0f) && p.t_base + t < zero_t) zero_t = p.t_base + t;
             const float r = rcp(cs);
             __syncwarp();
             if (act) {  // a shorter half-warp leaf keeps its final state while its partner runs on
@@ -959,10 +960,10 @@ __global__ void __launch_bounds__(256) lg_sweep_kernel(const LgParams p) {
 #pragma unroll
                 for (int k4 = 0; k4 < DP; k4 += 4) {
                     const float4 x = *reinterpret_cast<const float4*>(vv + k4);
-                    sc[k4] = x.x + ((t == 0) ? lpv[0] : LAc[0][k4]);
-                    sc[k4 + 1] = x.y + ((t == 0) ? lpv[0] : LAc[0][k4 + 1]);
-                    sc[k4 + 2] = x.z + ((t == 0) ? lpv[0] : LAc[0][k4 + 2]);
-                    sc[k4 + 3] = x.w + ((t == 0) ? lpv[0] : LAc[0][k4 + 3]);
+                    sc[k4] = x.x +  ((p.t_base + t == 0) ? lpv[0] : LAc[0][k4]);
+                    sc[k4 + 1] = x.y +  ((p.t_base + t == 0) ? lpv[0] : LAc[0][k4 + 1]);
+                    sc[k4 + 2] = x.z +  ((p.t_base + t == 0) ? lpv[0] : LAc[0][k4 + 2]);
+                    sc[k4 + 3] = x.w +  ((p.t_base + t == 0) ? lpv[0] : LAc[0][k4 + 3]);
                 }
                 const float bm = vmax_tree<DP>(sc);
                 int a = 0;
@@ -978,7 +979,7 @@ __global__ void __launch_bounds__(256) lg_sweep_kernel(const LgParams p) {
                     const float vk = vv[k];
 #pragma unroll
                     for (int c = 0; c < CPL; c++) {
-                        const float sc = vk + ((t == 0) ? lpv[c] : LAc[c][k]);
+                        const float sc = vk + ((p.t_base + t == 0) ? lpv[c] : LAc[c][k]);
                         if (sc > best[c]) {
                             best[c] = sc;
                             arg[c] = k;
@@ -994,7 +995,7 @@ __global__ void __launch_bounds__(256) lg_sweep_kernel(const LgParams p) {
             }
             o = grp_max<LPL>(o);
             if (!(o > neg_inf())) {
-                if (act && t < zero_t) zero_t = t;
+                if (act && p.t_base + t < zero_t) zero_t = p.t_base + t;
                 o = 0.0f;
             }
             if (act && cl == 0) acc += (double)(o + m);
@@ -1155,6 +1156,48 @@ __global__ void lg_finalize_kernel(const LgParams p) {
 }
 
 // ------------------------------------------------------------------------------------------- host
+// Split phase: the carries entering and leaving this rank's slice from the gathered rank aggregates
+// (one CTA, DP threads): forward = 1^T Agg_0 ... Agg_{rank-1}, backward = Agg_{rank+1} ... Agg_{W-1} 1,
+// each step renormalised by an exact power of two (Thms 1-2 across ranks).
+template <int DP>
+__global__ void __launch_bounds__(DP) lg_rank_carry_kernel(const LgParams p) {
+    __shared__ float u[DP], w[DP];
+    __shared__ float red[DP];
+    const int j = threadIdx.x;
+    u[j] = 1.0f;
+    w[j] = 1.0f;
+    __syncthreads();
+    auto renorm = [&](float y, float* dst) {
+        red[j] = y;
+        __syncthreads();
+        float m = 0.0f;
+        for (int k = 0; k < DP; k++) m = fmaxf(m, red[k]);
+        __syncthreads();
+        dst[j] = y * pow2_inv(m);
+        __syncthreads();
+    };
+    for (int q = 0; q < p.rank; q++) {  // u <- u Agg_q
+        const float* M = p.agg_all + (size_t)q * DP * DP;
+        float y = 0.0f;
+        for (int k = 0; k < DP; k++) y = fmaf(u[k], __ldg(M + k * DP + j), y);
+        renorm(y, u);
+    }
+    for (int q = p.world - 1; q > p.rank; q--) {  // w <- Agg_q w
+        const float* M = p.agg_all + (size_t)q * DP * DP;
+        float y = 0.0f;
+        for (int k = 0; k < DP; k++) y = fmaf(__ldg(M + j * DP + k), w[k], y);
+        renorm(y, w);
+    }
+    p.rcar[j] = u[j];
+    p.rcar[DP + j] = w[j];
+}
+// Split-phase reduce: input errors (NaN / +inf seen by the leaf kernels) -> info, flag cleared.
+__global__ void lg_reduce_info_kernel(const LgParams p) {
+    uint32_t* bad = reinterpret_cast<uint32_t*>(p.ws_sync) + 8;
+    const uint32_t f = atomicExch(bad, 0u);
+    p.info[0] = f ? -1 : 0;
+}
+
 template <int DP, int OP>
 static cudaError_t lg_launch(const LgParams& p, cudaStream_t s) {
     using C = LG<DP>;
@@ -1165,26 +1208,43 @@ static cudaError_t lg_launch(const LgParams& p, cudaStream_t s) {
     if (cudaError_t e = ensure_smem_optin(reinterpret_cast<const void*>(lg_sweep_kernel<DP, OP>), sm3); e != cudaSuccess)
         return e;
     const dim3 grid((unsigned)p.NB, (unsigned)p.B);
-    if (OP == 0 && DP == 64 && p.tc) {
-        cudaError_t e = launch_large_tc_leaf(p, p.lik, s);
-        if (e != cudaSuccess) return e;
+    const size_t smg = (size_t)3 * DP * DP * 4;
+    if (cudaError_t e = ensure_smem_optin(reinterpret_cast<const void*>(lg_group_kernel<DP, OP>), smg); e != cudaSuccess)
+        return e;
+    const bool do_leaf = (p.mode == HMM_MODE_FULL || p.mode == HMM_MODE_REDUCE);
+    if (do_leaf) {
+        if (OP == 0 && DP == 64 && p.tc) {
+            cudaError_t e = launch_large_tc_leaf(p, p.lik, s);
+            if (e != cudaSuccess) return e;
+        }
+        lg_leaf_kernel<DP, OP><<<grid, 256, sm1, s>>>(p);
+        if (p.NG > 1)  // group products (also the first level of the rank aggregate)
+            lg_group_kernel<DP, OP><<<dim3((unsigned)p.NG, (unsigned)p.B), 256, smg, s>>>(p, p.groot, p.NB, p.KG, p.NG,
+                                                                                          p.gprod);
     }
-    lg_leaf_kernel<DP, OP><<<grid, 256, sm1, s>>>(p);
+    if (p.mode == HMM_MODE_REDUCE) {  // the rank aggregate = the ordered product of every block root
+        if (p.NG > 1) lg_group_kernel<DP, OP><<<dim3(1, 1), 256, smg, s>>>(p, p.gprod, p.NG, p.NG, 1, p.agg_out);
+        else lg_group_kernel<DP, OP><<<dim3(1, 1), 256, smg, s>>>(p, p.groot, p.NB, p.NB, 1, p.agg_out);
+        lg_reduce_info_kernel<<<1, 1, 0, s>>>(p);
+        return cudaGetLastError();
+    }
+    const float* init_pre = nullptr;
+    const float* init_suf = nullptr;
+    if (p.mode == HMM_MODE_SFINISH) {
+        lg_rank_carry_kernel<DP><<<1, DP, 0, s>>>(p);
+        init_pre = p.rcar;
+        init_suf = p.rcar + DP;
+    }
     {
         const size_t smc = (size_t)6 * DP * DP * 4;
         if (cudaError_t e = ensure_smem_optin(reinterpret_cast<const void*>(lg_carry_kernel<DP, OP>), smc);
             e != cudaSuccess)
             return e;
         if (p.NG <= 1) {  // one level: the chain over the NB block roots
-            const LgChain ch{p.groot, p.NB, p.NB * DP * DP, p.NB, 1, nullptr, nullptr, p.bpre, p.bsuf};
+            const LgChain ch{p.groot, p.NB, p.NB * DP * DP, p.NB, 1, init_pre, init_suf, p.bpre, p.bsuf};
             lg_carry_kernel<DP, OP><<<dim3((unsigned)p.B, 2), 64, smc, s>>>(p, ch);
-        } else {  // two levels: group products, the chain over them, then the chains inside the groups
-            const size_t smg = (size_t)3 * DP * DP * 4;
-            if (cudaError_t e = ensure_smem_optin(reinterpret_cast<const void*>(lg_group_kernel<DP, OP>), smg);
-                e != cudaSuccess)
-                return e;
-            lg_group_kernel<DP, OP><<<dim3((unsigned)p.NG, (unsigned)p.B), 256, smg, s>>>(p, p.KG, p.NG, p.gprod);
-            const LgChain top{p.gprod, p.NG, p.NG * DP * DP, p.NG, 1, nullptr, nullptr, p.gpre, p.gsuf};
+        } else {  // two levels: the chain over the group products, then the chains inside the groups
+            const LgChain top{p.gprod, p.NG, p.NG * DP * DP, p.NG, 1, init_pre, init_suf, p.gpre, p.gsuf};
             lg_carry_kernel<DP, OP><<<dim3((unsigned)p.B, 2), 64, smc, s>>>(p, top);
             const LgChain low{p.groot, p.NB, p.NB * DP * DP, p.KG, p.NG, p.gpre, p.gsuf, p.bpre, p.bsuf};
             lg_carry_kernel<DP, OP><<<dim3((unsigned)(p.B * p.NG), 2), 64, smc, s>>>(p, low);

@@ -42,6 +42,14 @@ struct LgParams {
     float* gprod;  // [B][NG][DP*DP]
     float* gpre;   // [B][NG][DP]
     float* gsuf;   // [B][NG][DP]
+    // split-phase distributed smoother (B = 1; hmm_plan.h HMM_MODE_*): this rank's global offset, the
+    // gathered rank aggregates (DP x DP floats each), the rank aggregate out, the rank carries [2][DP]
+    int mode;
+    int64_t t_base;
+    int rank, world;
+    const float* agg_all;
+    float* agg_out;
+    float* rcar;
 };
 
 // Batch-parallel plan (hmm_batchseq.cu): one lane group per sequence, 9 <= D <= 32.

@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(256, 1) lg_leaf_tc_kernel(const LgParams p, co
     float v[64];
     if (n > 0) {
         const float4* lr = reinterpret_cast<const float4*>(lik + ((size_t)b * T + t0) * 64);
-        const bool first = (t0 == 0);
+        const bool first = (p.t_base + t0 == 0);
 #pragma unroll
         for (int j4 = 0; j4 < 16; j4++) {
             const float4 l4 = __ldg(lr + j4);

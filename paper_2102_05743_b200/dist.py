@@ -184,7 +184,7 @@ def _all_gather(x: torch.Tensor, group=None) -> torch.Tensor:
 
 
 def smooth_dist(log_pi, log_A, log_lik_local, t_base: int, group=None, backend=None):
-    """Parallel smoother over a T-partitioned sequence.  Returns (filtered, smoothed, log_z [1], info [1])
+    """Parallel smoother over a T-partitioned sequence (1 <= D <= 64; the Viterbi split phase is D <= 8).  Returns (filtered, smoothed, log_z [1], info [1])
     for the local slice; log_z and info are global and identical on every rank (rank-order sums and
     info combination done by the library's hmm_dist_combine)."""
     be = _backend(backend)

@@ -182,3 +182,32 @@ def test_dist_misaligned_output_rejected():
     f, s, z, i = be.smooth_finish(lp, la, ll, 0, agg, 0, 1)  # the workspace is still consistent
     torch.cuda.synchronize()
     assert int(i[0]) == 0
+
+
+@pytest.mark.parametrize("D,world,T", [(12, 2, 20_000), (16, 4, 100_003), (24, 3, 50_000), (40, 8, 100_000),
+                                       (64, 2, 100_000), (64, 1, 5000), (33, 8, 64)])
+def test_dist_smoother_large_D(D, world, T):
+    """Split-phase smoother at D > 8 (the large-D block scan: reduce -> DP x DP rank aggregate, finish ->
+    rank carries, carry chains, sweeps): rank-count invariant and equal to the oracle on the whole
+    sequence (D = 64 runs the tcgen05 leaf products)."""
+    wl = W.dense(D, T, seed=7 + D)
+    filt, sm, lz, info = emulate_smooth(wl, world)
+    assert all(i == 0 for i in info), info
+    o = oracle.smooth(wl.log_pi, wl.log_A, wl.log_lik)
+    assert float(np.abs(sm - o["smoothed"]).max()) <= TOL_MARG
+    assert float(np.abs(filt - o["filtered"]).max()) <= TOL_MARG
+    assert rel(lz, o["log_z"]) <= TOL_REL
+
+
+def test_dist_large_D_info_and_viterbi_unsupported():
+    import paper_2102_05743_b200 as H
+    wl = W.dense(20, 30_000, seed=3)
+    wl.log_lik[17_345, :] = -np.inf
+    filt, sm, lz, info = emulate_smooth(wl, 4)
+    assert 17_346 in info  # the first impossible GLOBAL step + 1, reported by the rank that holds it
+    from paper_2102_05743_b200.dist import LibBackend
+    dev = torch.device("cuda")
+    lp, la = torch.from_numpy(wl.log_pi).to(dev), torch.from_numpy(wl.log_A).to(dev)
+    ll = torch.from_numpy(wl.log_lik).to(dev)
+    with pytest.raises(H.HmmError):
+        LibBackend().viterbi_reduce(lp, la, ll, 0)
