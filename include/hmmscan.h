@@ -235,9 +235,11 @@ hmm_status_t hmm_viterbi_path_elements(int D, int64_t T, int64_t B, const float*
  * the phases the CALLER all-gathers small fixed-size blobs (e.g. torch.distributed
  * all_gather_into_tensor over NCCL/NVLink) into rank order.  All phases of one rank must use the same
  * workspace (hmm_dist_workspace_size bytes, zero-filled once), on the same stream, in order.
- * Supported for a single sequence: the smoother for 1 <= D <= 64, the Viterbi for 1 <= D <= 8 (its rank
- * records are 16-byte maps; D > 8 -> HMM_ERR_UNSUPPORTED).  hmm_dist_agg_bytes(D) is align16(D*D*4) for
- * D <= 8 and DP*DP*4 (DP = 16, 32 or 64, the padded state count) for D > 8.
+ * Supported for a single sequence, 1 <= D <= 64.  hmm_dist_agg_bytes(D) is align16(D*D*4) for D <= 8
+ * and DP*DP*4 (DP = 16, 32 or 64, the padded state count) for D > 8.  The Viterbi rank record is
+ * hmm_dist_record_bytes_d(D) bytes: 16 for D <= 8 (u64 byte map, i32 x*; hmm_dist_record_bytes()), and
+ * DP + 16 for D > 8 (uint8 map[DP], i32 x* at byte DP); hmm_dist_pack / hmm_dist_combine carry only the
+ * 16-byte records, so at D > 8 the caller all-gathers the records itself.
  *
  * Smoother (Algorithm 3 across ranks; the rank aggregate is the ordered product of the rank's
  * elements, Def. 3 / PAPER.md:281-290):
@@ -248,7 +250,7 @@ hmm_status_t hmm_viterbi_path_elements(int D, int64_t T, int64_t B, const float*
  * Viterbi (Def. 5 aggregates; rank backpointer maps compose right to left):
  *   1. hmm_viterbi_dist_reduce  -> agg_out
  *   2. caller: all-gather -> agg_all
- *   3. hmm_viterbi_dist_forward -> record_out (hmm_dist_record_bytes() = 16 bytes: u64 map, i32 x*),
+ *   3. hmm_viterbi_dist_forward -> record_out (hmm_dist_record_bytes_d(D) bytes, see above),
  *      log_prob_partial[1]; log_prob = sum of partials over ranks.
  *   4. caller: all-gather the records -> records_all[world]
  *   5. hmm_viterbi_dist_finish  -> path of the local slice.
@@ -262,6 +264,7 @@ hmm_status_t hmm_viterbi_path_elements(int D, int64_t T, int64_t B, const float*
  */
 size_t hmm_dist_agg_bytes(int D);
 size_t hmm_dist_record_bytes(void);
+size_t hmm_dist_record_bytes_d(int D);
 size_t hmm_dist_workspace_size(int op, int D, int64_t T_local);
 hmm_status_t hmm_smooth_dist_reduce(int D, int64_t T_local, int64_t t_base, const float* log_pi, const float* log_A,
                                     const float* log_lik, void* agg_out, int32_t* info, void* workspace,

@@ -328,21 +328,26 @@ hmm_status_t run(int op, int D, int64_t T, int64_t B, const float* log_pi, const
                  size_t ws_bytes, void* stream, const DistArgs& da = DistArgs()) {
     if (D < 1 || T < 1 || B < 1 || B > 65535) return HMM_ERR_INVALID_VALUE;
     if (D > HMM_MAX_D) return HMM_ERR_UNSUPPORTED;
-    // split phase at D > 8: the smoother on one sequence (reduce / finish); the Viterbi records are D <= 8
+    // split phase at D > 8 (one sequence): smoother reduce / finish, Viterbi reduce / forward / finish
     if (D > 8 && da.mode != hmm::HMM_MODE_FULL &&
-        (op != 0 || B != 1 || (da.mode != hmm::HMM_MODE_REDUCE && da.mode != hmm::HMM_MODE_SFINISH)))
+        (B != 1 || (op == 0 && da.mode != hmm::HMM_MODE_REDUCE && da.mode != hmm::HMM_MODE_SFINISH) ||
+         (op == 1 && da.mode != hmm::HMM_MODE_REDUCE && da.mode != hmm::HMM_MODE_VFORWARD &&
+          da.mode != hmm::HMM_MODE_VFINISH)))
         return HMM_ERR_UNSUPPORTED;
     if (D > 8) {
         const bool ldist = da.mode != hmm::HMM_MODE_FULL;
         const bool lreduce = da.mode == hmm::HMM_MODE_REDUCE;
-        if (!log_pi || !log_A || !log_lik || (!lreduce && !scalar) || !info) return HMM_ERR_INVALID_VALUE;
+        const bool vfwd = da.mode == hmm::HMM_MODE_VFORWARD, vfin = da.mode == hmm::HMM_MODE_VFINISH;
+        const bool need_sc = !lreduce && !vfin;
+        if (!log_pi || !log_A || !log_lik || (need_sc && !scalar) || !info) return HMM_ERR_INVALID_VALUE;
         if (op == 0 && !lreduce && !smoothed) return HMM_ERR_INVALID_VALUE;
-        if (op == 1 && !path) return HMM_ERR_INVALID_VALUE;
+        if (op == 1 && (da.mode == hmm::HMM_MODE_FULL || vfin) && !path) return HMM_ERR_INVALID_VALUE;
         if (op == 0 && !lreduce && !filtered) return HMM_ERR_UNSUPPORTED;  // large-D smoother stages alpha in `filtered`
         if (!al4(log_pi) || !al4(log_A) || !al4(log_lik) || (scalar && !al8(scalar)) || !al4(info))
             return HMM_ERR_INVALID_VALUE;
         if (ldist && (da.world < 1 || da.rank < 0 || da.rank >= da.world || da.t_base < 0 ||
-                      (lreduce && !da.agg_out) || (!lreduce && !da.agg_all)))
+                      (lreduce && !da.agg_out) || ((da.mode == hmm::HMM_MODE_SFINISH || vfwd) && !da.agg_all) ||
+                      (vfwd && !da.rec_out) || (vfin && !da.rec_all)))
             return HMM_ERR_INVALID_VALUE;
         if (!ldist && use_batchseq(D, op, B))
             return run_batchseq(op, D, T, B, nullptr, 0, 0, log_pi, log_A, log_lik, filtered, smoothed, path, scalar,
@@ -374,6 +379,7 @@ hmm_status_t run(int op, int D, int64_t T, int64_t B, const float* log_pi, const
         lp.rcar = reinterpret_cast<float*>(w + G.o_rcar);
         lp.mode = da.mode; lp.t_base = da.t_base; lp.rank = da.rank; lp.world = da.world;
         lp.agg_all = da.agg_all; lp.agg_out = da.agg_out;
+        lp.rec_out = da.rec_out; lp.rec_all = da.rec_all; lp.rec_bytes = (int)hmm_dist_record_bytes_d(D);
         lp.tc = G.tc ? 1 : 0;
         lp.lik = reinterpret_cast<float*>(w + G.o_lik);
         cudaError_t e = hmm::launch_large(G.DP, op, lp, static_cast<cudaStream_t>(stream));
@@ -759,11 +765,18 @@ size_t hmm_dist_agg_bytes(int D) {
 
 size_t hmm_dist_record_bytes(void) { return 16; }
 
+size_t hmm_dist_record_bytes_d(int D) {
+    if (D < 1 || D > HMM_MAX_D) return 0;
+    if (D <= 8) return 16;
+    const size_t DP = D <= 16 ? 16 : (D <= 32 ? 32 : 64);
+    return DP + 16;  // uint8 map[DP], int32 x* at byte DP, padded to 16
+}
+
 size_t hmm_dist_workspace_size(int op, int D, int64_t T_local) {
     if ((op != 0 && op != 1) || D < 1 || D > HMM_MAX_D || T_local < 1) return 0;
-    if (D > 8) {  // split phase at D > 8: smoother only
+    if (D > 8) {  // split phase at D > 8: the large-D block scan
         LgPlan G;
-        return (op == 0 && make_large_plan(D, 0, T_local, 1, G)) ? G.total : 0;
+        return make_large_plan(D, op, T_local, 1, G) ? G.total : 0;
     }
     Plan P;
     if (!make_plan(D, op, T_local, 1, P, true)) return 0;

@@ -1159,6 +1159,51 @@ __global__ void lg_finalize_kernel(const LgParams p) {
 // Split phase: the carries entering and leaving this rank's slice from the gathered rank aggregates
 // (one CTA, DP threads): forward = 1^T Agg_0 ... Agg_{rank-1}, backward = Agg_{rank+1} ... Agg_{W-1} 1,
 // each step renormalised by an exact power of two (Thms 1-2 across ranks).
+// Split-phase Viterbi (max-product): the forward carry entering this rank, 0 (x) Agg_0 ... Agg_{rank-1}
+// in the max-plus semiring (Prop. 2 across ranks), normalised to max 0.
+template <int DP>
+__global__ void __launch_bounds__(DP) lg_rank_carry_mp_kernel(const LgParams p) {
+    __shared__ float u[DP], red[DP];
+    const int j = threadIdx.x;
+    u[j] = 0.0f;
+    __syncthreads();
+    for (int q = 0; q < p.rank; q++) {
+        const float* M = p.agg_all + (size_t)q * DP * DP;
+        float y = neg_inf();
+        for (int k = 0; k < DP; k++) y = fmaxf(y, u[k] + __ldg(M + k * DP + j));
+        red[j] = y;
+        __syncthreads();
+        float m = neg_inf();
+        for (int k = 0; k < DP; k++) m = fmaxf(m, red[k]);
+        __syncthreads();
+        u[j] = (m > neg_inf()) ? y - m : y;
+        __syncthreads();
+    }
+    p.rcar[j] = u[j];
+}
+// Viterbi forward (split phase): this rank's record = the composition of its block maps, F(x) = the
+// state before the rank's first step reached by backtracking from x at its last step, and x* = the
+// smallest argmax of V at its last step (used when this rank ends the sequence).
+__global__ void lg_rank_record_kernel(const LgParams p, int DP) {
+    const int x0 = threadIdx.x;
+    if (x0 < DP) {
+        int x = x0;
+        for (int64_t blk = p.NB - 1; blk >= 0; blk--) x = p.bmap[(size_t)blk * DP + x];
+        p.rec_out[x0] = (uint8_t)x;
+    }
+    if (x0 == 0) *reinterpret_cast<int32_t*>(p.rec_out + DP) = p.xstar[0];
+}
+// Viterbi finish (split phase): this rank's end state from the gathered records: x* of the last rank
+// mapped back through the ranks to our right; it seeds the block resolve.  Finish only backtracks:
+// info = 0 (errors were reported by reduce / forward).
+__global__ void lg_rank_end_kernel(const LgParams p, int DP) {
+    if (threadIdx.x != 0) return;
+    int x = *reinterpret_cast<const int32_t*>(p.rec_all + (size_t)(p.world - 1) * p.rec_bytes + DP);
+    for (int q = p.world - 1; q > p.rank; q--) x = p.rec_all[(size_t)q * p.rec_bytes + (x < 0 ? 0 : x)];
+    p.xstar[0] = x;
+    p.info[0] = 0;
+}
+
 template <int DP>
 __global__ void __launch_bounds__(DP) lg_rank_carry_kernel(const LgParams p) {
     __shared__ float u[DP], w[DP];
@@ -1228,12 +1273,21 @@ static cudaError_t lg_launch(const LgParams& p, cudaStream_t s) {
         lg_reduce_info_kernel<<<1, 1, 0, s>>>(p);
         return cudaGetLastError();
     }
+    if (p.mode == HMM_MODE_VFINISH) {  // backtrack only, from the end state the records give
+        lg_rank_end_kernel<<<1, 32, 0, s>>>(p, DP);
+        lg_resolve_kernel<<<(unsigned)p.B, 256, 0, s>>>(p, DP);
+        lg_backtrack_kernel<DP><<<grid, 256, 0, s>>>(p);
+        return cudaGetLastError();
+    }
     const float* init_pre = nullptr;
     const float* init_suf = nullptr;
     if (p.mode == HMM_MODE_SFINISH) {
         lg_rank_carry_kernel<DP><<<1, DP, 0, s>>>(p);
         init_pre = p.rcar;
         init_suf = p.rcar + DP;
+    } else if (p.mode == HMM_MODE_VFORWARD) {
+        lg_rank_carry_mp_kernel<DP><<<1, DP, 0, s>>>(p);
+        init_pre = p.rcar;
     }
     {
         const size_t smc = (size_t)6 * DP * DP * 4;
@@ -1251,11 +1305,12 @@ static cudaError_t lg_launch(const LgParams& p, cudaStream_t s) {
         }
     }
     lg_sweep_kernel<DP, OP><<<grid, 256, sm3, s>>>(p);
-    if (OP == 1) {
+    if (OP == 1 && p.mode == HMM_MODE_FULL) {
         lg_resolve_kernel<<<(unsigned)p.B, 256, 0, s>>>(p, DP);
         lg_backtrack_kernel<DP><<<grid, 256, 0, s>>>(p);
     }
     lg_finalize_kernel<<<(unsigned)p.B, 256, 0, s>>>(p);
+    if (OP == 1 && p.mode == HMM_MODE_VFORWARD) lg_rank_record_kernel<<<1, 64, 0, s>>>(p, DP);
     return cudaGetLastError();
 }
 

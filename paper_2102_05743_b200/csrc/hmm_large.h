@@ -50,6 +50,9 @@ struct LgParams {
     const float* agg_all;
     float* agg_out;
     float* rcar;
+    uint8_t* rec_out;       // Viterbi forward: this rank's record {uint8 map[DP], int32 x* at byte DP}
+    const uint8_t* rec_all; // Viterbi finish: the gathered records, rec_bytes apart
+    int rec_bytes;
 };
 
 // Batch-parallel plan (hmm_batchseq.cu): one lane group per sequence, 9 <= D <= 32.

@@ -59,6 +59,8 @@ class LibBackend:
         i32, i64, p, sz = ctypes.c_int, ctypes.c_int64, ctypes.c_void_p, ctypes.c_size_t
         L.hmm_dist_agg_bytes.restype = sz
         L.hmm_dist_agg_bytes.argtypes = [i32]
+        L.hmm_dist_record_bytes_d.restype = sz
+        L.hmm_dist_record_bytes_d.argtypes = [i32]
         L.hmm_dist_workspace_size.restype = sz
         L.hmm_dist_workspace_size.argtypes = [i32, i32, i64]
         L.hmm_smooth_dist_reduce.argtypes = [i32, i64, i64, p, p, p, p, p, p, sz, p]
@@ -139,7 +141,7 @@ class LibBackend:
     def viterbi_forward(self, lp, la, ll, t_base, agg_all, rank, world):
         T, D = ll.shape
         ws = self.ws(1, D, T, ll.device)
-        rec = torch.zeros(RECORD_BYTES, dtype=torch.uint8, device=ll.device)
+        rec = torch.zeros(int(self.L.hmm_dist_record_bytes_d(D)), dtype=torch.uint8, device=ll.device)
         lpp = torch.empty(1, dtype=torch.float64, device=ll.device)
         info = torch.empty(1, dtype=torch.int32, device=ll.device)
         _check(self.L.hmm_viterbi_dist_forward(D, T, t_base, _ptr(lp), _ptr(la), _ptr(ll), _ptr(agg_all), rank, world,
@@ -184,7 +186,7 @@ def _all_gather(x: torch.Tensor, group=None) -> torch.Tensor:
 
 
 def smooth_dist(log_pi, log_A, log_lik_local, t_base: int, group=None, backend=None):
-    """Parallel smoother over a T-partitioned sequence (1 <= D <= 64; the Viterbi split phase is D <= 8).  Returns (filtered, smoothed, log_z [1], info [1])
+    """Parallel smoother over a T-partitioned sequence (1 <= D <= 64).  Returns (filtered, smoothed, log_z [1], info [1])
     for the local slice; log_z and info are global and identical on every rank (rank-order sums and
     info combination done by the library's hmm_dist_combine)."""
     be = _backend(backend)
@@ -206,8 +208,13 @@ def viterbi_dist(log_pi, log_A, log_lik_local, t_base: int, group=None, backend=
     agg, info1 = be.viterbi_reduce(log_pi, log_A, log_lik_local, t_base)
     agg_all = _all_gather(agg, group)
     rec, lpp, info2 = be.viterbi_forward(log_pi, log_A, log_lik_local, t_base, agg_all, rank, world)
-    g = _all_gather(be.pack(rec, None, lpp, None, None, info1, info2), group)
-    rec_all, _, log_prob, _, info = be.combine(g, world)
+    if rec.numel() == RECORD_BYTES:
+        g = _all_gather(be.pack(rec, None, lpp, None, None, info1, info2), group)
+        rec_all, _, log_prob, _, info = be.combine(g, world)
+    else:  # D > 8: the wider rank records travel in their own all-gather
+        rec_all = _all_gather(rec, group)
+        g = _all_gather(be.pack(None, None, lpp, None, None, info1, info2), group)
+        _, _, log_prob, _, info = be.combine(g, world)
     # finish only backtracks: its info is always 0 (errors are reported by reduce / forward, hmmscan.h)
     path, _ = be.viterbi_finish(log_pi, log_A, log_lik_local, t_base, rec_all, rank, world)
     return path, log_prob, info
@@ -232,8 +239,13 @@ def smooth_viterbi_dist(log_pi, log_A, log_lik_local, t_base: int, group=None, b
         filt, sm, lzp, s_i2 = be.smooth_finish(log_pi, log_A, log_lik_local, t_base, s_all, rank, world)
         rec, lpp, v_i2 = be.viterbi_forward(log_pi, log_A, log_lik_local, t_base, v_all, rank, world)
     with _nvtx("hmm.allgather.records"):
-        g = _all_gather(be.pack(rec, lzp, lpp, s_i1, s_i2, v_i1, v_i2), group)
-        rec_all, log_z, log_prob, info, vinfo = be.combine(g, world)
+        if rec.numel() == RECORD_BYTES:
+            g = _all_gather(be.pack(rec, lzp, lpp, s_i1, s_i2, v_i1, v_i2), group)
+            rec_all, log_z, log_prob, info, vinfo = be.combine(g, world)
+        else:  # D > 8: the wider rank records travel in their own all-gather
+            rec_all = _all_gather(rec, group)
+            g = _all_gather(be.pack(None, lzp, lpp, s_i1, s_i2, v_i1, v_i2), group)
+            _, log_z, log_prob, info, vinfo = be.combine(g, world)
     with _nvtx("hmm.backtrack"):
         path, _ = be.viterbi_finish(log_pi, log_A, log_lik_local, t_base, rec_all, rank, world)
     return filt, sm, log_z, info, path, log_prob, vinfo

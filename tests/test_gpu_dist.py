@@ -199,15 +199,56 @@ def test_dist_smoother_large_D(D, world, T):
     assert rel(lz, o["log_z"]) <= TOL_REL
 
 
-def test_dist_large_D_info_and_viterbi_unsupported():
-    import paper_2102_05743_b200 as H
+def test_dist_large_D_info():
     wl = W.dense(20, 30_000, seed=3)
     wl.log_lik[17_345, :] = -np.inf
     filt, sm, lz, info = emulate_smooth(wl, 4)
     assert 17_346 in info  # the first impossible GLOBAL step + 1, reported by the rank that holds it
-    from paper_2102_05743_b200.dist import LibBackend
+    path, lpr, vinfo = emulate_viterbi(wl, 4)
+    assert 17_346 in vinfo
+
+
+@pytest.mark.parametrize("D,world,T", [(12, 2, 20_000), (16, 4, 100_003), (24, 3, 50_000), (40, 8, 100_000),
+                                       (64, 2, 100_000), (64, 1, 5000), (33, 8, 64)])
+def test_dist_viterbi_large_D(D, world, T):
+    """Split-phase Viterbi at D > 8 (records = DP-byte rank maps + x*): the MAP path is bit-exact where the
+    oracle's max-marginal gap >= TAU and attains the MAP weight; log_prob to 1e-6."""
+    wl = W.dense(D, T, seed=11 + D)
+    wl.log_lik = wl.log_lik + W.random_potentials(D, T, seed=5, sigma=0.1).log_lik
+    path, lpr, info = emulate_viterbi(wl, world)
+    assert all(i == 0 for i in info), info
+    v = oracle.viterbi(wl.log_pi, wl.log_A, wl.log_lik)
+    assert rel(lpr, v["log_prob"]) <= TOL_REL
+    _, gap = oracle.max_marginals(wl.log_pi, wl.log_A, wl.log_lik)
+    safe = gap >= TAU
+    assert np.array_equal(path[safe], v["path"][safe])
+    assert rel(oracle.joint_weight(wl.log_pi, wl.log_A, wl.log_lik, path), v["log_prob"]) <= TOL_REL
+
+
+@pytest.mark.parametrize("D", [4, 20])
+def test_dist_python_orchestration_one_rank(D):
+    """paper_2102_05743_b200.dist.smooth_viterbi_dist / viterbi_dist end to end in a one-rank gloo group on
+    the GPU (the collectives degenerate to copies): covers the 16-byte-record path (D <= 8, packed with
+    the scalars) and the wide-record path (D > 8, its own all-gather)."""
+    import os
+    import torch.distributed as dist
+    from paper_2102_05743_b200 import dist as HD
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29613")
+        dist.init_process_group("gloo", rank=0, world_size=1)
+    wl = W.dense(D, 20_000, seed=21 + D)
+    wl.log_lik = wl.log_lik + W.random_potentials(D, 20_000, seed=8, sigma=0.1).log_lik
     dev = torch.device("cuda")
-    lp, la = torch.from_numpy(wl.log_pi).to(dev), torch.from_numpy(wl.log_A).to(dev)
-    ll = torch.from_numpy(wl.log_lik).to(dev)
-    with pytest.raises(H.HmmError):
-        LibBackend().viterbi_reduce(lp, la, ll, 0)
+    lp, la, ll = (torch.from_numpy(x).to(dev) for x in (wl.log_pi, wl.log_A, wl.log_lik))
+    f, s, lz, info, path, lpr, vinfo = HD.smooth_viterbi_dist(lp, la, ll, 0)
+    p2, lpr2, vinfo2 = HD.viterbi_dist(lp, la, ll, 0)
+    torch.cuda.synchronize()
+    o = oracle.smooth(wl.log_pi, wl.log_A, wl.log_lik)
+    v = oracle.viterbi(wl.log_pi, wl.log_A, wl.log_lik)
+    assert int(info.item()) == 0 and int(vinfo.item()) == 0 and int(vinfo2.item()) == 0
+    assert float(np.abs(s.cpu().numpy() - o["smoothed"]).max()) <= TOL_MARG
+    assert rel(float(lz.item()), o["log_z"]) <= TOL_REL
+    for p_, l_ in ((path, lpr), (p2, lpr2)):
+        assert rel(float(l_.item()), v["log_prob"]) <= TOL_REL
+        assert rel(oracle.joint_weight(wl.log_pi, wl.log_A, wl.log_lik, p_.cpu().numpy()), v["log_prob"]) <= TOL_REL
