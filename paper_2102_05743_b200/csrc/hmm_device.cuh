@@ -147,6 +147,25 @@ __device__ __forceinline__ void group_arrive_wait(unsigned long long* counter, u
     __syncthreads();
 }
 
+// Copy the G published CTA-root slots (contiguous, slot_bytes a multiple of 16) into the SMEM stage that
+// mirrors them: one round of coalesced 16-B L2 loads per thread.  Every CTA of the grid reads the same few
+// KB right after the barrier; per-slot scalar loads (16 requests per slot) hot-spotted the few L2 slices
+// holding them (3.3 us at G = 148, tools/phase_timers.py).
+__device__ __forceinline__ void copy_root_slots(float* stage, const uint8_t* slots, int G, size_t slot_bytes,
+                                                int tid, int NT) {
+    const int n4 = (int)((size_t)G * slot_bytes / 16);
+    const float4* src4 = reinterpret_cast<const float4*>(slots);
+    float4* dst4 = reinterpret_cast<float4*>(stage);
+    float4 v[4];
+#pragma unroll
+    for (int j = 0; j < 4; j++)
+        if (tid + j * NT < n4) v[j] = __ldcg(src4 + tid + j * NT);
+#pragma unroll
+    for (int j = 0; j < 4; j++)
+        if (tid + j * NT < n4) dst4[tid + j * NT] = v[j];
+    for (int i = tid + 4 * NT; i < n4; i += NT) dst4[i] = __ldcg(src4 + i);
+}
+
 // ---------------------------------------------------------------- arithmetic helpers
 __device__ __forceinline__ float ex2(float x) {
     float y;

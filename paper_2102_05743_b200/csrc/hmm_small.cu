@@ -178,15 +178,7 @@ __global__ void __launch_bounds__(small_nt(D)) hmm_small_kernel(const KParams p)
         if (G > 1 || !do_pass1 || mode == HMM_MODE_REDUCE) {
             if (do_pass1) group_arrive_wait(arrive1, (uint32_t)G);  // (G == 1: just a CTA barrier)
             HMM_STAMP(3);
-            // copy all G roots into SMEM: one round of independent loads
-            for (int i = tid; i < G; i += NT) {
-                const float* src = reinterpret_cast<const float*>(slots + (size_t)i * p.slot_bytes);
-                float v[D * D];
-#pragma unroll
-                for (int e = 0; e < D * D; e++) v[e] = __ldcg(src + e);
-#pragma unroll
-                for (int e = 0; e < D * D; e++) stage[(size_t)i * sw + e] = v[e];
-            }
+            copy_root_slots(stage, slots, G, p.slot_bytes, tid, NT);
             __syncthreads();
         }
         if (mode == HMM_MODE_REDUCE) {

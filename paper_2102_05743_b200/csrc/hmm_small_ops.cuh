@@ -533,9 +533,102 @@ __device__ inline void warp_store_wait() {
 // ---------------------------------------------------------------------------- leaf kernels
 // Sum-product leaf: P = psi_{t0} psi_{t0+1} ... (n >= 1 elements), renormalised every step.
 // If write_l, overwrites the tile rows with l_t = exp(ll_t - m_t) (reused by the sweeps).
+// D = 4 leaf: two chains (rows [0, h) and [h, n), combined at the end: 2x ILP on the latency-bound fold)
+// of packed column-pair steps, P <- P psi_t = (P A) diag(l_t) as FMUL2 / FFMA2 with the broadcast P(r,k);
+// the exact power-of-two renormalisation is folded into the next step's ex2 argument (d = 127 - E(max)),
+// so it costs no multiplies.  The l rows written back for the sweeps then carry that factor 2^d: the
+// sweeps are scale-free except log Z, from which the written factors' sum (an exact integer times ln 2)
+// is removed here.
+__device__ __forceinline__ void sp_leaf4_step(const float* row, float* wrow, bool start, bool t0, const float2* A2,
+                                              const float* pi, float2* P2, float& d, float& dsum, double& msum,
+                                              bool acc_m) {
+    float v[4];
+    ld_row<4>(row, v);
+    const float mr = fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3]));
+    if (acc_m && mr > neg_inf()) msum += (double)mr;
+    const float m = fmaxf(mr, -1e30f);  // all -inf (impossible step): l = 0
+    const float c = fmaf(-m, kLog2e, d);
+    float l[4];
+#pragma unroll
+    for (int j = 0; j < 4; j++) l[j] = ex2(fmaf(v[j], kLog2e, c));
+    if (wrow) {
+        st_row<4>(wrow, l);
+        dsum += d;
+    }
+    const float2 l2[2] = {make_float2(l[0], l[1]), make_float2(l[2], l[3])};
+    if (start) {
+#pragma unroll
+        for (int r = 0; r < 4; r++)
+#pragma unroll
+            for (int jj = 0; jj < 2; jj++)
+                P2[r * 2 + jj] = t0 ? __fmul2_rn(make_float2(pi[2 * jj], pi[2 * jj + 1]), l2[jj])
+                                    : __fmul2_rn(A2[r * 2 + jj], l2[jj]);
+    } else {
+        float2 R2[8];
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+#pragma unroll
+            for (int jj = 0; jj < 2; jj++) R2[k * 2 + jj] = __fmul2_rn(A2[k * 2 + jj], l2[jj]);
+        float2 Pn[8];
+#pragma unroll
+        for (int r = 0; r < 4; r++) {
+            const float p0 = P2[r * 2].x, p1 = P2[r * 2].y, p2 = P2[r * 2 + 1].x, p3 = P2[r * 2 + 1].y;
+#pragma unroll
+            for (int jj = 0; jj < 2; jj++) {
+                float2 acc = __fmul2_rn(make_float2(p0, p0), R2[jj]);
+                acc = __ffma2_rn(make_float2(p1, p1), R2[2 + jj], acc);
+                acc = __ffma2_rn(make_float2(p2, p2), R2[4 + jj], acc);
+                acc = __ffma2_rn(make_float2(p3, p3), R2[6 + jj], acc);
+                Pn[r * 2 + jj] = acc;
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < 8; e++) P2[e] = Pn[e];
+    }
+    float mx[8];
+#pragma unroll
+    for (int e = 0; e < 8; e++) mx[e] = fmaxf(P2[e].x, P2[e].y);
+    d = exp_offset(vmax2_tree<8>(mx));
+}
+
 template <int D>
 __device__ __forceinline__ void sp_leaf(float* rows, int n, bool t0, const float* A, const float* pi, float* P,
                                         double& msum, bool write_l, bool acc_m, bool& bad) {
+    if constexpr (D == 4) {
+        float2 A2[8];
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            A2[k * 2] = make_float2(A[k * 4], A[k * 4 + 1]);
+            A2[k * 2 + 1] = make_float2(A[k * 4 + 2], A[k * 4 + 3]);
+        }
+        const int h = (n + 1) / 2;  // chain X: rows [0, h); chain Y: rows [h, n)
+        float2 X2[8], Y2[8];
+        float dx = 0.0f, dy = 0.0f, dsum = 0.0f;
+        double mx = 0.0, my = 0.0;
+        for (int q = 0; q < h; q++) {
+            sp_leaf4_step(rows + q * 4, write_l ? rows + q * 4 : nullptr, q == 0, t0 && q == 0, A2, pi, X2, dx, dsum,
+                          mx, acc_m);
+            if (h + q < n)
+                sp_leaf4_step(rows + (h + q) * 4, write_l ? rows + (h + q) * 4 : nullptr, q == 0, false, A2, pi, Y2,
+                              dy, dsum, my, acc_m);
+        }
+        msum += mx + my - (double)dsum * (double)kLn2;
+        float X[16], Y[16];
+#pragma unroll
+        for (int e = 0; e < 8; e++) {
+            X[2 * e] = X2[e].x; X[2 * e + 1] = X2[e].y;
+            Y[2 * e] = Y2[e].x; Y[2 * e + 1] = Y2[e].y;
+        }
+        if (n > h) mat_op<4, false>(X, Y, P);  // (renormalised by an exact power of two)
+        else {
+            const float s = pow2_inv(vmax<16>(X));
+#pragma unroll
+            for (int e = 0; e < 16; e++) P[e] = X[e] * s;
+        }
+        const float chk = vsum<16>(P);  // a NaN or +inf input anywhere in the leaf leaves a NaN here
+        bad |= (chk != chk);
+        return;
+    }
     float s = 1.0f;
     for (int i = 0; i < n; i++) {
         float v[D], l[D];
