@@ -741,12 +741,18 @@ __global__ void __launch_bounds__(stream_nt(D)) hmm_stream_kernel(const SParams 
         const int64_t rem = T - (wbase + (int64_t)j * n + (int64_t)k * S);
         return rem <= 0 ? 0 : (rem < S ? (int)rem : S);
     };
-    auto warp_full = [&](int k) -> bool { return wbase + 31 * n + (int64_t)k * S + S <= T; };
-    // The warp holding the end of the sequence: bit j of `fullmask(k)` = lane j's slice k is full (one
-    // ballot per slice).  Its full slices take the same 16-B copies as a full warp; only the one
-    // partial lane slice of the sequence takes the element-wise path.
-    const int my_nfull = (int)((a1 > a0 ? a1 - a0 : 0) / S);
-    auto fullmask = [&](int k) -> uint32_t { return __ballot_sync(0xffffffffu, my_nfull > k); };
+    // Warp geometry against the sequence end, computed once (warp-uniform): lanes [0, jT) are complete,
+    // lane jT (if < 32) holds the end with nfT full slices and a partial slice of remT rows, later lanes
+    // are empty.  Slice k then has full lane slices [0, jfull(k)); the warp holding the end of the
+    // sequence moves them with the same 16-B copies as a full warp, and only the one partial lane slice
+    // (k == nfT) takes the element-wise path.  (A per-slice ballot here cost the last warp ~5 % over
+    // the other warps in both passes: the step's tail straggler.)
+    const int64_t wrem = T - wbase;
+    const int jT = wrem >= 32 * n ? 32 : (wrem <= 0 ? 0 : (int)(wrem / n));
+    const int64_t inT = (jT < 32 && wrem > 0) ? wrem - (int64_t)jT * n : 0;
+    const int nfT = (int)(inT / S), remT = (int)(inT - (int64_t)nfT * S);
+    auto jfull = [&](int k) -> int { return jT == 32 ? 32 : jT + (k < nfT ? 1 : 0); };
+    auto warp_full = [&](int k) -> bool { return jfull(k) == 32; };
     // async load of slice k of the warp's lanes into ring stage st (one cp.async group per call)
     auto coop_load = [&](int k, int st) {
         uint8_t* sbase = ring + (size_t)st * NT * PITCH + (size_t)warp * 32 * PITCH;
@@ -778,7 +784,7 @@ __global__ void __launch_bounds__(stream_nt(D)) hmm_stream_kernel(const SParams 
                     dst += LPI * PITCH;
                 }
             } else {  // the warp holding the end of the sequence (lanes past the end load nothing)
-                const int jp = __popc(fullmask(k));  // lanes [0, jp) full; lane jp's slice may be partial
+                const int jp = jfull(k);  // lanes [0, jp) full; lane jp's slice k is partial iff k == nfT
                 const int nv = (jp - j0 + LPI - 1) / LPI;  // this thread's chunks in full lane slices
 #pragma unroll
                 for (int it = 0; it < CPL; it++) {
@@ -786,10 +792,10 @@ __global__ void __launch_bounds__(stream_nt(D)) hmm_stream_kernel(const SParams 
                     src += (int64_t)LPI * n * D;
                     dst += LPI * PITCH;
                 }
-                if (jp < 32 && ((jp - j0) % LPI) == 0 && jp >= j0) {
-                    const int64_t rem64 = (T - (wbase + (int64_t)jp * n + (int64_t)k * S)) * D - ch * 4;
-                    if (rem64 > 0) {
-                        const int f = rem64 > 4 ? 4 : (int)rem64;
+                if (k == nfT && remT > 0 && ((jp - j0) % LPI) == 0 && jp >= j0) {
+                    const int rem = remT * D - ch * 4;
+                    if (rem > 0) {
+                        const int f = rem > 4 ? 4 : rem;
                         cp_async16_zfill(sbase + (size_t)jp * PITCH + ch * 16,
                                          ll + (wbase + (int64_t)jp * n + (int64_t)k * S) * D + ch * 4, 4u * f);
                     }
@@ -830,7 +836,7 @@ __global__ void __launch_bounds__(stream_nt(D)) hmm_stream_kernel(const SParams 
                     src += LPI * PITCH;
                 }
             } else {  // the warp holding the end of the sequence: full lane slices as above
-                const int jp = __popc(fullmask(k));  // lanes [0, jp) full; lane jp's slice may be partial
+                const int jp = jfull(k);
                 const int nv = (jp - j0 + LPI - 1) / LPI;
 #pragma unroll
                 for (int it = 0; it < CPL; it++) {
@@ -838,13 +844,13 @@ __global__ void __launch_bounds__(stream_nt(D)) hmm_stream_kernel(const SParams 
                     dst += (int64_t)LPI * n * D;
                     src += LPI * PITCH;
                 }
-                if (jp < 32 && ((jp - j0) % LPI) == 0 && jp >= j0) {
-                    const int64_t rem64 = (T - (wbase + (int64_t)jp * n + (int64_t)k * S)) * D - ch * 4;
-                    if (rem64 > 0) {
+                if (k == nfT && remT > 0 && ((jp - j0) % LPI) == 0 && jp >= j0) {
+                    const int rem = remT * D - ch * 4;
+                    if (rem > 0) {
                         float* d2 = g + (wbase + (int64_t)jp * n + (int64_t)k * S) * D + ch * 4;
                         const float* s2 = reinterpret_cast<const float*>(sbase + (size_t)jp * PITCH + ch * 16);
-                        if (rem64 >= 4) __stcs(reinterpret_cast<float4*>(d2), *reinterpret_cast<const float4*>(s2));
-                        else for (int f = 0; f < (int)rem64; f++) d2[f] = s2[f];
+                        if (rem >= 4) __stcs(reinterpret_cast<float4*>(d2), *reinterpret_cast<const float4*>(s2));
+                        else for (int f = 0; f < rem; f++) d2[f] = s2[f];
                     }
                 }
             }
@@ -1165,7 +1171,7 @@ __global__ void __launch_bounds__(stream_nt(D)) hmm_stream_kernel(const SParams 
 #pragma unroll
                     for (int it = 0; it < NCB; it++) {
                         const int q = lane + 32 * it, j = q / NCB, ch = q - j * NCB;
-                        if (lane_rows(j, k) > 0)
+                        if (j < jfull(k) || (j == jT && k == nfT && remT > 0))  // (lane_rows(j, k) > 0)
                             *reinterpret_cast<uint2*>(bpg + (size_t)(wbase + (int64_t)j * n + (int64_t)k * S) * BPB + ch * 8) =
                                 *reinterpret_cast<const uint2*>(sbase + (size_t)j * PITCH + ch * 8);
                     }
