@@ -689,6 +689,11 @@ __global__ void __launch_bounds__(stream_nt(D)) hmm_stream_kernel(const SParams 
     unsigned long long* tmr = p.timers ? p.timers + (size_t)c * 16 : nullptr;
 #define HMM_STAMP(i) do { if (tmr && tid == 0) tmr[i] = global_ns(); } while (0)
     HMM_STAMP(0);
+    if (tmr && tid == 0) {  // slot 13: the SM this CTA runs on (phase profiles per SM)
+        uint32_t smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        tmr[13] = smid;
+    }
     if (tid == 0) {
         for (int w = 0; w < NW; w++) mbar_init(&qbar[w], 1);
         fence_mbar_init();

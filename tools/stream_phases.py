@@ -34,6 +34,10 @@ for op in (0, 1):
             continue
         col = (col - t0) / 1e3
         print(f"  {i:2d} {nm:10s} min {col.min():9.1f}  med {np.median(col):9.1f}  max {col.max():9.1f} us")
+    if len(sys.argv) > 2 and op == 0:  # per-CTA pass-2 duration with the SM id, sorted
+        p2 = (t[:, 6] - t[:, 5]) / 1e3; p1 = (t[:, 1] - t[:, 0]) / 1e3
+        for j in np.argsort(p2):
+            print(f"    cta {j:3d} sm {int(t[j, 13]):3d}  pass1 {p1[j]:7.1f}  pass2 {p2[j]:7.1f} us")
     for i in (1, 2, 6, 10, 11, 12):
         col = (t[:, i] - t0) / 1e3
         idx = np.argsort(-col)[:4]
