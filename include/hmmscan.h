@@ -323,7 +323,9 @@ hmm_status_t hmm_dist_combine(int world, const double* gathered, void* records_a
  *     aligned buffers required, else automatic), 2 resident/chunked; for 33 <= D <= 64: 3 keeps the
  *     sum-product leaf products on the FP32 CUDA cores instead of the tensor cores; for 9 <= D <= 32:
  *     4 forces the batch-parallel plan (one lane group per sequence running the Algorithm 1 / 4
- *     recursions, chosen automatically for large B), 5 forbids it (block scan).  Test and profiling
+ *     recursions, chosen automatically for large B; two warps per sequence running the forward and
+ *     backward recursions from both ends while B fits one wave, else one warp), 5 forbids it (block
+ *     scan), 6 forces the one-warp batch-parallel plan.  Test and profiling
  *     use only; the results agree within the stated tolerances whichever path runs.
  */
 void hmm_debug_set_timers(unsigned long long* device_buf);

@@ -20,7 +20,8 @@ cudaError_t launch_large(int DP, int op, const LgParams& p, cudaStream_t s);
 cudaError_t launch_stream(int D, int op, unsigned G, const SParams& sp, cudaStream_t s);
 int large_leaves_per_block(int DP);
 size_t variants_workspace_size(int op, int D, int64_t T, int64_t B);
-cudaError_t launch_batchseq(int DP, int op, const BSParams& p, cudaStream_t s);
+cudaError_t launch_batchseq(int DP, int op, bool bidir, const BSParams& p, cudaStream_t s);
+int64_t bs2_beta_rows(int64_t Tmax);
 }
 
 using hmm::Plan;
@@ -218,13 +219,24 @@ int bs_dp(int D) { return D <= 16 ? 16 : (D <= 32 ? 32 : 0); }
 bool use_batchseq(int D, int op, int64_t B) {
     const int DP = bs_dp(D);
     if (D <= 8 || DP == 0) return false;
-    if (t_force_path == 4) return true;
+    if (t_force_path == 4 || t_force_path == 6) return true;
     if (t_force_path == 5) return false;
     const int64_t bmin = DP == 16 ? (op == 0 ? 768 : 512) : (op == 0 ? 160 : 128);
     return B >= bmin;
 }
+// Bidirectional variant (two warps per sequence, hmm_batchseq.cu): the forward and backward recursions
+// run at the same time from the two ends, halving the per-sequence latency; it needs one CTA slot per
+// sequence (7 per SM at DP = 16, 3 at DP = 32), so the one-warp plan stays for batches past one wave.
+// hmm_debug_force_path 6 forces the one-warp plan.
+bool bs_bidir(int D, int op, int64_t B) {
+    if (t_force_path == 6) return false;
+    const int DP = bs_dp(D);
+    (void)op;
+    return DP == 16 ? B <= 148 * 7 : B <= 148 * 3;
+}
 size_t bs_workspace(int op, int D, int64_t T, int64_t B) {
-    return op == 1 ? (((size_t)B * T * bs_dp(D) + 255) & ~(size_t)255) : 256;
+    if (op == 1) return ((size_t)B * T * bs_dp(D) + 255) & ~(size_t)255;
+    return ((size_t)B * (size_t)hmm::bs2_beta_rows(T) * (size_t)D * 4 + 511) & ~(size_t)255;
 }
 hmm_status_t run_batchseq(int op, int D, int64_t T, int64_t B, const int64_t* offsets, int64_t pis, int64_t As,
                           const float* log_pi, const float* log_A, const float* log_lik, float* filtered,
@@ -237,8 +249,10 @@ hmm_status_t run_batchseq(int op, int D, int64_t T, int64_t B, const int64_t* of
     bp.log_pi = log_pi; bp.log_A = log_A; bp.log_lik = log_lik;
     bp.filtered = filtered; bp.smoothed = smoothed; bp.path = path; bp.scalar_out = scalar; bp.info = info;
     bp.bp = static_cast<uint8_t*>(ws);
+    bp.sbeta = static_cast<float*>(ws);
+    bp.s_rows = hmm::bs2_beta_rows(T);
     bp.offsets = offsets; bp.pi_stride = pis; bp.A_stride = As;
-    const cudaError_t e = hmm::launch_batchseq(bs_dp(D), op, bp, static_cast<cudaStream_t>(stream));
+    const cudaError_t e = hmm::launch_batchseq(bs_dp(D), op, bs_bidir(D, op, B), bp, static_cast<cudaStream_t>(stream));
     return e == cudaSuccess ? HMM_SUCCESS : HMM_ERR_CUDA;
 }
 
@@ -679,7 +693,7 @@ const char* hmm_version(void) { return "hmmscan 0.1 sm_100a"; }
 
 void hmm_debug_set_timers(unsigned long long* device_buf) { t_timers = device_buf; }
 
-void hmm_debug_force_path(int path) { t_force_path = (path >= 0 && path <= 5) ? path : 0; }
+void hmm_debug_force_path(int path) { t_force_path = (path >= 0 && path <= 6) ? path : 0; }
 
 int hmm_debug_plan(int op, int D, int64_t T, int64_t B, int64_t* out /*[8]*/) {
     StPlan SP;

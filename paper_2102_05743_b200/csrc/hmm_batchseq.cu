@@ -462,18 +462,491 @@ __global__ void __launch_bounds__(kBsThreads) bs_viterbi_kernel(const BSParams p
     }
 }
 
-size_t bs_smem(int DP, int op) {
+// ============================================================================ bidirectional plan
+// Two warps per sequence (one CTA): the forward recursion (Algorithm 1 forward / Algorithm 4 forward) and
+// the backward recursion (Algorithm 1 backward / the max-product backward recursion of Lemma 3,
+// PAPER.md:640-669) run at the same time from the two ends and meet in the middle, so a sequence takes T
+// recursion steps of latency instead of 2T (sum-product) or T + the backtrack (max-product).  The
+// sequence is cut at mid = ceil(nch / 2) chunks:
+//   smoother  phase 1: forward over [0, mid) (filtered) | backward over [mid, T) (b_t kept in the
+//             workspace);  phase 2: forward over [mid, T) (filtered, smoothed = a_t o b_t / sum from the
+//             kept b_t) | backward over [0, mid) (smoothed from the filtered rows of phase 1).
+//   Viterbi   forward max-product over [0, mid) with backpointers | backward max-product over [mid, T)
+//             with forward pointers; x*_{mid-1} = argmax (V^f + V^b) (Theorem 4's max-marginal at one
+//             step, smallest index), log_prob = its value; then both halves of the path in parallel
+//             (backtrack / forward track).
+// One CTA barrier separates the phases.  Results are the recursions' own (the scan's associativity is
+// not used here: the whole sequence is one block-wise element).
+constexpr int kBs2Threads = 64;
+__host__ __device__ inline int64_t bs2_half_rows(int64_t Tmax) {
+    const int64_t nch = (Tmax + kBsC - 1) / kBsC;
+    return (nch / 2) * kBsC;
+}
+
+template <int DP>
+__global__ void __launch_bounds__(kBs2Threads) bs2_smooth_kernel(const BSParams p) {
+    using S = BsShape<DP>;
+    constexpr int H = S::H, NV = S::NV;
+    constexpr int RING = kBsStages * kBsC * DP;
+    constexpr int OUT = (kBsC + 1) * DP;
+    constexpr int PER = 2 * RING + OUT + 2 * kBsC;
+    extern __shared__ __align__(16) float bsm[];
+    const int lane = threadIdx.x % 32, role = threadIdx.x / 32;  // role 0: forward, 1: backward
+    const int j = lane % DP, h = lane / DP;
+    float* r0buf = bsm + (size_t)role * PER;  // log_lik chunks (turned into l in place)
+    float* r1buf = r0buf + RING;              // forward: kept b_t rows; backward: filtered rows
+    float* out = r1buf + RING;                // [1 + C][DP] staged rows
+    float* mrow = out + OUT;
+    float* inv = mrow + kBsC;
+    const int64_t b = blockIdx.x;
+    if (b >= p.B) return;
+    int64_t base, raw;
+    const int64_t T = seq_span(p.offsets, p.T, b, base, raw);
+    if (T < 1) {
+        if (role == 0 && lane == 0) { p.scalar_out[b] = 0.0; p.info[b] = kInfoBadLength; }
+        return;
+    }
+    const int D = p.D;
+    const bool act = j < D;
+    const float* la = p.log_A + b * p.A_stride;
+    float Am[NV];  // forward: A(i, j); backward: A(j, i), i in this lane's half
+#pragma unroll
+    for (int k = 0; k < NV; k++) {
+        const int i = h * NV + k;
+        Am[k] = (act && i < D) ? ex2(__ldg(role == 0 ? la + i * D + j : la + j * D + i) * kLog2e) : 0.0f;
+    }
+    const float piv = act ? ex2(__ldg(p.log_pi + b * p.pi_stride + j) * kLog2e) : 0.0f;
+    float* filt = p.filtered + base * D;
+    float* smo = p.smoothed + base * D;
+    const int64_t nch = (T + kBsC - 1) / kBsC, nch1 = (nch + 1) / 2;
+    const int64_t mid = (nch1 * kBsC < T) ? nch1 * kBsC : T;
+    float* sb = p.sbeta + b * p.s_rows * D;  // row t - mid
+    bs_fill<DP>(r0buf, PER, 0.0f);
+    __syncwarp();
+    const BsRing<DP> rl{r0buf, p.log_lik + base * D, T, D, j, h};
+    const BsRing<DP> r1{r1buf, role == 0 ? sb - mid * D : filt, T, D, j, h};
+    auto hsum = [&](float v) -> float { return (H == 2) ? v + __shfl_xor_sync(0xffffffffu, v, 16) : v; };
+    auto hmax = [&](float v) -> float { return (H == 2) ? fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 16)) : v; };
+    auto nrows = [&](int64_t c) -> int { return (int)((T - c * kBsC < kBsC) ? T - c * kBsC : kBsC); };
+    // issue chunk c of ring R if c lies in [lo, hi), else an empty group (keeps the wait counts uniform)
+    auto iss = [&](const BsRing<DP>& R, int64_t c, int64_t lo, int64_t hi) {
+        if (c >= lo && c < hi) R.issue(c); else cp_async_commit();
+    };
+
+    double msum = 0.0;
+    int es = 0;
+    int64_t zero_t = -1;
+    bool bad = false;
+    float lastsum = 0.0f;
+    float bt = act ? 1.0f : 0.0f;  // b_{T-1} = 1 (Thm 2: a_{T:T+1} = 1)
+    // forward recursion over one staged chunk (rows hold l_t), a_t staged in out rows 1..n
+    auto fwd_chunk = [&](int64_t c, const float* rows, int n) {
+        for (int i = 0; i < n; i++) msum += (double)mrow[i];
+        for (int i = 0; i < n; i++) {
+            const int64_t t = c * kBsC + i;
+            const float l = rows[i * DP + j];
+            float a;
+            if (t == 0) {
+                a = piv * l;
+            } else {
+                float g[NV];
+                ld_vec<NV>(out + i * DP + h * NV, g);
+                const float mx = hmax(tmax<NV>(g));
+                const float s2 = pow2_inv(mx);
+                es += pow2_inv_log2(mx);
+                float c0 = 0.0f, c1 = 0.0f, c2 = 0.0f, c3 = 0.0f;
+#pragma unroll
+                for (int k = 0; k < NV; k += 4) {
+                    c0 = fmaf(g[k], Am[k], c0);
+                    c1 = fmaf(g[k + 1], Am[k + 1], c1);
+                    c2 = fmaf(g[k + 2], Am[k + 2], c2);
+                    c3 = fmaf(g[k + 3], Am[k + 3], c3);
+                }
+                a = hsum((c0 + c1) + (c2 + c3)) * (l * s2);
+            }
+            if (h == 0) out[(i + 1) * DP + j] = a;
+            __syncwarp();
+        }
+    };
+    // backward recursion over one staged chunk; stage(i, t) stages row i of the output before the update
+    auto bwd_chunk = [&](int64_t c, float* rows, int n, const float* frows) {
+        for (int i = n - 1; i >= 0; i--) {
+            const int64_t t = c * kBsC + i;
+            if (h == 0) {
+                out[(i + 1) * DP + j] = frows ? frows[i * DP + j] * bt : bt;  // gam_t, or b_t itself
+                rows[i * DP + j] *= bt;                                       // w = l_t o b_t
+            }
+            __syncwarp();
+            if (t > 0) {  // b_{t-1} = A (l_t o b_t), renormalised by an exact power of two
+                float g[NV];
+                ld_vec<NV>(rows + i * DP + h * NV, g);
+                const float s2 = pow2_inv(hmax(tmax<NV>(g)));
+                float c0 = 0.0f, c1 = 0.0f, c2 = 0.0f, c3 = 0.0f;
+#pragma unroll
+                for (int k = 0; k < NV; k += 4) {
+                    c0 = fmaf(Am[k], g[k], c0);
+                    c1 = fmaf(Am[k + 1], g[k + 1], c1);
+                    c2 = fmaf(Am[k + 2], g[k + 2], c2);
+                    c3 = fmaf(Am[k + 3], g[k + 3], c3);
+                }
+                bt = hsum((c0 + c1) + (c2 + c3)) * s2;
+            }
+        }
+        __syncwarp();
+    };
+
+    // ---------------- phase 1
+    if (role == 0) {  // forward over chunks [0, nch1): filtered
+        iss(rl, 0, 0, nch1);
+        iss(rl, 1, 0, nch1);
+        for (int64_t c = 0; c < nch1; c++) {
+            iss(rl, c + 2, 0, nch1);
+            cp_async_wait<2>();
+            __syncwarp();
+            float* rows = rl.stage(c);
+            const int n = nrows(c);
+            bad |= bs_prep<DP, false>(rows, mrow, n, D, j, h);
+            fwd_chunk(c, rows, n);
+            const int z = bs_flush<DP>(out + DP, n, filt + c * kBsC * D, D, j, h, inv, bad, lastsum);
+            if (z >= 0 && zero_t < 0) zero_t = c * kBsC + z;
+            if (h == 0) out[j] = out[n * DP + j];
+            __syncwarp();
+        }
+    } else {  // backward over chunks [nch1, nch) in reverse: b_t kept (row-normalised) in the workspace
+        iss(rl, nch - 1, nch1, nch);
+        iss(rl, nch - 2, nch1, nch);
+        for (int64_t c = nch - 1; c >= nch1; c--) {
+            iss(rl, c - 2, nch1, nch);
+            cp_async_wait<2>();
+            __syncwarp();
+            float* rows = rl.stage(c);
+            const int n = nrows(c);
+            bs_prep<DP, false>(rows, mrow, n, D, j, h);
+            bwd_chunk(c, rows, n, nullptr);
+            bool dummy = false;
+            float dl;
+            bs_flush<DP>(out + DP, n, sb + (c * kBsC - mid) * D, D, j, h, inv, dummy, dl);
+        }
+    }
+    cp_async_wait<0>();
+    __threadfence_block();
+    __syncthreads();  // phase-1 filtered rows and kept b_t rows are visible to the other warp
+
+    // ---------------- phase 2
+    if (role == 0) {  // forward over [nch1, nch): filtered and smoothed = a_t o b_t / sum
+        iss(rl, nch1, nch1, nch); iss(r1, nch1, nch1, nch);
+        iss(rl, nch1 + 1, nch1, nch); iss(r1, nch1 + 1, nch1, nch);
+        for (int64_t c = nch1; c < nch; c++) {
+            iss(rl, c + 2, nch1, nch); iss(r1, c + 2, nch1, nch);
+            cp_async_wait<4>();
+            __syncwarp();
+            float* rows = rl.stage(c);
+            float* brows = r1.stage(c);
+            const int n = nrows(c);
+            bad |= bs_prep<DP, false>(rows, mrow, n, D, j, h);
+            fwd_chunk(c, rows, n);
+            for (int r = h; r < n; r += H) brows[r * DP + j] *= out[(r + 1) * DP + j];  // gam_t = a_t o b_t
+            __syncwarp();
+            const int z = bs_flush<DP>(out + DP, n, filt + c * kBsC * D, D, j, h, inv, bad, lastsum);
+            if (z >= 0 && zero_t < 0) zero_t = c * kBsC + z;
+            bool dummy = false;
+            float dl;
+            bs_flush<DP>(brows, n, smo + c * kBsC * D, D, j, h, inv, dummy, dl);
+            if (h == 0) out[j] = out[n * DP + j];
+            __syncwarp();
+        }
+        cp_async_wait<0>();
+        const double logz = log((double)lastsum) - (double)es * (double)kLn2 + msum;
+        if (lane == 0) {
+            p.scalar_out[b] = logz;
+            int32_t inf = 0;
+            if (bad || logz != logz) inf = -1;
+            else if (zero_t >= 0) inf = (int32_t)(zero_t + 1);
+            if (raw < 1 || raw > p.T) inf = kInfoBadLength;
+            p.info[b] = inf;
+        }
+    } else {  // backward over [0, nch1) in reverse: smoothed from the filtered rows of phase 1
+        iss(rl, nch1 - 1, 0, nch1); iss(r1, nch1 - 1, 0, nch1);
+        iss(rl, nch1 - 2, 0, nch1); iss(r1, nch1 - 2, 0, nch1);
+        for (int64_t c = nch1 - 1; c >= 0; c--) {
+            iss(rl, c - 2, 0, nch1); iss(r1, c - 2, 0, nch1);
+            cp_async_wait<4>();
+            __syncwarp();
+            float* rows = rl.stage(c);
+            const float* frows = r1.stage(c);
+            const int n = nrows(c);
+            bs_prep<DP, false>(rows, mrow, n, D, j, h);
+            bwd_chunk(c, rows, n, frows);
+            bool dummy = false;
+            float dl;
+            bs_flush<DP>(out + DP, n, smo + c * kBsC * D, D, j, h, inv, dummy, dl);
+        }
+        cp_async_wait<0>();
+    }
+}
+
+template <int DP>
+__global__ void __launch_bounds__(kBs2Threads) bs2_viterbi_kernel(const BSParams p) {
+    using S = BsShape<DP>;
+    constexpr int H = S::H, NV = S::NV;
+    constexpr int RING = kBsStages * kBsC * DP;
+    constexpr int PER = RING + 2 * DP + kBsC + kBsChunk + kBsChunk * DP / 4;
+    extern __shared__ __align__(16) float bsm[];
+    __shared__ float vmeet[2][DP];
+    __shared__ double cmeet;
+    __shared__ int fmeet[2];
+    const int lane = threadIdx.x % 32, role = threadIdx.x / 32;  // role 0: forward, 1: backward
+    const int j = lane % DP, h = lane / DP;
+    float* rl_buf = bsm + (size_t)role * PER;
+    float* xbuf = rl_buf + RING;                                  // [2][DP]
+    float* mrow = xbuf + 2 * DP;                                  // [C]
+    int32_t* spath = reinterpret_cast<int32_t*>(mrow + kBsC);     // [kBsChunk]
+    uint8_t* sbp = reinterpret_cast<uint8_t*>(spath + kBsChunk);  // [kBsChunk][DP]
+    const int64_t b = blockIdx.x;
+    if (b >= p.B) return;
+    int64_t base, raw;
+    const int64_t T = seq_span(p.offsets, p.T, b, base, raw);
+    if (T < 1) {
+        if (role == 0 && lane == 0) { p.scalar_out[b] = 0.0; p.info[b] = kInfoBadLength; }
+        return;
+    }
+    const int D = p.D;
+    const bool act = j < D;
+    const float* la = p.log_A + b * p.A_stride;
+    float LA[NV];  // forward: log A(i, j); backward: log A(j, i), i in this lane's half
+#pragma unroll
+    for (int k = 0; k < NV; k++) {
+        const int i = h * NV + k;
+        LA[k] = (act && i < D) ? __ldg(role == 0 ? la + i * D + j : la + j * D + i) : neg_inf();
+    }
+    const float lpv = act ? __ldg(p.log_pi + b * p.pi_stride + j) : neg_inf();
+    uint8_t* bp = p.bp + (size_t)b * p.T * DP;
+    bs_fill<DP>(rl_buf, RING + 2 * DP, neg_inf());
+    __syncwarp();
+    const BsRing<DP> rl{rl_buf, p.log_lik + base * D, T, D, j, h};
+    const int64_t nch = (T + kBsC - 1) / kBsC, nch1 = (nch + 1) / 2;
+    const int64_t mid = (nch1 * kBsC < T) ? nch1 * kBsC : T;
+    auto nrows = [&](int64_t c) -> int { return (int)((T - c * kBsC < kBsC) ? T - c * kBsC : kBsC); };
+    auto iss = [&](int64_t c, int64_t lo, int64_t hi) {
+        if (c >= lo && c < hi) rl.issue(c); else cp_async_commit();
+    };
+    int par = 0;
+    // one max-plus step over the exchanged vector x (lane j's value): best_i = max_k (x_k - o + LA(k or i)),
+    // smallest maximising index (the lower half wins ties); returns o = max x (0 if all -inf)
+    auto mp_step = [&](float xv, float& best, int& arg, bool& dead) -> float {
+        float* xb = xbuf + par * DP;
+        par ^= 1;
+        if (h == 0) xb[j] = xv;
+        __syncwarp();
+        float g[NV];
+        ld_vec<NV>(xb + h * NV, g);
+        float o = tmax<NV>(g);
+        if (H == 2) o = fmaxf(o, __shfl_xor_sync(0xffffffffu, o, 16));
+        dead = !(o > neg_inf());
+        if (dead) o = 0.0f;
+        float sc[NV];
+#pragma unroll
+        for (int k = 0; k < NV; k++) sc[k] = (g[k] - o) + LA[k];
+        best = tmax<NV>(sc);
+        arg = first_argmax<NV>(sc, best) + h * NV;
+        if (H == 2) {
+            const float bo = __shfl_xor_sync(0xffffffffu, best, 16);
+            const int ao = __shfl_xor_sync(0xffffffffu, arg, 16);
+            const float bl = h ? bo : best, bh = h ? best : bo;
+            const int al = h ? ao : arg, ah = h ? arg : ao;
+            best = fmaxf(bl, bh);
+            arg = (bl == best) ? al : ah;
+        }
+        return o;
+    };
+    double cf = 0.0;  // forward offset: V_t = V~_t + cf
+    int64_t zero_t = -1;
+    bool bad = false;
+    float V = neg_inf();
+    // forward max-product with backpointers over chunks [lo, hi) (Algorithm 4 lines 3-6)
+    auto fwd_range = [&](int64_t lo, int64_t hi) {
+        iss(lo, lo, hi);
+        iss(lo + 1, lo, hi);
+        for (int64_t ch = lo; ch < hi; ch++) {
+            iss(ch + 2, lo, hi);
+            cp_async_wait<2>();
+            __syncwarp();
+            float* rows = rl.stage(ch);
+            const int n = nrows(ch);
+            bad |= bs_prep<DP, true>(rows, mrow, n, D, j, h);
+            for (int i = 0; i < n; i++) {
+                const int64_t t = ch * kBsC + i;
+                const float w = rows[i * DP + j];
+                const float m = mrow[i];
+                if (t == 0) {
+                    V = lpv + w;
+                    cf = (double)m;
+                } else {
+                    float best;
+                    int arg;
+                    bool dead;
+                    const float o = mp_step(V, best, arg, dead);
+                    if (dead && zero_t < 0) zero_t = t - 1;
+                    if (h == 0 && act) bp[t * DP + j] = (uint8_t)arg;
+                    V = best + w;
+                    cf += (double)o + (double)m;
+                }
+            }
+            __syncwarp();
+        }
+        cp_async_wait<0>();
+        __syncwarp();
+    };
+    // path over steps [s, e) through SMEM-staged pointer chunks: backward (x given at e-1, x_{t-1} =
+    // bp_t(x_t)) or forward (x given at s-1, x_t = fp_t(x_{t-1}))
+    auto walk = [&](int64_t s, int64_t e, int x, bool backward) {
+        for (int64_t q = 0; q < e - s; q += kBsChunk) {
+            const int64_t s0 = backward ? ((e - q - kBsChunk > s) ? e - q - kBsChunk : s) : s + q;
+            const int64_t e0 = backward ? e - q : ((s + q + kBsChunk < e) ? s + q + kBsChunk : e);
+            const int n = (int)(e0 - s0);
+            for (int r = lane; r < n * DP / 4; r += 32)
+                reinterpret_cast<uint32_t*>(sbp)[r] = reinterpret_cast<const uint32_t*>(bp + s0 * DP)[r];
+            __syncwarp();
+            if (lane == 0) {
+                if (backward) {
+                    for (int i = n - 1; i >= 0; i--) {
+                        spath[i] = x;
+                        if (s0 + i > 0) x = sbp[i * DP + x];
+                    }
+                } else {
+                    for (int i = 0; i < n; i++) {
+                        x = sbp[i * DP + x];
+                        spath[i] = x;
+                    }
+                }
+            }
+            x = __shfl_sync(0xffffffffu, x, 0);
+            __syncwarp();
+            for (int i = lane; i < n; i += 32) p.path[base + s0 + i] = spath[i];
+            __syncwarp();
+        }
+    };
+    // smallest argmax / max of a staged vector
+    auto vec_argmax = [&](const float* v, float& o) -> int {
+        float g[DP];
+        ld_vec<DP>(v, g);
+        o = tmax<DP>(g);
+        return first_argmax<DP>(g, o);
+    };
+
+    if (role == 0) {
+        fwd_range(0, nch1);
+        if (h == 0) vmeet[0][j] = V;
+    } else {
+        // backward max-product over [mid, T) (Lemma 3's backward recursion): U = V^b_t, forward pointers
+        // fp_t(i) = argmax_k (log A(i, k) + w_t(k) + V^b_t(k)) stored at bp[t][i]
+        float U = act ? 0.0f : neg_inf();
+        double cb = 0.0;
+        bool dead_any = false;
+        iss(nch - 1, nch1, nch);
+        iss(nch - 2, nch1, nch);
+        for (int64_t ch = nch - 1; ch >= nch1; ch--) {
+            iss(ch - 2, nch1, nch);
+            cp_async_wait<2>();
+            __syncwarp();
+            float* rows = rl.stage(ch);
+            const int n = nrows(ch);
+            bad |= bs_prep<DP, true>(rows, mrow, n, D, j, h);
+            for (int i = n - 1; i >= 0; i--) {
+                const int64_t t = ch * kBsC + i;
+                float best;
+                int arg;
+                bool dead;
+                const float o = mp_step(U + rows[i * DP + j], best, arg, dead);
+                dead_any |= dead;
+                if (h == 0 && act) bp[t * DP + j] = (uint8_t)arg;
+                U = act ? best : neg_inf();
+                cb += (double)o + (double)mrow[i];
+            }
+            __syncwarp();
+        }
+        cp_async_wait<0>();
+        if (h == 0) vmeet[1][j] = U;
+        if (lane == 0) { cmeet = cb; fmeet[1] = (bad ? 1 : 0) | (dead_any ? 2 : 0); }
+    }
+    __threadfence_block();
+    __syncthreads();  // meet: V^f_{mid-1}, V^b_{mid-1}, the pointers of both halves
+
+    float tot_o;
+    int xs;
+    {
+        float* xb = xbuf + par * DP;  // (per-warp scratch)
+        if (h == 0) xb[j] = vmeet[0][j] + vmeet[1][j];
+        __syncwarp();
+        xs = vec_argmax(xb, tot_o);
+        __syncwarp();
+    }
+    const bool fallback = !(tot_o > neg_inf()) || (fmeet[1] & 2);
+    if (role == 0) {
+        bool bd = bad || (fmeet[1] & 1);
+        double lp;
+        if (!fallback) {
+            lp = (double)tot_o + cf + cmeet;
+            walk(0, mid, xs, true);
+        } else {
+            // an impossible step somewhere: the forward pass over the rest locates it (info) and the
+            // path is backtracked from argmax V_{T-1} as in the one-warp plan
+            fwd_range(nch1, nch);
+            float* xb = xbuf + par * DP;
+            if (h == 0) xb[j] = V;
+            __syncwarp();
+            float o;
+            int x = vec_argmax(xb, o);
+            if (!(o > neg_inf())) {
+                if (zero_t < 0) zero_t = T - 1;
+                o = 0.0f;
+                x = 0;
+            }
+            lp = cf + (double)o;
+            __syncwarp();
+            walk(0, T, x, true);
+        }
+        if (lane == 0) {
+            p.scalar_out[b] = lp;
+            int32_t inf = 0;
+            if (bd || lp != lp) inf = -1;
+            else if (zero_t >= 0) inf = (int32_t)(zero_t + 1);
+            if (raw < 1 || raw > p.T) inf = kInfoBadLength;
+            p.info[b] = inf;
+        }
+    } else if (!fallback && mid < T) {
+        walk(mid, T, xs, false);
+    }
+}
+
+size_t bs_smem(int DP, int op, bool bidir) {
     const size_t ring = (size_t)kBsStages * kBsC * DP;
     const size_t per = op == 0 ? 2 * ring + (size_t)(kBsC + 1) * DP + 2 * kBsC
                                : ring + 2 * DP + kBsC + kBsChunk + (size_t)kBsChunk * DP / 4;
-    return per * 4 * (kBsThreads / 32);
+    return per * 4 * (bidir ? 2 : kBsThreads / 32);
 }
+int64_t bs2_beta_rows(int64_t Tmax) { return bs2_half_rows(Tmax); }
 
-cudaError_t launch_batchseq(int DP, int op, const BSParams& p, cudaStream_t s) {
+cudaError_t launch_batchseq(int DP, int op, bool bidir, const BSParams& p, cudaStream_t s) {
+    const size_t sm = bs_smem(DP, op, bidir);
+    const void* k = nullptr;
+    if (bidir) {
+        if (DP == 16) k = op == 0 ? (const void*)bs2_smooth_kernel<16> : (const void*)bs2_viterbi_kernel<16>;
+        else if (DP == 32) k = op == 0 ? (const void*)bs2_smooth_kernel<32> : (const void*)bs2_viterbi_kernel<32>;
+        else return cudaErrorInvalidValue;
+        if (cudaError_t e = ensure_smem_optin(k, sm); e != cudaSuccess) return e;
+        const unsigned grid = (unsigned)p.B;  // one CTA (forward warp + backward warp) per sequence
+        if (DP == 16) {
+            if (op == 0) bs2_smooth_kernel<16><<<grid, kBs2Threads, sm, s>>>(p);
+            else bs2_viterbi_kernel<16><<<grid, kBs2Threads, sm, s>>>(p);
+        } else {
+            if (op == 0) bs2_smooth_kernel<32><<<grid, kBs2Threads, sm, s>>>(p);
+            else bs2_viterbi_kernel<32><<<grid, kBs2Threads, sm, s>>>(p);
+        }
+        return cudaGetLastError();
+    }
     const unsigned spb = kBsThreads / 32;  // one warp per sequence
     const unsigned grid = (unsigned)((p.B + spb - 1) / spb);
-    const size_t sm = bs_smem(DP, op);
-    const void* k = nullptr;
     if (DP == 16) k = op == 0 ? (const void*)bs_smooth_kernel<16> : (const void*)bs_viterbi_kernel<16>;
     else if (DP == 32) k = op == 0 ? (const void*)bs_smooth_kernel<32> : (const void*)bs_viterbi_kernel<32>;
     else return cudaErrorInvalidValue;

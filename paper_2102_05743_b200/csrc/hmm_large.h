@@ -68,6 +68,8 @@ struct BSParams {
     double* scalar_out;
     int32_t* info;
     uint8_t* bp;  // [B][T][DP] Viterbi backpointers (workspace)
+    float* sbeta;       // bidirectional smoother: [B][s_rows][D] backward potentials of each second half
+    int64_t s_rows;
     const int64_t* offsets;
     int64_t pi_stride, A_stride;
 };

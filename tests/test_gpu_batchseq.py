@@ -35,12 +35,16 @@ def _run(wl, force):
     return [x.cpu().numpy() for x in (f, s, lz, info)], [x.cpu().numpy() for x in (p, q, vinfo)]
 
 
+@pytest.mark.parametrize("force", [4, 6], ids=["bidir", "one_warp"])
 @pytest.mark.parametrize("D", [9, 12, 16, 17, 25, 32])
-@pytest.mark.parametrize("T", [1, 2, 7, 1000, 4099])
-def test_batchseq_vs_oracle(D, T):
+@pytest.mark.parametrize("T", [1, 2, 7, 31, 32, 33, 64, 65, 1000, 4099])
+def test_batchseq_vs_oracle(D, T, force):
+    """force 4: the bidirectional plan (two warps per sequence, forward and backward recursions from both
+    ends, meeting at mid = ceil(chunks / 2); T around the 32-step chunk covers mid = T and a one-row
+    second half); force 6: the one-warp plan."""
     wl = W.dense_batch(5, D, T, model_seed=77 + D, seed0=31 * T)
     wl.log_lik = wl.log_lik + W.random_potentials(D, T, seed=D, B=5, sigma=0.1).log_lik  # near-tie-free
-    s, v = _run(wl, 4)
+    s, v = _run(wl, force)
     for b in range(5):
         check_smooth(wl, *s, b=b)
         check_viterbi(wl, *v, b=b)
@@ -106,3 +110,33 @@ def test_batchseq_varlen_per_sequence_models():
         v = oracle.viterbi(*models[b], lls[b])
         assert rel(float(q[b]), v["log_prob"]) <= TOL_REL
         assert rel(oracle.joint_weight(*models[b], lls[b], p[a:e]), v["log_prob"]) <= TOL_REL
+
+
+@pytest.mark.parametrize("D", [16, 32])
+def test_batchseq_bidir_equals_one_warp(D):
+    """Both batch-parallel variants on the same unnormalised inputs: the forward pass is the same code
+    (filtered, log Z bitwise equal), smoothed within rounding, the MAP value within rounding of its
+    offsets and the path equal (no ties in random potentials)."""
+    wl = W.random_potentials(D, 2500, seed=9, B=6)
+    s4, v4 = _run(wl, 4)
+    s6, v6 = _run(wl, 6)
+    assert np.array_equal(s4[0], s6[0]) and np.array_equal(s4[2], s6[2])
+    assert float(np.abs(s4[1] - s6[1]).max()) <= TOL_MARG
+    assert np.array_equal(v4[0], v6[0])
+    assert float(np.max(np.abs(v4[1] - v6[1]) / np.abs(v6[1]))) <= TOL_REL
+    assert np.array_equal(s4[3], s6[3]) and np.array_equal(v4[2], v6[2])
+
+
+def test_batchseq_bidir_impossible_second_half():
+    """An impossible step in the backward warp's half: the meet sees -inf, the forward warp runs on to
+    locate it (info = t + 1) exactly as the one-warp plan."""
+    wl = W.dense_batch(3, 16, 700, model_seed=5, seed0=3)
+    wl.log_lik = np.ascontiguousarray(wl.log_lik.copy())
+    wl.log_lik[1, 600, :] = -np.inf
+    s4, v4 = _run(wl, 4)
+    s6, v6 = _run(wl, 6)
+    assert s4[3][1] == 601 and v4[2][1] == 601
+    assert np.array_equal(s4[3], s6[3]) and np.array_equal(v4[2], v6[2])
+    for b in (0, 2):
+        check_smooth(wl, *s4, b=b)
+        check_viterbi(wl, *v4, b=b)
