@@ -22,6 +22,7 @@ int large_leaves_per_block(int DP);
 size_t variants_workspace_size(int op, int D, int64_t T, int64_t B);
 cudaError_t launch_batchseq(int DP, int op, bool bidir, const BSParams& p, cudaStream_t s);
 int64_t bs2_beta_rows(int64_t Tmax);
+size_t bs_smem(int DP, int op, bool bidir);
 }
 
 using hmm::Plan;
@@ -212,16 +213,16 @@ bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 // more than the recursions' per-step latency.  hmm_debug_force_path: 4 forces it,
 // 5 forbids it.
 int bs_dp(int D) { return D <= 16 ? 16 : (D <= 32 ? 32 : 0); }
-// The plan's time is T x (per-step latency of the recursion, ~190 ns) until the batch saturates the
-// issue slots; the scan's is proportional to B T D^3.  Measured crossover (tools/batchseq_crossover.py,
-// T = 4096, profiles/r2/batchseq_crossover.txt; T cancels): DP = 16 smoother B ~ 770, Viterbi ~ 550;
-// DP = 32 smoother ~ 150, Viterbi ~ 100.
+// The plan's time is T x (per-step latency of the recursion) until the batch saturates the issue slots;
+// the scan's is proportional to B T D^3.  Measured crossover with the bidirectional variant
+// (tools/batchseq_crossover.py, T = 4096, profiles/r2/bidir/crossover.txt; T cancels): DP = 16 smoother
+// B ~ 380, Viterbi ~ 300; DP = 32 below B = 128 for both.
 bool use_batchseq(int D, int op, int64_t B) {
     const int DP = bs_dp(D);
     if (D <= 8 || DP == 0) return false;
     if (t_force_path == 4 || t_force_path == 6) return true;
     if (t_force_path == 5) return false;
-    const int64_t bmin = DP == 16 ? (op == 0 ? 768 : 512) : (op == 0 ? 160 : 128);
+    const int64_t bmin = DP == 16 ? (op == 0 ? 384 : 320) : 64;
     return B >= bmin;
 }
 // Bidirectional variant (two warps per sequence, hmm_batchseq.cu): the forward and backward recursions
@@ -231,8 +232,9 @@ bool use_batchseq(int D, int op, int64_t B) {
 bool bs_bidir(int D, int op, int64_t B) {
     if (t_force_path == 6) return false;
     const int DP = bs_dp(D);
-    (void)op;
-    return DP == 16 ? B <= 148 * 7 : B <= 148 * 3;
+    const size_t smem = hmm::bs_smem(DP, op, true) + 1024;  // (+ the per-CTA reservation)
+    const int64_t ctas_per_sm = (int64_t)((228u * 1024u) / smem);
+    return B <= 148 * ctas_per_sm * (32 / DP);  // one wave of CTAs (sequences of the one-warp plan queue)
 }
 size_t bs_workspace(int op, int D, int64_t T, int64_t B) {
     if (op == 1) return ((size_t)B * T * bs_dp(D) + 255) & ~(size_t)255;

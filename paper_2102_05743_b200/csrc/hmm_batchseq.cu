@@ -463,9 +463,9 @@ __global__ void __launch_bounds__(kBsThreads) bs_viterbi_kernel(const BSParams p
 }
 
 // ============================================================================ bidirectional plan
-// Two warps per sequence (one CTA): the forward recursion (Algorithm 1 forward / Algorithm 4 forward) and
-// the backward recursion (Algorithm 1 backward / the max-product backward recursion of Lemma 3,
-// PAPER.md:640-669) run at the same time from the two ends and meet in the middle, so a sequence takes T
+// Two recursions per sequence running at the same time from the two ends and meeting in the middle: the
+// forward recursion (Algorithm 1 forward / Algorithm 4 forward) and the backward recursion (Algorithm 1
+// backward / the max-product backward recursion of Lemma 3), so a sequence takes T
 // recursion steps of latency instead of 2T (sum-product) or T + the backtrack (max-product).  The
 // sequence is cut at mid = ceil(nch / 2) chunks:
 //   smoother  phase 1: forward over [0, mid) (filtered) | backward over [mid, T) (b_t kept in the
@@ -475,63 +475,177 @@ __global__ void __launch_bounds__(kBsThreads) bs_viterbi_kernel(const BSParams p
 //             with forward pointers; x*_{mid-1} = argmax (V^f + V^b) (Theorem 4's max-marginal at one
 //             step, smallest index), log_prob = its value; then both halves of the path in parallel
 //             (backtrack / forward track).
-// One CTA barrier separates the phases.  Results are the recursions' own (the scan's associativity is
-// not used here: the whole sequence is one block-wise element).
+// Layout: a CTA = 2 warps (warp 0 forward, warp 1 backward) x G = 32 / DP sequences per warp; lane group
+// g (DP lanes) of a warp serves sequence 2 b0 + g, lane j of a group holds state j and computes its whole
+// dot product (no half-warp split: at DP = 16 two sequences share each warp instruction, the plan is
+// issue-bound at config 4's batch).  One CTA barrier separates the phases; everything else is per lane
+// group (group masks: sequences of one warp may differ in length).  Chunk rings are 2 deep (a chunk is
+// ~6 us of recursion, far above the load latency).
 constexpr int kBs2Threads = 64;
+constexpr int kBs2Stages = 2;
 __host__ __device__ inline int64_t bs2_half_rows(int64_t Tmax) {
     const int64_t nch = (Tmax + kBsC - 1) / kBsC;
     return (nch / 2) * kBsC;
 }
+template <int DP> struct Bs2 {
+    static constexpr int G = 32 / DP;                        // sequences per warp
+    static constexpr int RING = kBs2Stages * kBsC * DP;      // floats per chunk ring
+    static constexpr int SP_PER = 2 * RING + (kBsC + 1) * DP + 2 * kBsC;  // smoother floats per (role, group)
+    static constexpr int VT_PER = RING + 2 * DP + kBsC + kBsChunk + kBsChunk * DP / 4;  // Viterbi
+};
+template <int DP>
+__device__ __forceinline__ unsigned bs2_gmask(int g) {
+    if constexpr (DP == 32) return 0xffffffffu;
+    else return 0xffffu << (16 * g);
+}
+// per-group staging ring: element (r, j) of chunk c copied by lane j (4-B cp.async, any D / alignment)
+template <int DP>
+struct Bs2Ring {
+    float* buf;  // [kBs2Stages][kBsC][DP]
+    const float* src;
+    int64_t T;
+    int D, j;
+    __device__ __forceinline__ float* stage(int64_t c) const { return buf + (size_t)(c % kBs2Stages) * kBsC * DP; }
+    bool vec;    // D % 4 == 0 and 16-B aligned rows: 16-B copies
+    __device__ __forceinline__ void issue(int64_t c, bool live) const {
+        if (live && c >= 0 && c * kBsC < T) {
+            const int64_t r0 = c * kBsC;
+            const int n = (int)((T - r0 < kBsC) ? T - r0 : kBsC);
+            if (vec) {
+                const int nq = D >> 2;
+                float* dst = stage(c);
+                const float* s = src + r0 * D;
+                for (int e = j; e < n * nq; e += DP) {
+                    const int r = e / nq, q = e - r * nq;
+                    cp_async16(dst + r * DP + 4 * q, s + (int64_t)r * D + 4 * q);
+                }
+            } else if (j < D) {
+                float* dst = stage(c) + j;
+                const float* s = src + r0 * D + j;
+                for (int r = 0; r < n; r++) cp_async4(dst + r * DP, s + (int64_t)r * D);
+            }
+        }
+        cp_async_commit();
+    }
+};
+__device__ __forceinline__ bool bs2_vec_ok(const void* p, int D) {
+    return (D & 3) == 0 && (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
+}
+// chunk preparation per group (as bs_prep): row maxima m_r (lane j handles rows j, j + DP, ..), NaN / +inf
+// flag, then l = exp(ll - m) / w = ll - m in place (pads: 0 / -inf)
+template <int DP, bool MP>
+__device__ __forceinline__ bool bs2_prep(float* rows, float* mrow, int n, int D, int j, unsigned gm) {
+    bool bad = false;
+    for (int r = j; r < n; r += DP) {
+        float v[DP];
+        ld_vec<DP>(rows + r * DP, v);
+        float cs = 0.0f;
+#pragma unroll
+        for (int k = 0; k < DP; k++) {
+            cs += (k < D) ? v[k] : 0.0f;
+            v[k] = (k < D) ? v[k] : neg_inf();
+        }
+        const float m = tmax<DP>(v);
+        bad |= (cs != cs) || (cs == INFINITY);
+        mrow[r] = (m > -FLT_MAX) ? m : 0.0f;
+    }
+    __syncwarp(gm);
+    constexpr int QP = DP / 4;  // quads per staged row (pads included)
+    for (int e = j; e < n * QP; e += DP) {
+        const int r = e / QP, q = e - r * QP;
+        float4* pr = reinterpret_cast<float4*>(rows + r * DP) + q;
+        const float4 x4 = *pr;
+        const float m = mrow[r];
+        float x[4] = {x4.x, x4.y, x4.z, x4.w};
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const float d = x[u] - m;
+            x[u] = (4 * q + u < D) ? (MP ? d : ex2(d * kLog2e)) : (MP ? neg_inf() : 0.0f);
+        }
+        *pr = make_float4(x[0], x[1], x[2], x[3]);
+    }
+    __syncwarp(gm);
+    return __any_sync(gm, bad);
+}
+// normalise n staged rows and store them to dst (pitch D); first zero-mass row (or -1), sum of row n-1
+template <int DP>
+__device__ __forceinline__ int bs2_flush(const float* rows, int n, float* dst, int D, int j, unsigned gm, float* inv,
+                                         bool& bad, float& last, bool vec) {
+    uint32_t zm = 0u;
+    bool nan = false;
+    for (int r = j; r < n; r += DP) {
+        float v[DP];
+        ld_vec<DP>(rows + r * DP, v);
+        const float sm = tsum<DP>(v);
+        inv[r] = (sm > 0.0f) ? rcp(sm) : 0.0f;
+        if (!(sm > 0.0f)) zm |= 1u << r;
+        nan |= (sm != sm);
+    }
+    __syncwarp(gm);
+    // OR of the groups' zero masks (bit r = row r), first set bit
+#pragma unroll
+    for (int o = DP / 2; o >= 1; o >>= 1) zm |= __shfl_xor_sync(gm, zm, o, DP);
+    bad |= __any_sync(gm, nan);
+    {
+        float v[DP];
+        ld_vec<DP>(rows + (n - 1) * DP, v);
+        last = tsum<DP>(v);
+    }
+    if (vec) {  // 16-B stores: lane j takes quads j, j + DP, .. of the chunk's n x D/4
+        const int nq = D >> 2;
+        for (int e = j; e < n * nq; e += DP) {
+            const int r = e / nq, q = e - r * nq;
+            const float4 v = reinterpret_cast<const float4*>(rows + r * DP)[q];
+            const float iv = inv[r];
+            reinterpret_cast<float4*>(dst + (int64_t)r * D)[q] = make_float4(v.x * iv, v.y * iv, v.z * iv, v.w * iv);
+        }
+    } else if (j < D) {
+        for (int r = 0; r < n; r++) dst[(int64_t)r * D + j] = rows[r * DP + j] * inv[r];
+    }
+    __syncwarp(gm);
+    return zm ? __ffs(zm) - 1 : -1;
+}
 
 template <int DP>
 __global__ void __launch_bounds__(kBs2Threads) bs2_smooth_kernel(const BSParams p) {
-    using S = BsShape<DP>;
-    constexpr int H = S::H, NV = S::NV;
-    constexpr int RING = kBsStages * kBsC * DP;
-    constexpr int OUT = (kBsC + 1) * DP;
-    constexpr int PER = 2 * RING + OUT + 2 * kBsC;
+    using Z = Bs2<DP>;
+    constexpr int G = Z::G, RING = Z::RING, PER = Z::SP_PER, OUT = (kBsC + 1) * DP;
     extern __shared__ __align__(16) float bsm[];
     const int lane = threadIdx.x % 32, role = threadIdx.x / 32;  // role 0: forward, 1: backward
-    const int j = lane % DP, h = lane / DP;
-    float* r0buf = bsm + (size_t)role * PER;  // log_lik chunks (turned into l in place)
-    float* r1buf = r0buf + RING;              // forward: kept b_t rows; backward: filtered rows
-    float* out = r1buf + RING;                // [1 + C][DP] staged rows
+    const int g = lane / DP, j = lane % DP;
+    const unsigned gm = bs2_gmask<DP>(g);
+    float* r0buf = bsm + (size_t)(role * G + g) * PER;  // log_lik chunks (turned into l in place)
+    float* r1buf = r0buf + RING;                         // forward: kept b_t rows; backward: filtered rows
+    float* out = r1buf + RING;                           // [1 + C][DP] staged rows
     float* mrow = out + OUT;
     float* inv = mrow + kBsC;
-    const int64_t b = blockIdx.x;
-    if (b >= p.B) return;
-    int64_t base, raw;
-    const int64_t T = seq_span(p.offsets, p.T, b, base, raw);
-    if (T < 1) {
-        if (role == 0 && lane == 0) { p.scalar_out[b] = 0.0; p.info[b] = kInfoBadLength; }
-        return;
-    }
+    const int64_t b = (int64_t)blockIdx.x * G + g;
+    int64_t base = 0, raw = 0, T = 0;
+    if (b < p.B) T = seq_span(p.offsets, p.T, b, base, raw);
+    const bool live = T >= 1;  // (groups past B or with a bad length skip the work but keep the barrier)
+    if (b < p.B && !live && role == 0 && j == 0) { p.scalar_out[b] = 0.0; p.info[b] = kInfoBadLength; }
     const int D = p.D;
     const bool act = j < D;
-    const float* la = p.log_A + b * p.A_stride;
-    float Am[NV];  // forward: A(i, j); backward: A(j, i), i in this lane's half
+    const float* la = p.log_A + (b < p.B ? b : 0) * p.A_stride;
+    float Am[DP];  // forward: column j of A (A(i, j)); backward: row j (A(j, i))
 #pragma unroll
-    for (int k = 0; k < NV; k++) {
-        const int i = h * NV + k;
-        Am[k] = (act && i < D) ? ex2(__ldg(role == 0 ? la + i * D + j : la + j * D + i) * kLog2e) : 0.0f;
-    }
-    const float piv = act ? ex2(__ldg(p.log_pi + b * p.pi_stride + j) * kLog2e) : 0.0f;
+    for (int i = 0; i < DP; i++)
+        Am[i] = (act && i < D && live) ? ex2(__ldg(role == 0 ? la + i * D + j : la + j * D + i) * kLog2e) : 0.0f;
+    const float piv = (act && live) ? ex2(__ldg(p.log_pi + b * p.pi_stride + j) * kLog2e) : 0.0f;
     float* filt = p.filtered + base * D;
     float* smo = p.smoothed + base * D;
     const int64_t nch = (T + kBsC - 1) / kBsC, nch1 = (nch + 1) / 2;
     const int64_t mid = (nch1 * kBsC < T) ? nch1 * kBsC : T;
-    float* sb = p.sbeta + b * p.s_rows * D;  // row t - mid
-    bs_fill<DP>(r0buf, PER, 0.0f);
-    __syncwarp();
-    const BsRing<DP> rl{r0buf, p.log_lik + base * D, T, D, j, h};
-    const BsRing<DP> r1{r1buf, role == 0 ? sb - mid * D : filt, T, D, j, h};
-    auto hsum = [&](float v) -> float { return (H == 2) ? v + __shfl_xor_sync(0xffffffffu, v, 16) : v; };
-    auto hmax = [&](float v) -> float { return (H == 2) ? fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 16)) : v; };
+    float* sb = p.sbeta + (b < p.B ? b : 0) * p.s_rows * D;  // row t - mid
+    for (int e = j; e < PER; e += DP) r0buf[e] = 0.0f;
+    __syncwarp(gm);
+    // 16-B paths when every row of the arrays involved starts 16-B aligned (D % 4 == 0, aligned bases)
+    const bool vec = bs2_vec_ok(p.log_lik, D) && bs2_vec_ok(p.filtered, D) && bs2_vec_ok(p.smoothed, D) &&
+                     bs2_vec_ok(p.sbeta, D);
+    const Bs2Ring<DP> rl{r0buf, p.log_lik + base * D, T, D, j, vec};
+    const Bs2Ring<DP> r1{r1buf, role == 0 ? sb - mid * D : filt, T, D, j, vec};
     auto nrows = [&](int64_t c) -> int { return (int)((T - c * kBsC < kBsC) ? T - c * kBsC : kBsC); };
-    // issue chunk c of ring R if c lies in [lo, hi), else an empty group (keeps the wait counts uniform)
-    auto iss = [&](const BsRing<DP>& R, int64_t c, int64_t lo, int64_t hi) {
-        if (c >= lo && c < hi) R.issue(c); else cp_async_commit();
-    };
+    auto iss = [&](const Bs2Ring<DP>& R, int64_t c, int64_t lo, int64_t hi) { R.issue(c, c >= lo && c < hi); };
 
     double msum = 0.0;
     int es = 0;
@@ -539,7 +653,7 @@ __global__ void __launch_bounds__(kBs2Threads) bs2_smooth_kernel(const BSParams 
     bool bad = false;
     float lastsum = 0.0f;
     float bt = act ? 1.0f : 0.0f;  // b_{T-1} = 1 (Thm 2: a_{T:T+1} = 1)
-    // forward recursion over one staged chunk (rows hold l_t), a_t staged in out rows 1..n
+    // forward recursion over one staged chunk (rows hold l_t): a_t staged in out rows 1..n
     auto fwd_chunk = [&](int64_t c, const float* rows, int n) {
         for (int i = 0; i < n; i++) msum += (double)mrow[i];
         for (int i = 0; i < n; i++) {
@@ -549,115 +663,113 @@ __global__ void __launch_bounds__(kBs2Threads) bs2_smooth_kernel(const BSParams 
             if (t == 0) {
                 a = piv * l;
             } else {
-                float g[NV];
-                ld_vec<NV>(out + i * DP + h * NV, g);
-                const float mx = hmax(tmax<NV>(g));
+                float v[DP];
+                ld_vec<DP>(out + i * DP, v);  // a_{t-1}
+                const float mx = tmax<DP>(v);
                 const float s2 = pow2_inv(mx);
                 es += pow2_inv_log2(mx);
                 float c0 = 0.0f, c1 = 0.0f, c2 = 0.0f, c3 = 0.0f;
 #pragma unroll
-                for (int k = 0; k < NV; k += 4) {
-                    c0 = fmaf(g[k], Am[k], c0);
-                    c1 = fmaf(g[k + 1], Am[k + 1], c1);
-                    c2 = fmaf(g[k + 2], Am[k + 2], c2);
-                    c3 = fmaf(g[k + 3], Am[k + 3], c3);
+                for (int k = 0; k < DP; k += 4) {
+                    c0 = fmaf(v[k], Am[k], c0);
+                    c1 = fmaf(v[k + 1], Am[k + 1], c1);
+                    c2 = fmaf(v[k + 2], Am[k + 2], c2);
+                    c3 = fmaf(v[k + 3], Am[k + 3], c3);
                 }
-                a = hsum((c0 + c1) + (c2 + c3)) * (l * s2);
+                a = ((c0 + c1) + (c2 + c3)) * (l * s2);
             }
-            if (h == 0) out[(i + 1) * DP + j] = a;
-            __syncwarp();
+            out[(i + 1) * DP + j] = a;
+            __syncwarp(gm);
         }
     };
-    // backward recursion over one staged chunk; stage(i, t) stages row i of the output before the update
+    // backward recursion over one staged chunk: out row i+1 = gam_t (frows given) or b_t itself
     auto bwd_chunk = [&](int64_t c, float* rows, int n, const float* frows) {
         for (int i = n - 1; i >= 0; i--) {
             const int64_t t = c * kBsC + i;
-            if (h == 0) {
-                out[(i + 1) * DP + j] = frows ? frows[i * DP + j] * bt : bt;  // gam_t, or b_t itself
-                rows[i * DP + j] *= bt;                                       // w = l_t o b_t
-            }
-            __syncwarp();
+            out[(i + 1) * DP + j] = frows ? frows[i * DP + j] * bt : bt;
+            rows[i * DP + j] *= bt;  // w = l_t o b_t
+            __syncwarp(gm);
             if (t > 0) {  // b_{t-1} = A (l_t o b_t), renormalised by an exact power of two
-                float g[NV];
-                ld_vec<NV>(rows + i * DP + h * NV, g);
-                const float s2 = pow2_inv(hmax(tmax<NV>(g)));
+                float v[DP];
+                ld_vec<DP>(rows + i * DP, v);
+                const float s2 = pow2_inv(tmax<DP>(v));
                 float c0 = 0.0f, c1 = 0.0f, c2 = 0.0f, c3 = 0.0f;
 #pragma unroll
-                for (int k = 0; k < NV; k += 4) {
-                    c0 = fmaf(Am[k], g[k], c0);
-                    c1 = fmaf(Am[k + 1], g[k + 1], c1);
-                    c2 = fmaf(Am[k + 2], g[k + 2], c2);
-                    c3 = fmaf(Am[k + 3], g[k + 3], c3);
+                for (int k = 0; k < DP; k += 4) {
+                    c0 = fmaf(Am[k], v[k], c0);
+                    c1 = fmaf(Am[k + 1], v[k + 1], c1);
+                    c2 = fmaf(Am[k + 2], v[k + 2], c2);
+                    c3 = fmaf(Am[k + 3], v[k + 3], c3);
                 }
-                bt = hsum((c0 + c1) + (c2 + c3)) * s2;
+                bt = ((c0 + c1) + (c2 + c3)) * s2;
             }
         }
-        __syncwarp();
+        __syncwarp(gm);
     };
 
     // ---------------- phase 1
-    if (role == 0) {  // forward over chunks [0, nch1): filtered
-        iss(rl, 0, 0, nch1);
-        iss(rl, 1, 0, nch1);
-        for (int64_t c = 0; c < nch1; c++) {
-            iss(rl, c + 2, 0, nch1);
-            cp_async_wait<2>();
-            __syncwarp();
-            float* rows = rl.stage(c);
-            const int n = nrows(c);
-            bad |= bs_prep<DP, false>(rows, mrow, n, D, j, h);
-            fwd_chunk(c, rows, n);
-            const int z = bs_flush<DP>(out + DP, n, filt + c * kBsC * D, D, j, h, inv, bad, lastsum);
-            if (z >= 0 && zero_t < 0) zero_t = c * kBsC + z;
-            if (h == 0) out[j] = out[n * DP + j];
-            __syncwarp();
-        }
-    } else {  // backward over chunks [nch1, nch) in reverse: b_t kept (row-normalised) in the workspace
-        iss(rl, nch - 1, nch1, nch);
-        iss(rl, nch - 2, nch1, nch);
-        for (int64_t c = nch - 1; c >= nch1; c--) {
-            iss(rl, c - 2, nch1, nch);
-            cp_async_wait<2>();
-            __syncwarp();
-            float* rows = rl.stage(c);
-            const int n = nrows(c);
-            bs_prep<DP, false>(rows, mrow, n, D, j, h);
-            bwd_chunk(c, rows, n, nullptr);
-            bool dummy = false;
-            float dl;
-            bs_flush<DP>(out + DP, n, sb + (c * kBsC - mid) * D, D, j, h, inv, dummy, dl);
+    if (live) {
+        if (role == 0) {  // forward over chunks [0, nch1): filtered
+            iss(rl, 0, 0, nch1);
+            for (int64_t c = 0; c < nch1; c++) {
+                iss(rl, c + 1, 0, nch1);
+                cp_async_wait<1>();
+                __syncwarp(gm);
+                float* rows = rl.stage(c);
+                const int n = nrows(c);
+                bad |= bs2_prep<DP, false>(rows, mrow, n, D, j, gm);
+                fwd_chunk(c, rows, n);
+                const int z = bs2_flush<DP>(out + DP, n, filt + c * kBsC * D, D, j, gm, inv, bad, lastsum, vec);
+                if (z >= 0 && zero_t < 0) zero_t = c * kBsC + z;
+                out[j] = out[n * DP + j];
+                __syncwarp(gm);
+            }
+        } else {  // backward over chunks [nch1, nch) in reverse: b_t kept (row-normalised) in the workspace
+            iss(rl, nch - 1, nch1, nch);
+            for (int64_t c = nch - 1; c >= nch1; c--) {
+                iss(rl, c - 1, nch1, nch);
+                cp_async_wait<1>();
+                __syncwarp(gm);
+                float* rows = rl.stage(c);
+                const int n = nrows(c);
+                bs2_prep<DP, false>(rows, mrow, n, D, j, gm);
+                bwd_chunk(c, rows, n, nullptr);
+                bool dummy = false;
+                float dl;
+                bs2_flush<DP>(out + DP, n, sb + (c * kBsC - mid) * D, D, j, gm, inv, dummy, dl, vec);
+            }
         }
     }
     cp_async_wait<0>();
     __threadfence_block();
     __syncthreads();  // phase-1 filtered rows and kept b_t rows are visible to the other warp
+    if (!live) return;
 
     // ---------------- phase 2
     if (role == 0) {  // forward over [nch1, nch): filtered and smoothed = a_t o b_t / sum
         iss(rl, nch1, nch1, nch); iss(r1, nch1, nch1, nch);
-        iss(rl, nch1 + 1, nch1, nch); iss(r1, nch1 + 1, nch1, nch);
         for (int64_t c = nch1; c < nch; c++) {
-            iss(rl, c + 2, nch1, nch); iss(r1, c + 2, nch1, nch);
-            cp_async_wait<4>();
-            __syncwarp();
+            iss(rl, c + 1, nch1, nch); iss(r1, c + 1, nch1, nch);
+            cp_async_wait<2>();
+            __syncwarp(gm);
             float* rows = rl.stage(c);
             float* brows = r1.stage(c);
             const int n = nrows(c);
-            bad |= bs_prep<DP, false>(rows, mrow, n, D, j, h);
+            bad |= bs2_prep<DP, false>(rows, mrow, n, D, j, gm);
             fwd_chunk(c, rows, n);
-            for (int r = h; r < n; r += H) brows[r * DP + j] *= out[(r + 1) * DP + j];  // gam_t = a_t o b_t
-            __syncwarp();
-            const int z = bs_flush<DP>(out + DP, n, filt + c * kBsC * D, D, j, h, inv, bad, lastsum);
+            for (int r = 0; r < n; r++) brows[r * DP + j] *= out[(r + 1) * DP + j];  // gam_t = a_t o b_t
+            __syncwarp(gm);
+            const int z = bs2_flush<DP>(out + DP, n, filt + c * kBsC * D, D, j, gm, inv, bad, lastsum, vec);
             if (z >= 0 && zero_t < 0) zero_t = c * kBsC + z;
             bool dummy = false;
             float dl;
-            bs_flush<DP>(brows, n, smo + c * kBsC * D, D, j, h, inv, dummy, dl);
-            if (h == 0) out[j] = out[n * DP + j];
-            __syncwarp();
+            bs2_flush<DP>(brows, n, smo + c * kBsC * D, D, j, gm, inv, dummy, dl, vec);
+            out[j] = out[n * DP + j];
+            __syncwarp(gm);
         }
         cp_async_wait<0>();
         const double logz = log((double)lastsum) - (double)es * (double)kLn2 + msum;
-        if (lane == 0) {
+        if (j == 0) {
             p.scalar_out[b] = logz;
             int32_t inf = 0;
             if (bad || logz != logz) inf = -1;
@@ -667,19 +779,18 @@ __global__ void __launch_bounds__(kBs2Threads) bs2_smooth_kernel(const BSParams 
         }
     } else {  // backward over [0, nch1) in reverse: smoothed from the filtered rows of phase 1
         iss(rl, nch1 - 1, 0, nch1); iss(r1, nch1 - 1, 0, nch1);
-        iss(rl, nch1 - 2, 0, nch1); iss(r1, nch1 - 2, 0, nch1);
         for (int64_t c = nch1 - 1; c >= 0; c--) {
-            iss(rl, c - 2, 0, nch1); iss(r1, c - 2, 0, nch1);
-            cp_async_wait<4>();
-            __syncwarp();
+            iss(rl, c - 1, 0, nch1); iss(r1, c - 1, 0, nch1);
+            cp_async_wait<2>();
+            __syncwarp(gm);
             float* rows = rl.stage(c);
             const float* frows = r1.stage(c);
             const int n = nrows(c);
-            bs_prep<DP, false>(rows, mrow, n, D, j, h);
+            bs2_prep<DP, false>(rows, mrow, n, D, j, gm);
             bwd_chunk(c, rows, n, frows);
             bool dummy = false;
             float dl;
-            bs_flush<DP>(out + DP, n, smo + c * kBsC * D, D, j, h, inv, dummy, dl);
+            bs2_flush<DP>(out + DP, n, smo + c * kBsC * D, D, j, gm, inv, dummy, dl, vec);
         }
         cp_async_wait<0>();
     }
@@ -687,76 +798,59 @@ __global__ void __launch_bounds__(kBs2Threads) bs2_smooth_kernel(const BSParams 
 
 template <int DP>
 __global__ void __launch_bounds__(kBs2Threads) bs2_viterbi_kernel(const BSParams p) {
-    using S = BsShape<DP>;
-    constexpr int H = S::H, NV = S::NV;
-    constexpr int RING = kBsStages * kBsC * DP;
-    constexpr int PER = RING + 2 * DP + kBsC + kBsChunk + kBsChunk * DP / 4;
+    using Z = Bs2<DP>;
+    constexpr int G = Z::G, RING = Z::RING, PER = Z::VT_PER;
     extern __shared__ __align__(16) float bsm[];
-    __shared__ float vmeet[2][DP];
-    __shared__ double cmeet;
-    __shared__ int fmeet[2];
+    __shared__ float vmeet[G][2][DP];
+    __shared__ double cmeet[G];
+    __shared__ int fmeet[G];
     const int lane = threadIdx.x % 32, role = threadIdx.x / 32;  // role 0: forward, 1: backward
-    const int j = lane % DP, h = lane / DP;
-    float* rl_buf = bsm + (size_t)role * PER;
+    const int g = lane / DP, j = lane % DP;
+    const unsigned gm = bs2_gmask<DP>(g);
+    float* rl_buf = bsm + (size_t)(role * G + g) * PER;
     float* xbuf = rl_buf + RING;                                  // [2][DP]
     float* mrow = xbuf + 2 * DP;                                  // [C]
     int32_t* spath = reinterpret_cast<int32_t*>(mrow + kBsC);     // [kBsChunk]
     uint8_t* sbp = reinterpret_cast<uint8_t*>(spath + kBsChunk);  // [kBsChunk][DP]
-    const int64_t b = blockIdx.x;
-    if (b >= p.B) return;
-    int64_t base, raw;
-    const int64_t T = seq_span(p.offsets, p.T, b, base, raw);
-    if (T < 1) {
-        if (role == 0 && lane == 0) { p.scalar_out[b] = 0.0; p.info[b] = kInfoBadLength; }
-        return;
-    }
+    const int64_t b = (int64_t)blockIdx.x * G + g;
+    int64_t base = 0, raw = 0, T = 0;
+    if (b < p.B) T = seq_span(p.offsets, p.T, b, base, raw);
+    const bool live = T >= 1;
+    if (b < p.B && !live && role == 0 && j == 0) { p.scalar_out[b] = 0.0; p.info[b] = kInfoBadLength; }
     const int D = p.D;
     const bool act = j < D;
-    const float* la = p.log_A + b * p.A_stride;
-    float LA[NV];  // forward: log A(i, j); backward: log A(j, i), i in this lane's half
+    const float* la = p.log_A + (b < p.B ? b : 0) * p.A_stride;
+    float LA[DP];  // forward: log A(i, j); backward: log A(j, i)
 #pragma unroll
-    for (int k = 0; k < NV; k++) {
-        const int i = h * NV + k;
-        LA[k] = (act && i < D) ? __ldg(role == 0 ? la + i * D + j : la + j * D + i) : neg_inf();
-    }
-    const float lpv = act ? __ldg(p.log_pi + b * p.pi_stride + j) : neg_inf();
-    uint8_t* bp = p.bp + (size_t)b * p.T * DP;
-    bs_fill<DP>(rl_buf, RING + 2 * DP, neg_inf());
-    __syncwarp();
-    const BsRing<DP> rl{rl_buf, p.log_lik + base * D, T, D, j, h};
+    for (int i = 0; i < DP; i++)
+        LA[i] = (act && i < D && live) ? __ldg(role == 0 ? la + i * D + j : la + j * D + i) : neg_inf();
+    const float lpv = (act && live) ? __ldg(p.log_pi + b * p.pi_stride + j) : neg_inf();
+    uint8_t* bp = p.bp + (size_t)(b < p.B ? b : 0) * p.T * DP;
+    for (int e = j; e < RING + 2 * DP; e += DP) rl_buf[e] = neg_inf();
+    __syncwarp(gm);
+    const Bs2Ring<DP> rl{rl_buf, p.log_lik + base * D, T, D, j, bs2_vec_ok(p.log_lik, D)};
     const int64_t nch = (T + kBsC - 1) / kBsC, nch1 = (nch + 1) / 2;
     const int64_t mid = (nch1 * kBsC < T) ? nch1 * kBsC : T;
     auto nrows = [&](int64_t c) -> int { return (int)((T - c * kBsC < kBsC) ? T - c * kBsC : kBsC); };
-    auto iss = [&](int64_t c, int64_t lo, int64_t hi) {
-        if (c >= lo && c < hi) rl.issue(c); else cp_async_commit();
-    };
+    auto iss = [&](int64_t c, int64_t lo, int64_t hi) { rl.issue(c, c >= lo && c < hi); };
     int par = 0;
-    // one max-plus step over the exchanged vector x (lane j's value): best_i = max_k (x_k - o + LA(k or i)),
-    // smallest maximising index (the lower half wins ties); returns o = max x (0 if all -inf)
+    // one max-plus step over the exchanged vector x (lane j's value): best_j = max_k (x_k - o + LA[k]),
+    // smallest maximising k; returns o = max x (0 if all -inf)
     auto mp_step = [&](float xv, float& best, int& arg, bool& dead) -> float {
         float* xb = xbuf + par * DP;
         par ^= 1;
-        if (h == 0) xb[j] = xv;
-        __syncwarp();
-        float g[NV];
-        ld_vec<NV>(xb + h * NV, g);
-        float o = tmax<NV>(g);
-        if (H == 2) o = fmaxf(o, __shfl_xor_sync(0xffffffffu, o, 16));
+        xb[j] = xv;
+        __syncwarp(gm);
+        float v[DP];
+        ld_vec<DP>(xb, v);
+        float o = tmax<DP>(v);
         dead = !(o > neg_inf());
         if (dead) o = 0.0f;
-        float sc[NV];
+        float sc[DP];
 #pragma unroll
-        for (int k = 0; k < NV; k++) sc[k] = (g[k] - o) + LA[k];
-        best = tmax<NV>(sc);
-        arg = first_argmax<NV>(sc, best) + h * NV;
-        if (H == 2) {
-            const float bo = __shfl_xor_sync(0xffffffffu, best, 16);
-            const int ao = __shfl_xor_sync(0xffffffffu, arg, 16);
-            const float bl = h ? bo : best, bh = h ? best : bo;
-            const int al = h ? ao : arg, ah = h ? arg : ao;
-            best = fmaxf(bl, bh);
-            arg = (bl == best) ? al : ah;
-        }
+        for (int k = 0; k < DP; k++) sc[k] = (v[k] - o) + LA[k];
+        best = tmax<DP>(sc);
+        arg = first_argmax<DP>(sc, best);
         return o;
     };
     double cf = 0.0;  // forward offset: V_t = V~_t + cf
@@ -766,14 +860,13 @@ __global__ void __launch_bounds__(kBs2Threads) bs2_viterbi_kernel(const BSParams
     // forward max-product with backpointers over chunks [lo, hi) (Algorithm 4 lines 3-6)
     auto fwd_range = [&](int64_t lo, int64_t hi) {
         iss(lo, lo, hi);
-        iss(lo + 1, lo, hi);
         for (int64_t ch = lo; ch < hi; ch++) {
-            iss(ch + 2, lo, hi);
-            cp_async_wait<2>();
-            __syncwarp();
+            iss(ch + 1, lo, hi);
+            cp_async_wait<1>();
+            __syncwarp(gm);
             float* rows = rl.stage(ch);
             const int n = nrows(ch);
-            bad |= bs_prep<DP, true>(rows, mrow, n, D, j, h);
+            bad |= bs2_prep<DP, true>(rows, mrow, n, D, j, gm);
             for (int i = 0; i < n; i++) {
                 const int64_t t = ch * kBsC + i;
                 const float w = rows[i * DP + j];
@@ -787,15 +880,15 @@ __global__ void __launch_bounds__(kBs2Threads) bs2_viterbi_kernel(const BSParams
                     bool dead;
                     const float o = mp_step(V, best, arg, dead);
                     if (dead && zero_t < 0) zero_t = t - 1;
-                    if (h == 0 && act) bp[t * DP + j] = (uint8_t)arg;
+                    if (act) bp[t * DP + j] = (uint8_t)arg;
                     V = best + w;
                     cf += (double)o + (double)m;
                 }
             }
-            __syncwarp();
+            __syncwarp(gm);
         }
         cp_async_wait<0>();
-        __syncwarp();
+        __syncwarp(gm);
     };
     // path over steps [s, e) through SMEM-staged pointer chunks: backward (x given at e-1, x_{t-1} =
     // bp_t(x_t)) or forward (x given at s-1, x_t = fp_t(x_{t-1}))
@@ -804,10 +897,10 @@ __global__ void __launch_bounds__(kBs2Threads) bs2_viterbi_kernel(const BSParams
             const int64_t s0 = backward ? ((e - q - kBsChunk > s) ? e - q - kBsChunk : s) : s + q;
             const int64_t e0 = backward ? e - q : ((s + q + kBsChunk < e) ? s + q + kBsChunk : e);
             const int n = (int)(e0 - s0);
-            for (int r = lane; r < n * DP / 4; r += 32)
+            for (int r = j; r < n * DP / 4; r += DP)
                 reinterpret_cast<uint32_t*>(sbp)[r] = reinterpret_cast<const uint32_t*>(bp + s0 * DP)[r];
-            __syncwarp();
-            if (lane == 0) {
+            __syncwarp(gm);
+            if (j == 0) {
                 if (backward) {
                     for (int i = n - 1; i >= 0; i--) {
                         spath[i] = x;
@@ -820,81 +913,82 @@ __global__ void __launch_bounds__(kBs2Threads) bs2_viterbi_kernel(const BSParams
                     }
                 }
             }
-            x = __shfl_sync(0xffffffffu, x, 0);
-            __syncwarp();
-            for (int i = lane; i < n; i += 32) p.path[base + s0 + i] = spath[i];
-            __syncwarp();
+            x = __shfl_sync(gm, x, 0, DP);
+            __syncwarp(gm);
+            for (int i = j; i < n; i += DP) p.path[base + s0 + i] = spath[i];
+            __syncwarp(gm);
         }
     };
-    // smallest argmax / max of a staged vector
-    auto vec_argmax = [&](const float* v, float& o) -> int {
-        float g[DP];
-        ld_vec<DP>(v, g);
-        o = tmax<DP>(g);
-        return first_argmax<DP>(g, o);
+    auto vec_argmax = [&](const float* vv, float& o) -> int {
+        float v[DP];
+        ld_vec<DP>(vv, v);
+        o = tmax<DP>(v);
+        return first_argmax<DP>(v, o);
     };
 
-    if (role == 0) {
-        fwd_range(0, nch1);
-        if (h == 0) vmeet[0][j] = V;
-    } else {
-        // backward max-product over [mid, T) (Lemma 3's backward recursion): U = V^b_t, forward pointers
-        // fp_t(i) = argmax_k (log A(i, k) + w_t(k) + V^b_t(k)) stored at bp[t][i]
-        float U = act ? 0.0f : neg_inf();
-        double cb = 0.0;
-        bool dead_any = false;
-        iss(nch - 1, nch1, nch);
-        iss(nch - 2, nch1, nch);
-        for (int64_t ch = nch - 1; ch >= nch1; ch--) {
-            iss(ch - 2, nch1, nch);
-            cp_async_wait<2>();
-            __syncwarp();
-            float* rows = rl.stage(ch);
-            const int n = nrows(ch);
-            bad |= bs_prep<DP, true>(rows, mrow, n, D, j, h);
-            for (int i = n - 1; i >= 0; i--) {
-                const int64_t t = ch * kBsC + i;
-                float best;
-                int arg;
-                bool dead;
-                const float o = mp_step(U + rows[i * DP + j], best, arg, dead);
-                dead_any |= dead;
-                if (h == 0 && act) bp[t * DP + j] = (uint8_t)arg;
-                U = act ? best : neg_inf();
-                cb += (double)o + (double)mrow[i];
+    if (live) {
+        if (role == 0) {
+            fwd_range(0, nch1);
+            vmeet[g][0][j] = V;
+        } else {
+            // backward max-product over [mid, T) (Lemma 3's backward recursion): U = V^b_t; forward
+            // pointers fp_t(i) = argmax_k (log A(i, k) + w_t(k) + V^b_t(k)) stored at bp[t][i]
+            float U = act ? 0.0f : neg_inf();
+            double cb = 0.0;
+            bool dead_any = false;
+            iss(nch - 1, nch1, nch);
+            for (int64_t ch = nch - 1; ch >= nch1; ch--) {
+                iss(ch - 1, nch1, nch);
+                cp_async_wait<1>();
+                __syncwarp(gm);
+                float* rows = rl.stage(ch);
+                const int n = nrows(ch);
+                bad |= bs2_prep<DP, true>(rows, mrow, n, D, j, gm);
+                for (int i = n - 1; i >= 0; i--) {
+                    const int64_t t = ch * kBsC + i;
+                    float best;
+                    int arg;
+                    bool dead;
+                    const float o = mp_step(U + rows[i * DP + j], best, arg, dead);
+                    dead_any |= dead;
+                    if (act) bp[t * DP + j] = (uint8_t)arg;
+                    U = act ? best : neg_inf();
+                    cb += (double)o + (double)mrow[i];
+                }
+                __syncwarp(gm);
             }
-            __syncwarp();
+            cp_async_wait<0>();
+            vmeet[g][1][j] = U;
+            if (j == 0) { cmeet[g] = cb; fmeet[g] = (bad ? 1 : 0) | (dead_any ? 2 : 0); }
         }
-        cp_async_wait<0>();
-        if (h == 0) vmeet[1][j] = U;
-        if (lane == 0) { cmeet = cb; fmeet[1] = (bad ? 1 : 0) | (dead_any ? 2 : 0); }
     }
     __threadfence_block();
     __syncthreads();  // meet: V^f_{mid-1}, V^b_{mid-1}, the pointers of both halves
+    if (!live) return;
 
     float tot_o;
     int xs;
     {
-        float* xb = xbuf + par * DP;  // (per-warp scratch)
-        if (h == 0) xb[j] = vmeet[0][j] + vmeet[1][j];
-        __syncwarp();
+        float* xb = xbuf + par * DP;
+        xb[j] = vmeet[g][0][j] + vmeet[g][1][j];
+        __syncwarp(gm);
         xs = vec_argmax(xb, tot_o);
-        __syncwarp();
+        __syncwarp(gm);
     }
-    const bool fallback = !(tot_o > neg_inf()) || (fmeet[1] & 2);
+    const bool fallback = !(tot_o > neg_inf()) || (fmeet[g] & 2);
     if (role == 0) {
-        bool bd = bad || (fmeet[1] & 1);
+        const bool bd = bad || (fmeet[g] & 1);
         double lp;
         if (!fallback) {
-            lp = (double)tot_o + cf + cmeet;
+            lp = (double)tot_o + cf + cmeet[g];
             walk(0, mid, xs, true);
         } else {
             // an impossible step somewhere: the forward pass over the rest locates it (info) and the
             // path is backtracked from argmax V_{T-1} as in the one-warp plan
             fwd_range(nch1, nch);
             float* xb = xbuf + par * DP;
-            if (h == 0) xb[j] = V;
-            __syncwarp();
+            xb[j] = V;
+            __syncwarp(gm);
             float o;
             int x = vec_argmax(xb, o);
             if (!(o > neg_inf())) {
@@ -903,10 +997,10 @@ __global__ void __launch_bounds__(kBs2Threads) bs2_viterbi_kernel(const BSParams
                 x = 0;
             }
             lp = cf + (double)o;
-            __syncwarp();
+            __syncwarp(gm);
             walk(0, T, x, true);
         }
-        if (lane == 0) {
+        if (j == 0) {
             p.scalar_out[b] = lp;
             int32_t inf = 0;
             if (bd || lp != lp) inf = -1;
@@ -920,10 +1014,15 @@ __global__ void __launch_bounds__(kBs2Threads) bs2_viterbi_kernel(const BSParams
 }
 
 size_t bs_smem(int DP, int op, bool bidir) {
+    if (bidir) {
+        const size_t per = DP == 16 ? (op == 0 ? Bs2<16>::SP_PER : Bs2<16>::VT_PER)
+                                    : (op == 0 ? Bs2<32>::SP_PER : Bs2<32>::VT_PER);
+        return per * 4 * 2 * (32 / DP);  // 2 roles x sequences per warp
+    }
     const size_t ring = (size_t)kBsStages * kBsC * DP;
     const size_t per = op == 0 ? 2 * ring + (size_t)(kBsC + 1) * DP + 2 * kBsC
                                : ring + 2 * DP + kBsC + kBsChunk + (size_t)kBsChunk * DP / 4;
-    return per * 4 * (bidir ? 2 : kBsThreads / 32);
+    return per * 4 * (kBsThreads / 32);
 }
 int64_t bs2_beta_rows(int64_t Tmax) { return bs2_half_rows(Tmax); }
 
@@ -935,7 +1034,7 @@ cudaError_t launch_batchseq(int DP, int op, bool bidir, const BSParams& p, cudaS
         else if (DP == 32) k = op == 0 ? (const void*)bs2_smooth_kernel<32> : (const void*)bs2_viterbi_kernel<32>;
         else return cudaErrorInvalidValue;
         if (cudaError_t e = ensure_smem_optin(k, sm); e != cudaSuccess) return e;
-        const unsigned grid = (unsigned)p.B;  // one CTA (forward warp + backward warp) per sequence
+        const unsigned grid = (unsigned)((p.B + 32 / DP - 1) / (32 / DP));  // (forward, backward) warps x 32/DP seqs
         if (DP == 16) {
             if (op == 0) bs2_smooth_kernel<16><<<grid, kBs2Threads, sm, s>>>(p);
             else bs2_viterbi_kernel<16><<<grid, kBs2Threads, sm, s>>>(p);

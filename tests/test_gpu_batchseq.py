@@ -114,13 +114,14 @@ def test_batchseq_varlen_per_sequence_models():
 
 @pytest.mark.parametrize("D", [16, 32])
 def test_batchseq_bidir_equals_one_warp(D):
-    """Both batch-parallel variants on the same unnormalised inputs: the forward pass is the same code
-    (filtered, log Z bitwise equal), smoothed within rounding, the MAP value within rounding of its
+    """Both batch-parallel variants on the same unnormalised inputs: filtered, smoothed and log Z within
+    rounding (the dot products are summed in a different order), the MAP value within rounding of its
     offsets and the path equal (no ties in random potentials)."""
     wl = W.random_potentials(D, 2500, seed=9, B=6)
     s4, v4 = _run(wl, 4)
     s6, v6 = _run(wl, 6)
-    assert np.array_equal(s4[0], s6[0]) and np.array_equal(s4[2], s6[2])
+    assert float(np.abs(s4[0] - s6[0]).max()) <= TOL_MARG
+    assert float(np.max(np.abs(s4[2] - s6[2]) / np.abs(s6[2]))) <= TOL_REL
     assert float(np.abs(s4[1] - s6[1]).max()) <= TOL_MARG
     assert np.array_equal(v4[0], v6[0])
     assert float(np.max(np.abs(v4[1] - v6[1]) / np.abs(v6[1]))) <= TOL_REL
