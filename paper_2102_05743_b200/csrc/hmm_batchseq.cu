@@ -483,14 +483,10 @@ __global__ void __launch_bounds__(kBsThreads) bs_viterbi_kernel(const BSParams p
 // ~6 us of recursion, far above the load latency).
 constexpr int kBs2Threads = 64;
 constexpr int kBs2Stages = 2;
-__host__ __device__ inline int64_t bs2_half_rows(int64_t Tmax) {
-    const int64_t nch = (Tmax + kBsC - 1) / kBsC;
-    return (nch / 2) * kBsC;
-}
+
 template <int DP> struct Bs2 {
     static constexpr int G = 32 / DP;                        // sequences per warp
     static constexpr int RING = kBs2Stages * kBsC * DP;      // floats per chunk ring
-    static constexpr int SP_PER = 2 * RING + (kBsC + 1) * DP + 2 * kBsC;  // smoother floats per (role, group)
     static constexpr int VT_PER = RING + 2 * DP + kBsC + kBsChunk + kBsChunk * DP / 4;  // Viterbi
 };
 template <int DP>
@@ -604,196 +600,6 @@ __device__ __forceinline__ int bs2_flush(const float* rows, int n, float* dst, i
     }
     __syncwarp(gm);
     return zm ? __ffs(zm) - 1 : -1;
-}
-
-template <int DP>
-__global__ void __launch_bounds__(kBs2Threads) bs2_smooth_kernel(const BSParams p) {
-    using Z = Bs2<DP>;
-    constexpr int G = Z::G, RING = Z::RING, PER = Z::SP_PER, OUT = (kBsC + 1) * DP;
-    extern __shared__ __align__(16) float bsm[];
-    const int lane = threadIdx.x % 32, role = threadIdx.x / 32;  // role 0: forward, 1: backward
-    const int g = lane / DP, j = lane % DP;
-    const unsigned gm = bs2_gmask<DP>(g);
-    float* r0buf = bsm + (size_t)(role * G + g) * PER;  // log_lik chunks (turned into l in place)
-    float* r1buf = r0buf + RING;                         // forward: kept b_t rows; backward: filtered rows
-    float* out = r1buf + RING;                           // [1 + C][DP] staged rows
-    float* mrow = out + OUT;
-    float* inv = mrow + kBsC;
-    const int64_t b = (int64_t)blockIdx.x * G + g;
-    int64_t base = 0, raw = 0, T = 0;
-    if (b < p.B) T = seq_span(p.offsets, p.T, b, base, raw);
-    const bool live = T >= 1;  // (groups past B or with a bad length skip the work but keep the barrier)
-    if (b < p.B && !live && role == 0 && j == 0) { p.scalar_out[b] = 0.0; p.info[b] = kInfoBadLength; }
-    const int D = p.D;
-    const bool act = j < D;
-    const float* la = p.log_A + (b < p.B ? b : 0) * p.A_stride;
-    float Am[DP];  // forward: column j of A (A(i, j)); backward: row j (A(j, i))
-#pragma unroll
-    for (int i = 0; i < DP; i++)
-        Am[i] = (act && i < D && live) ? ex2(__ldg(role == 0 ? la + i * D + j : la + j * D + i) * kLog2e) : 0.0f;
-    const float piv = (act && live) ? ex2(__ldg(p.log_pi + b * p.pi_stride + j) * kLog2e) : 0.0f;
-    float* filt = p.filtered + base * D;
-    float* smo = p.smoothed + base * D;
-    const int64_t nch = (T + kBsC - 1) / kBsC, nch1 = (nch + 1) / 2;
-    const int64_t mid = (nch1 * kBsC < T) ? nch1 * kBsC : T;
-    float* sb = p.sbeta + (b < p.B ? b : 0) * p.s_rows * D;  // row t - mid
-    for (int e = j; e < PER; e += DP) r0buf[e] = 0.0f;
-    __syncwarp(gm);
-    // 16-B paths when every row of the arrays involved starts 16-B aligned (D % 4 == 0, aligned bases)
-    const bool vec = bs2_vec_ok(p.log_lik, D) && bs2_vec_ok(p.filtered, D) && bs2_vec_ok(p.smoothed, D) &&
-                     bs2_vec_ok(p.sbeta, D);
-    const Bs2Ring<DP> rl{r0buf, p.log_lik + base * D, T, D, j, vec};
-    const Bs2Ring<DP> r1{r1buf, role == 0 ? sb - mid * D : filt, T, D, j, vec};
-    auto nrows = [&](int64_t c) -> int { return (int)((T - c * kBsC < kBsC) ? T - c * kBsC : kBsC); };
-    auto iss = [&](const Bs2Ring<DP>& R, int64_t c, int64_t lo, int64_t hi) { R.issue(c, c >= lo && c < hi); };
-
-    double msum = 0.0;
-    int es = 0;
-    int64_t zero_t = -1;
-    bool bad = false;
-    float lastsum = 0.0f;
-    float bt = act ? 1.0f : 0.0f;  // b_{T-1} = 1 (Thm 2: a_{T:T+1} = 1)
-    // forward recursion over one staged chunk (rows hold l_t): a_t staged in out rows 1..n
-    auto fwd_chunk = [&](int64_t c, const float* rows, int n) {
-        for (int i = 0; i < n; i++) msum += (double)mrow[i];
-        for (int i = 0; i < n; i++) {
-            const int64_t t = c * kBsC + i;
-            const float l = rows[i * DP + j];
-            float a;
-            if (t == 0) {
-                a = piv * l;
-            } else {
-                float v[DP];
-                ld_vec<DP>(out + i * DP, v);  // a_{t-1}
-                const float mx = tmax<DP>(v);
-                const float s2 = pow2_inv(mx);
-                es += pow2_inv_log2(mx);
-                float c0 = 0.0f, c1 = 0.0f, c2 = 0.0f, c3 = 0.0f;
-#pragma unroll
-                for (int k = 0; k < DP; k += 4) {
-                    c0 = fmaf(v[k], Am[k], c0);
-                    c1 = fmaf(v[k + 1], Am[k + 1], c1);
-                    c2 = fmaf(v[k + 2], Am[k + 2], c2);
-                    c3 = fmaf(v[k + 3], Am[k + 3], c3);
-                }
-                a = ((c0 + c1) + (c2 + c3)) * (l * s2);
-            }
-            out[(i + 1) * DP + j] = a;
-            __syncwarp(gm);
-        }
-    };
-    // backward recursion over one staged chunk: out row i+1 = gam_t (frows given) or b_t itself
-    auto bwd_chunk = [&](int64_t c, float* rows, int n, const float* frows) {
-        for (int i = n - 1; i >= 0; i--) {
-            const int64_t t = c * kBsC + i;
-            out[(i + 1) * DP + j] = frows ? frows[i * DP + j] * bt : bt;
-            rows[i * DP + j] *= bt;  // w = l_t o b_t
-            __syncwarp(gm);
-            if (t > 0) {  // b_{t-1} = A (l_t o b_t), renormalised by an exact power of two
-                float v[DP];
-                ld_vec<DP>(rows + i * DP, v);
-                const float s2 = pow2_inv(tmax<DP>(v));
-                float c0 = 0.0f, c1 = 0.0f, c2 = 0.0f, c3 = 0.0f;
-#pragma unroll
-                for (int k = 0; k < DP; k += 4) {
-                    c0 = fmaf(Am[k], v[k], c0);
-                    c1 = fmaf(Am[k + 1], v[k + 1], c1);
-                    c2 = fmaf(Am[k + 2], v[k + 2], c2);
-                    c3 = fmaf(Am[k + 3], v[k + 3], c3);
-                }
-                bt = ((c0 + c1) + (c2 + c3)) * s2;
-            }
-        }
-        __syncwarp(gm);
-    };
-
-    // ---------------- phase 1
-    if (live) {
-        if (role == 0) {  // forward over chunks [0, nch1): filtered
-            iss(rl, 0, 0, nch1);
-            for (int64_t c = 0; c < nch1; c++) {
-                iss(rl, c + 1, 0, nch1);
-                cp_async_wait<1>();
-                __syncwarp(gm);
-                float* rows = rl.stage(c);
-                const int n = nrows(c);
-                bad |= bs2_prep<DP, false>(rows, mrow, n, D, j, gm);
-                fwd_chunk(c, rows, n);
-                const int z = bs2_flush<DP>(out + DP, n, filt + c * kBsC * D, D, j, gm, inv, bad, lastsum, vec);
-                if (z >= 0 && zero_t < 0) zero_t = c * kBsC + z;
-                out[j] = out[n * DP + j];
-                __syncwarp(gm);
-            }
-        } else {  // backward over chunks [nch1, nch) in reverse: b_t kept (row-normalised) in the workspace
-            iss(rl, nch - 1, nch1, nch);
-            for (int64_t c = nch - 1; c >= nch1; c--) {
-                iss(rl, c - 1, nch1, nch);
-                cp_async_wait<1>();
-                __syncwarp(gm);
-                float* rows = rl.stage(c);
-                const int n = nrows(c);
-                bs2_prep<DP, false>(rows, mrow, n, D, j, gm);
-                bwd_chunk(c, rows, n, nullptr);
-                bool dummy = false;
-                float dl;
-                bs2_flush<DP>(out + DP, n, sb + (c * kBsC - mid) * D, D, j, gm, inv, dummy, dl, vec);
-            }
-        }
-    }
-    cp_async_wait<0>();
-    __threadfence_block();
-    __syncthreads();  // phase-1 filtered rows and kept b_t rows are visible to the other warp
-    if (!live) return;
-
-    // ---------------- phase 2
-    if (role == 0) {  // forward over [nch1, nch): filtered and smoothed = a_t o b_t / sum
-        iss(rl, nch1, nch1, nch); iss(r1, nch1, nch1, nch);
-        for (int64_t c = nch1; c < nch; c++) {
-            iss(rl, c + 1, nch1, nch); iss(r1, c + 1, nch1, nch);
-            cp_async_wait<2>();
-            __syncwarp(gm);
-            float* rows = rl.stage(c);
-            float* brows = r1.stage(c);
-            const int n = nrows(c);
-            bad |= bs2_prep<DP, false>(rows, mrow, n, D, j, gm);
-            fwd_chunk(c, rows, n);
-            for (int r = 0; r < n; r++) brows[r * DP + j] *= out[(r + 1) * DP + j];  // gam_t = a_t o b_t
-            __syncwarp(gm);
-            const int z = bs2_flush<DP>(out + DP, n, filt + c * kBsC * D, D, j, gm, inv, bad, lastsum, vec);
-            if (z >= 0 && zero_t < 0) zero_t = c * kBsC + z;
-            bool dummy = false;
-            float dl;
-            bs2_flush<DP>(brows, n, smo + c * kBsC * D, D, j, gm, inv, dummy, dl, vec);
-            out[j] = out[n * DP + j];
-            __syncwarp(gm);
-        }
-        cp_async_wait<0>();
-        const double logz = log((double)lastsum) - (double)es * (double)kLn2 + msum;
-        if (j == 0) {
-            p.scalar_out[b] = logz;
-            int32_t inf = 0;
-            if (bad || logz != logz) inf = -1;
-            else if (zero_t >= 0) inf = (int32_t)(zero_t + 1);
-            if (raw < 1 || raw > p.T) inf = kInfoBadLength;
-            p.info[b] = inf;
-        }
-    } else {  // backward over [0, nch1) in reverse: smoothed from the filtered rows of phase 1
-        iss(rl, nch1 - 1, 0, nch1); iss(r1, nch1 - 1, 0, nch1);
-        for (int64_t c = nch1 - 1; c >= 0; c--) {
-            iss(rl, c - 1, 0, nch1); iss(r1, c - 1, 0, nch1);
-            cp_async_wait<2>();
-            __syncwarp(gm);
-            float* rows = rl.stage(c);
-            const float* frows = r1.stage(c);
-            const int n = nrows(c);
-            bs2_prep<DP, false>(rows, mrow, n, D, j, gm);
-            bwd_chunk(c, rows, n, frows);
-            bool dummy = false;
-            float dl;
-            bs2_flush<DP>(out + DP, n, smo + c * kBsC * D, D, j, gm, inv, dummy, dl, vec);
-        }
-        cp_async_wait<0>();
-    }
 }
 
 template <int DP>
@@ -1013,10 +819,271 @@ __global__ void __launch_bounds__(kBs2Threads) bs2_viterbi_kernel(const BSParams
     }
 }
 
+// ---------------------------------------------------------------------------- bidirectional smoother,
+// warp-specialised: per role (forward / backward) a recursion warp runs only the recursion steps while a
+// helper warp streams the chunks in (cp.async), prepares them (row maxima, l = exp(ll - m)) one chunk
+// ahead and normalises + stores the finished chunk behind it (filtered / smoothed / kept b_t) -- the
+// chunk bookkeeping no longer sits between the recursion's steps (it cost ~0.4 ms of 1.16 at config 4).
+// One named barrier per role and chunk (64 threads: the two warps of the role); chunks of kBs3C steps, a
+// 3-deep ring (in use / prepared / loading) and a double-buffered output staging.  Lane groups of a warp
+// (two sequences at DP = 16) walk their own chunk ranges in lockstep (warp-uniform trip counts).
+constexpr int kBs3C = 16;
+constexpr int kBs3Threads = 128;
+template <int DP> struct Bs3 {
+    static constexpr int G = 32 / DP;
+    static constexpr int RING = 3 * kBs3C * DP;
+    static constexpr int OUTB = (kBs3C + 1) * DP;                 // one staging buffer (row 0 = carry)
+    static constexpr int PER = 2 * RING + 2 * OUTB + 2 * kBs3C;   // floats per (role, group)
+};
+template <int DP>
+struct Bs3Ring {
+    float* buf;  // [3][kBs3C][DP]
+    const float* src;
+    int64_t T;
+    int D, j;
+    bool vec;
+    __device__ __forceinline__ float* stage(int64_t c) const { return buf + (size_t)(c % 3) * kBs3C * DP; }
+    __device__ __forceinline__ void issue(int64_t c, bool ok) const {
+        if (ok && c >= 0 && c * kBs3C < T) {
+            const int64_t r0 = c * kBs3C;
+            const int n = (int)((T - r0 < kBs3C) ? T - r0 : kBs3C);
+            if (vec) {
+                const int nq = D >> 2;
+                float* dst = stage(c);
+                const float* s = src + r0 * D;
+                for (int e = j; e < n * nq; e += DP) {
+                    const int r = e / nq, q = e - r * nq;
+                    cp_async16(dst + r * DP + 4 * q, s + (int64_t)r * D + 4 * q);
+                }
+            } else if (j < D) {
+                float* dst = stage(c) + j;
+                const float* s = src + r0 * D + j;
+                for (int r = 0; r < n; r++) cp_async4(dst + r * DP, s + (int64_t)r * D);
+            }
+        }
+        cp_async_commit();
+    }
+};
+
+template <int DP>
+__global__ void __launch_bounds__(kBs3Threads) bs3_smooth_kernel(const BSParams p) {
+    using Z = Bs3<DP>;
+    constexpr int G = Z::G, RING = Z::RING, OUTB = Z::OUTB, PER = Z::PER;
+    extern __shared__ __align__(16) float bsm[];
+    __shared__ int s_es[G];
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int role = warp & 1, helper = warp >> 1;  // role 0 forward / 1 backward; warp 0,1 recursion, 2,3 helpers
+    const int g = lane / DP, j = lane % DP;
+    const unsigned gm = bs2_gmask<DP>(g);
+    float* region = bsm + (size_t)(role * G + g) * PER;
+    float* r0buf = region;            // log_lik chunks -> l (and w = l o b in the backward recursion)
+    float* r1buf = region + RING;     // phase 2: forward: kept b_t rows; backward: filtered rows
+    float* outb = r1buf + RING;       // [2][1 + C][DP]
+    float* mrow = outb + 2 * OUTB;    // [C]
+    float* inv = mrow + kBs3C;        // [C]
+    const int64_t b = (int64_t)blockIdx.x * G + g;
+    int64_t base = 0, raw = 0, T = 0;
+    if (b < p.B) T = seq_span(p.offsets, p.T, b, base, raw);
+    const bool live = T >= 1;
+    if (b < p.B && !live && role == 0 && helper && j == 0) { p.scalar_out[b] = 0.0; p.info[b] = kInfoBadLength; }
+    const int D = p.D;
+    const bool act = j < D;
+    const int64_t nch = (T + kBs3C - 1) / kBs3C, nch1 = (nch + 1) / 2;
+    const int64_t mid = (nch1 * kBs3C < T) ? nch1 * kBs3C : T;
+    float* filt = p.filtered + base * D;
+    float* smo = p.smoothed + base * D;
+    float* sb = p.sbeta + (b < p.B ? b : 0) * p.s_rows * D;  // row t - mid
+    const bool vec = bs2_vec_ok(p.log_lik, D) && bs2_vec_ok(p.filtered, D) && bs2_vec_ok(p.smoothed, D) &&
+                     bs2_vec_ok(p.sbeta, D);
+    const Bs3Ring<DP> rl{r0buf, p.log_lik + base * D, T, D, j, vec};
+    const Bs3Ring<DP> r1{r1buf, role == 0 ? sb - mid * D : filt, T, D, j, vec};
+    auto nrows = [&](int64_t c) -> int { return (int)((T - c * kBs3C < kBs3C) ? T - c * kBs3C : kBs3C); };
+    // per phase: this group's chunk count and the chunk of its k-th iteration; trip count = max over the
+    // groups of the warp (warp-uniform, the named barrier counts whole warps)
+    auto count = [&](int ph) -> int64_t {
+        if (!live) return 0;
+        return (role == 0) == (ph == 0) ? nch1 : nch - nch1;
+    };
+    auto chunk_of = [&](int ph, int64_t k) -> int64_t {
+        if (role == 0) return ph == 0 ? k : nch1 + k;
+        return ph == 0 ? nch - 1 - k : nch1 - 1 - k;
+    };
+    auto warp_max = [&](int64_t v) -> int64_t {
+        if constexpr (G == 2) {
+            const int64_t o = __shfl_xor_sync(0xffffffffu, v, 16);
+            return v > o ? v : o;
+        }
+        return v;
+    };
+    // output buffer of the group's k-th chunk of phase ph: its chunks alternate buffers across both phases
+    // (the forward carry a_{t0-1} travels in row 0 of the next buffer)
+    auto par_of = [&](int ph, int64_t k) -> int64_t { return (ph == 1 ? count(0) : 0) + k; };
+    const unsigned bar_id = 1 + role;
+    auto role_bar = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory"); };
+
+    if (!helper) {
+        // ============ recursion warp: only the recursion steps
+        const float* la = p.log_A + (b < p.B ? b : 0) * p.A_stride;
+        float Am[DP];  // forward: column j of A; backward: row j
+#pragma unroll
+        for (int i = 0; i < DP; i++)
+            Am[i] = (act && i < D && live) ? ex2(__ldg(role == 0 ? la + i * D + j : la + j * D + i) * kLog2e) : 0.0f;
+        const float piv = (act && live) ? ex2(__ldg(p.log_pi + b * p.pi_stride + j) * kLog2e) : 0.0f;
+        int es = 0;
+        float bt = act ? 1.0f : 0.0f;  // b_{T-1} = 1
+        for (int ph = 0; ph < 2; ph++) {
+            const int64_t n_g = count(ph), nk = warp_max(n_g);
+            role_bar();  // B_0: chunk 0 of the phase is prepared
+            for (int64_t k = 0; k < nk; k++) {
+                if (k < n_g) {
+                    const int64_t it = par_of(ph, k);  // this group's chunk counter (output buffer parity)
+                    const int64_t c = chunk_of(ph, k);
+                    float* rows = rl.stage(c);
+                    float* out = outb + (it & 1) * OUTB;
+                    const int n = nrows(c);
+                    if (role == 0) {
+                        for (int i = 0; i < n; i++) {
+                            const int64_t t = c * kBs3C + i;
+                            const float l = rows[i * DP + j];
+                            float a;
+                            if (t == 0) {
+                                a = piv * l;
+                            } else {
+                                float v[DP];
+                                ld_vec<DP>(out + i * DP, v);  // a_{t-1}
+                                const float mx = tmax<DP>(v);
+                                const float s2 = pow2_inv(mx);
+                                es += pow2_inv_log2(mx);
+                                float c0 = 0.0f, c1 = 0.0f, c2 = 0.0f, c3 = 0.0f;
+#pragma unroll
+                                for (int q = 0; q < DP; q += 4) {
+                                    c0 = fmaf(v[q], Am[q], c0);
+                                    c1 = fmaf(v[q + 1], Am[q + 1], c1);
+                                    c2 = fmaf(v[q + 2], Am[q + 2], c2);
+                                    c3 = fmaf(v[q + 3], Am[q + 3], c3);
+                                }
+                                a = ((c0 + c1) + (c2 + c3)) * (l * s2);
+                            }
+                            out[(i + 1) * DP + j] = a;
+                            __syncwarp(gm);
+                        }
+                        outb[((it + 1) & 1) * OUTB + j] = out[n * DP + j];  // carry a_{t0-1} into the next buffer
+                    } else {
+                        const float* frows = ph == 1 ? r1.stage(c) : nullptr;
+                        for (int i = n - 1; i >= 0; i--) {
+                            const int64_t t = c * kBs3C + i;
+                            out[(i + 1) * DP + j] = frows ? frows[i * DP + j] * bt : bt;  // gam_t, or b_t
+                            rows[i * DP + j] *= bt;                                       // w = l_t o b_t
+                            __syncwarp(gm);
+                            if (t > 0) {
+                                float v[DP];
+                                ld_vec<DP>(rows + i * DP, v);
+                                const float s2 = pow2_inv(tmax<DP>(v));
+                                float c0 = 0.0f, c1 = 0.0f, c2 = 0.0f, c3 = 0.0f;
+#pragma unroll
+                                for (int q = 0; q < DP; q += 4) {
+                                    c0 = fmaf(Am[q], v[q], c0);
+                                    c1 = fmaf(Am[q + 1], v[q + 1], c1);
+                                    c2 = fmaf(Am[q + 2], v[q + 2], c2);
+                                    c3 = fmaf(Am[q + 3], v[q + 3], c3);
+                                }
+                                bt = ((c0 + c1) + (c2 + c3)) * s2;
+                            }
+                        }
+                    }
+                    __syncwarp(gm);
+                }
+                role_bar();  // B_{k+1}: chunk k staged for the helper, chunk k+1 prepared
+            }
+            __syncthreads();  // phase boundary (both roles; the helpers flush the last chunk first)
+        }
+        if (role == 0 && j == 0) s_es[g] = es;
+        __syncthreads();
+        return;
+    }
+
+    // ============ helper warp: loads, preparation one chunk ahead, output one chunk behind
+    double msum = 0.0;
+    int64_t zero_t = -1;
+    bool bad = false;
+    float lastsum = 0.0f;
+    for (int i = j; i < 2 * RING + 2 * OUTB + 2 * kBs3C; i += DP) region[i] = 0.0f;  // pads stay 0
+    __syncwarp(gm);
+    auto prep = [&](int ph, int64_t k, int64_t n_g) {
+        if (k >= n_g) return;
+        const int64_t c = chunk_of(ph, k);
+        const int n = nrows(c);
+        const bool bd = bs2_prep<DP, false>(rl.stage(c), mrow, n, D, j, gm);
+        if (role == 0) {
+            bad |= bd;
+            for (int i = 0; i < n; i++) msum += (double)mrow[i];
+        }
+    };
+    auto flush = [&](int ph, int64_t k, int64_t n_g) {
+        if (k < 0 || k >= n_g) return;
+        const int64_t c = chunk_of(ph, k);
+        const int n = nrows(c);
+        float* out = outb + (par_of(ph, k) & 1) * OUTB + DP;
+        bool dummy = false;
+        float dl;
+        if (role == 0) {
+            const int z = bs2_flush<DP>(out, n, filt + c * kBs3C * D, D, j, gm, inv, bad, lastsum, vec);
+            if (z >= 0 && zero_t < 0) zero_t = c * kBs3C + z;
+            if (ph == 1) {  // smoothed = a_t o b_t / sum, in place over the kept b_t rows
+                float* brows = r1.stage(c);
+                for (int r = 0; r < n; r++) brows[r * DP + j] *= out[r * DP + j];
+                __syncwarp(gm);
+                bs2_flush<DP>(brows, n, smo + c * kBs3C * D, D, j, gm, inv, dummy, dl, vec);
+            }
+        } else {
+            float* dst = ph == 0 ? sb + (c * kBs3C - mid) * D : smo + c * kBs3C * D;
+            bs2_flush<DP>(out, n, dst, D, j, gm, inv, dummy, dl, vec);
+        }
+    };
+    for (int ph = 0; ph < 2; ph++) {
+        const int64_t n_g = count(ph), nk = warp_max(n_g);
+        const bool two = (ph == 1);  // phase 2 also streams the r1 ring (kept b_t / filtered rows)
+        auto load = [&](int64_t k) {
+            const bool ok = k >= 0 && k < n_g;
+            const int64_t c = ok ? chunk_of(ph, k) : 0;
+            rl.issue(c, ok);
+            if (two) r1.issue(c, ok); else cp_async_commit();
+        };
+        load(0);
+        load(1);
+        cp_async_wait<2>();
+        __syncwarp(gm);
+        prep(ph, 0, n_g);
+        role_bar();  // B_0
+        for (int64_t k = 0; k < nk; k++) {
+            flush(ph, k - 1, n_g);  // the chunk the recursion finished before B_k
+            load(k + 2);                    // into the stage of chunk k-1 (done with above)
+            cp_async_wait<2>();
+            __syncwarp(gm);
+            prep(ph, k + 1, n_g);
+            role_bar();  // B_{k+1}
+        }
+        flush(ph, nk - 1, n_g);
+        cp_async_wait<0>();
+        __threadfence_block();
+        __syncthreads();  // phase boundary
+    }
+    __syncthreads();  // the recursion warp's exponent sum
+    if (role == 0 && live && j == 0) {
+        const double logz = log((double)lastsum) - (double)s_es[g] * (double)kLn2 + msum;
+        p.scalar_out[b] = logz;
+        int32_t inf = 0;
+        if (bad || logz != logz) inf = -1;
+        else if (zero_t >= 0) inf = (int32_t)(zero_t + 1);
+        if (raw < 1 || raw > p.T) inf = kInfoBadLength;
+        p.info[b] = inf;
+    }
+}
+
 size_t bs_smem(int DP, int op, bool bidir) {
     if (bidir) {
-        const size_t per = DP == 16 ? (op == 0 ? Bs2<16>::SP_PER : Bs2<16>::VT_PER)
-                                    : (op == 0 ? Bs2<32>::SP_PER : Bs2<32>::VT_PER);
+        const size_t per = DP == 16 ? (op == 0 ? Bs3<16>::PER : Bs2<16>::VT_PER)
+                                    : (op == 0 ? Bs3<32>::PER : Bs2<32>::VT_PER);
         return per * 4 * 2 * (32 / DP);  // 2 roles x sequences per warp
     }
     const size_t ring = (size_t)kBsStages * kBsC * DP;
@@ -1024,22 +1091,26 @@ size_t bs_smem(int DP, int op, bool bidir) {
                                : ring + 2 * DP + kBsC + kBsChunk + (size_t)kBsChunk * DP / 4;
     return per * 4 * (kBsThreads / 32);
 }
-int64_t bs2_beta_rows(int64_t Tmax) { return bs2_half_rows(Tmax); }
+// rows of kept b_t per sequence: the second half of the smoother's kBs3C-step chunks (T <= Tmax)
+int64_t bs2_beta_rows(int64_t Tmax) {
+    const int64_t nch = (Tmax + kBs3C - 1) / kBs3C;
+    return (nch / 2) * kBs3C;
+}
 
 cudaError_t launch_batchseq(int DP, int op, bool bidir, const BSParams& p, cudaStream_t s) {
     const size_t sm = bs_smem(DP, op, bidir);
     const void* k = nullptr;
     if (bidir) {
-        if (DP == 16) k = op == 0 ? (const void*)bs2_smooth_kernel<16> : (const void*)bs2_viterbi_kernel<16>;
-        else if (DP == 32) k = op == 0 ? (const void*)bs2_smooth_kernel<32> : (const void*)bs2_viterbi_kernel<32>;
+        if (DP == 16) k = op == 0 ? (const void*)bs3_smooth_kernel<16> : (const void*)bs2_viterbi_kernel<16>;
+        else if (DP == 32) k = op == 0 ? (const void*)bs3_smooth_kernel<32> : (const void*)bs2_viterbi_kernel<32>;
         else return cudaErrorInvalidValue;
         if (cudaError_t e = ensure_smem_optin(k, sm); e != cudaSuccess) return e;
-        const unsigned grid = (unsigned)((p.B + 32 / DP - 1) / (32 / DP));  // (forward, backward) warps x 32/DP seqs
+        const unsigned grid = (unsigned)((p.B + 32 / DP - 1) / (32 / DP));  // (forward, backward) roles x 32/DP seqs
         if (DP == 16) {
-            if (op == 0) bs2_smooth_kernel<16><<<grid, kBs2Threads, sm, s>>>(p);
+            if (op == 0) bs3_smooth_kernel<16><<<grid, kBs3Threads, sm, s>>>(p);
             else bs2_viterbi_kernel<16><<<grid, kBs2Threads, sm, s>>>(p);
         } else {
-            if (op == 0) bs2_smooth_kernel<32><<<grid, kBs2Threads, sm, s>>>(p);
+            if (op == 0) bs3_smooth_kernel<32><<<grid, kBs3Threads, sm, s>>>(p);
             else bs2_viterbi_kernel<32><<<grid, kBs2Threads, sm, s>>>(p);
         }
         return cudaGetLastError();
