@@ -494,6 +494,20 @@ __device__ __forceinline__ unsigned bs2_gmask(int g) {
     if constexpr (DP == 32) return 0xffffffffu;
     else return 0xffffu << (16 * g);
 }
+// Visit the (row, quad) pairs of n rows x nq 16-B quads with lane j taking pairs j, j + DP, ..; when nq
+// divides DP the pair index splits without a division (q = j % nq fixed, r advances by DP / nq).
+template <int DP, class F>
+__device__ __forceinline__ void for_quads(int n, int nq, int j, F&& f) {
+    if ((DP % nq) == 0) {
+        const int q = j % nq, rs = DP / nq;
+        for (int r = j / nq; r < n; r += rs) f(r, q);
+    } else {
+        for (int e = j; e < n * nq; e += DP) {
+            const int r = e / nq;
+            f(r, e - r * nq);
+        }
+    }
+}
 // per-group staging ring: element (r, j) of chunk c copied by lane j (4-B cp.async, any D / alignment)
 template <int DP>
 struct Bs2Ring {
@@ -508,13 +522,10 @@ struct Bs2Ring {
             const int64_t r0 = c * kBsC;
             const int n = (int)((T - r0 < kBsC) ? T - r0 : kBsC);
             if (vec) {
-                const int nq = D >> 2;
                 float* dst = stage(c);
                 const float* s = src + r0 * D;
-                for (int e = j; e < n * nq; e += DP) {
-                    const int r = e / nq, q = e - r * nq;
-                    cp_async16(dst + r * DP + 4 * q, s + (int64_t)r * D + 4 * q);
-                }
+                const int Dl = D;
+                for_quads<DP>(n, D >> 2, j, [&](int r, int q) { cp_async16(dst + r * DP + 4 * q, s + (int64_t)r * Dl + 4 * q); });
             } else if (j < D) {
                 float* dst = stage(c) + j;
                 const float* s = src + r0 * D + j;
@@ -588,13 +599,11 @@ __device__ __forceinline__ int bs2_flush(const float* rows, int n, float* dst, i
         last = tsum<DP>(v);
     }
     if (vec) {  // 16-B stores: lane j takes quads j, j + DP, .. of the chunk's n x D/4
-        const int nq = D >> 2;
-        for (int e = j; e < n * nq; e += DP) {
-            const int r = e / nq, q = e - r * nq;
+        for_quads<DP>(n, D >> 2, j, [&](int r, int q) {
             const float4 v = reinterpret_cast<const float4*>(rows + r * DP)[q];
             const float iv = inv[r];
             reinterpret_cast<float4*>(dst + (int64_t)r * D)[q] = make_float4(v.x * iv, v.y * iv, v.z * iv, v.w * iv);
-        }
+        });
     } else if (j < D) {
         for (int r = 0; r < n; r++) dst[(int64_t)r * D + j] = rows[r * DP + j] * inv[r];
     }
@@ -848,13 +857,10 @@ struct Bs3Ring {
             const int64_t r0 = c * kBs3C;
             const int n = (int)((T - r0 < kBs3C) ? T - r0 : kBs3C);
             if (vec) {
-                const int nq = D >> 2;
                 float* dst = stage(c);
                 const float* s = src + r0 * D;
-                for (int e = j; e < n * nq; e += DP) {
-                    const int r = e / nq, q = e - r * nq;
-                    cp_async16(dst + r * DP + 4 * q, s + (int64_t)r * D + 4 * q);
-                }
+                const int Dl = D;
+                for_quads<DP>(n, D >> 2, j, [&](int r, int q) { cp_async16(dst + r * DP + 4 * q, s + (int64_t)r * Dl + 4 * q); });
             } else if (j < D) {
                 float* dst = stage(c) + j;
                 const float* s = src + r0 * D + j;
