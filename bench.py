@@ -251,6 +251,14 @@ def config_lines(H, dev, steps, warmup, flush, peaks):
                           "peak_source": "measured bf16 x 0.5 (TF32/BF16 nominal ratio)"})
             else:
                 r.update({"peak": fp32_peak, "frac": ach / fp32_peak})
+            if key == "configs[3]":
+                # the planner runs the batch-parallel recursions here: they execute
+                # ~4 D^2 flop/step (forward + backward dot products), not the scan's 2 D^3; `frac` above is
+                # the scan-equivalent rate of SURVEY §8(d), `executed_frac` the rate of the work done
+                ex = 4 * D * D
+                r.update({"executed_flop_per_step": ex,
+                          "executed_frac": ex * n / (ms_s * 1e-3) / 1e12 / fp32_peak,
+                          "note": "latency-bound recursions (bidirectional batch plan); frac is scan-equivalent"})
             rec["smoother_roofline"] = r
         out[key] = rec
     return out

@@ -225,16 +225,14 @@ bool use_batchseq(int D, int op, int64_t B) {
     const int64_t bmin = DP == 16 ? (op == 0 ? 384 : 320) : 64;
     return B >= bmin;
 }
-// Bidirectional variant (two warps per sequence, hmm_batchseq.cu): the forward and backward recursions
-// run at the same time from the two ends, halving the per-sequence latency; it needs one CTA slot per
-// sequence (7 per SM at DP = 16, 3 at DP = 32), so the one-warp plan stays for batches past one wave.
-// hmm_debug_force_path 6 forces the one-warp plan.
+// Bidirectional variant (hmm_batchseq.cu): the forward and backward recursions run at the same time from
+// the two ends, halving the per-sequence latency; it holds as many sequences per SM as the one-warp plan
+// (DP = 16) or more (DP = 32), so it is the batch-parallel plan at every B (profiles/r2/bidir:
+// D = 16, B = 2048: 1.95 vs 3.33 ms; D = 32, B = 1024: 2.46 vs 4.27 ms).  hmm_debug_force_path 6 forces
+// the one-warp plan (tests).
 bool bs_bidir(int D, int op, int64_t B) {
-    if (t_force_path == 6) return false;
-    const int DP = bs_dp(D);
-    const size_t smem = hmm::bs_smem(DP, op, true) + 1024;  // (+ the per-CTA reservation)
-    const int64_t ctas_per_sm = (int64_t)((228u * 1024u) / smem);
-    return B <= 148 * ctas_per_sm * (32 / DP);  // one wave of CTAs (sequences of the one-warp plan queue)
+    (void)D; (void)op; (void)B;
+    return t_force_path != 6;
 }
 size_t bs_workspace(int op, int D, int64_t T, int64_t B) {
     if (op == 1) return ((size_t)B * T * bs_dp(D) + 255) & ~(size_t)255;
