@@ -71,6 +71,29 @@ def variants():
     assert int(out[-1].abs().max().item()) == 0 and int(pe[-1].abs().max().item()) == 0
 
 
+def batchseq():
+    """bidirectional batch plan (bs3_smooth warp-specialised, bs2_viterbi), both lane-group widths, an odd
+    batch (an idle lane group), varlen groups of different lengths, and the one-warp plan"""
+    run(W.dense_batch(5, 16, 700, model_seed=3, seed0=1), force=4)
+    run(W.dense_batch(3, 32, 301, model_seed=4, seed0=2), force=4)
+    run(W.dense_batch(3, 12, 257, model_seed=5, seed0=3), force=6)
+    lengths = [100, 700, 33]
+    lls = [W.dense(16, n, seed=i, model_seed=9).log_lik for i, n in enumerate(lengths)]
+    wl0 = W.dense(16, 10, seed=0, model_seed=9)
+    off = torch.tensor(np.concatenate([[0], np.cumsum(lengths)]), dtype=torch.int64).cuda()
+    lp, la = torch.from_numpy(wl0.log_pi).cuda(), torch.from_numpy(wl0.log_A).cuda()
+    ll = torch.from_numpy(np.concatenate(lls)).cuda()
+    H.force_path(4)
+    try:
+        f, s, lz, info = H.smooth_varlen(lp, la, ll, off, max(lengths))
+        p, lpr, vinfo = H.viterbi_varlen(lp, la, ll, off, max(lengths))
+        torch.cuda.synchronize()
+    finally:
+        H.force_path(0)
+    assert int(info.abs().max().item()) == 0 and int(vinfo.abs().max().item()) == 0
+
+
+FAMILIES["batchseq"] = batchseq
 FAMILIES["variants"] = variants
 FAMILIES["stats"] = stats
 FAMILIES["symbols"] = symbols
