@@ -496,16 +496,24 @@ __device__ __forceinline__ unsigned bs2_gmask(int g) {
 }
 // Visit the (row, quad) pairs of n rows x nq 16-B quads with lane j taking pairs j, j + DP, ..; when nq
 // divides DP the pair index splits without a division (q = j % nq fixed, r advances by DP / nq).
+template <int DP, int NQ, class F>
+__device__ __forceinline__ void for_quads_c(int n, int j, F& f) {
+    constexpr int RS = DP / NQ;  // (NQ divides DP: q fixed per lane, rows advance by DP / NQ)
+    const int q = j % NQ;
+    for (int r = j / NQ; r < n; r += RS) f(r, q);
+}
 template <int DP, class F>
 __device__ __forceinline__ void for_quads(int n, int nq, int j, F&& f) {
-    if ((DP % nq) == 0) {
-        const int q = j % nq, rs = DP / nq;
-        for (int r = j / nq; r < n; r += rs) f(r, q);
-    } else {
-        for (int e = j; e < n * nq; e += DP) {
-            const int r = e / nq;
-            f(r, e - r * nq);
-        }
+    switch (nq) {  // compile-time divisors of DP: shifts instead of integer divisions
+        case 1: for_quads_c<DP, 1>(n, j, f); return;
+        case 2: for_quads_c<DP, 2>(n, j, f); return;
+        case 4: for_quads_c<DP, 4>(n, j, f); return;
+        case 8: if constexpr (DP % 8 == 0) { for_quads_c<DP, 8>(n, j, f); return; } break;
+        default: break;
+    }
+    for (int e = j; e < n * nq; e += DP) {
+        const int r = e / nq;
+        f(r, e - r * nq);
     }
 }
 // per-group staging ring: element (r, j) of chunk c copied by lane j (4-B cp.async, any D / alignment)
@@ -572,7 +580,7 @@ __device__ __forceinline__ bool bs2_prep(float* rows, float* mrow, int n, int D,
         *pr = make_float4(x[0], x[1], x[2], x[3]);
     }
     __syncwarp(gm);
-    return __any_sync(gm, bad);
+    return bad;  // lane-local: callers OR it over the lane group once, at the end
 }
 // normalise n staged rows and store them to dst (pitch D); first zero-mass row (or -1), sum of row n-1
 template <int DP>
@@ -592,7 +600,7 @@ __device__ __forceinline__ int bs2_flush(const float* rows, int n, float* dst, i
     // OR of the groups' zero masks (bit r = row r), first set bit
 #pragma unroll
     for (int o = DP / 2; o >= 1; o >>= 1) zm |= __shfl_xor_sync(gm, zm, o, DP);
-    bad |= __any_sync(gm, nan);
+    bad |= nan;  // lane-local (OR-ed over the lane group at the end)
     {
         float v[DP];
         ld_vec<DP>(rows + (n - 1) * DP, v);
@@ -744,6 +752,7 @@ __global__ void __launch_bounds__(kBs2Threads) bs2_viterbi_kernel(const BSParams
     if (live) {
         if (role == 0) {
             fwd_range(0, nch1);
+            bad = __any_sync(gm, bad);
             vmeet[g][0][j] = V;
         } else {
             // backward max-product over [mid, T) (Lemma 3's backward recursion): U = V^b_t; forward
@@ -773,6 +782,7 @@ __global__ void __launch_bounds__(kBs2Threads) bs2_viterbi_kernel(const BSParams
                 __syncwarp(gm);
             }
             cp_async_wait<0>();
+            bad = __any_sync(gm, bad);
             vmeet[g][1][j] = U;
             if (j == 0) { cmeet[g] = cb; fmeet[g] = (bad ? 1 : 0) | (dead_any ? 2 : 0); }
         }
@@ -1075,6 +1085,7 @@ __global__ void __launch_bounds__(kBs3Threads) bs3_smooth_kernel(const BSParams 
         __syncthreads();  // phase boundary
     }
     __syncthreads();  // the recursion warp's exponent sum
+    bad = __any_sync(gm, bad);
     if (role == 0 && live && j == 0) {
         const double logz = log((double)lastsum) - (double)s_es[g] * (double)kLn2 + msum;
         p.scalar_out[b] = logz;
