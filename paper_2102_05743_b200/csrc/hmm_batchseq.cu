@@ -497,7 +497,7 @@ __device__ __forceinline__ unsigned bs2_gmask(int g) {
 // Visit the (row, quad) pairs of n rows x nq 16-B quads with lane j taking pairs j, j + DP, ..; when nq
 // divides DP the pair index splits without a division (q = j % nq fixed, r advances by DP / nq).
 template <int DP, int NQ, class F>
-__device__ __forceinline__ void for_quads_c(int n, int j, F& f) {
+__device__ __forceinline__ void for_quads_c(int n, int j, F&& f) {
     constexpr int RS = DP / NQ;  // (NQ divides DP: q fixed per lane, rows advance by DP / NQ)
     const int q = j % NQ;
     for (int r = j / NQ; r < n; r += RS) f(r, q);
@@ -549,7 +549,8 @@ __device__ __forceinline__ bool bs2_vec_ok(const void* p, int D) {
 // chunk preparation per group (as bs_prep): row maxima m_r (lane j handles rows j, j + DP, ..), NaN / +inf
 // flag, then l = exp(ll - m) / w = ll - m in place (pads: 0 / -inf)
 template <int DP, bool MP>
-__device__ __forceinline__ bool bs2_prep(float* rows, float* mrow, int n, int D, int j, unsigned gm) {
+__device__ __forceinline__ bool bs2_prep(float* rows, float* mrow, int n, int D, int j, unsigned gm,
+                                         double* msum = nullptr) {
     bool bad = false;
     for (int r = j; r < n; r += DP) {
         float v[DP];
@@ -563,6 +564,7 @@ __device__ __forceinline__ bool bs2_prep(float* rows, float* mrow, int n, int D,
         const float m = tmax<DP>(v);
         bad |= (cs != cs) || (cs == INFINITY);
         mrow[r] = (m > -FLT_MAX) ? m : 0.0f;
+        if (msum) *msum += (double)mrow[r];  // this lane's share of sum m_t (rows j, j + DP, ..)
     }
     __syncwarp(gm);
     constexpr int QP = DP / 4;  // quads per staged row (pads included)
@@ -588,6 +590,7 @@ __device__ __forceinline__ int bs2_flush(const float* rows, int n, float* dst, i
                                          bool& bad, float& last, bool vec) {
     uint32_t zm = 0u;
     bool nan = false;
+    float mylast = 0.0f;
     for (int r = j; r < n; r += DP) {
         float v[DP];
         ld_vec<DP>(rows + r * DP, v);
@@ -595,17 +598,14 @@ __device__ __forceinline__ int bs2_flush(const float* rows, int n, float* dst, i
         inv[r] = (sm > 0.0f) ? rcp(sm) : 0.0f;
         if (!(sm > 0.0f)) zm |= 1u << r;
         nan |= (sm != sm);
+        if (r == n - 1) mylast = sm;
     }
     __syncwarp(gm);
     // OR of the groups' zero masks (bit r = row r), first set bit
 #pragma unroll
     for (int o = DP / 2; o >= 1; o >>= 1) zm |= __shfl_xor_sync(gm, zm, o, DP);
     bad |= nan;  // lane-local (OR-ed over the lane group at the end)
-    {
-        float v[DP];
-        ld_vec<DP>(rows + (n - 1) * DP, v);
-        last = tsum<DP>(v);
-    }
+    last = __shfl_sync(gm, mylast, (n - 1) % DP, DP);  // the row sum of row n-1, from the lane that took it
     if (vec) {  // 16-B stores: lane j takes quads j, j + DP, .. of the chunk's n x D/4
         for_quads<DP>(n, D >> 2, j, [&](int r, int q) {
             const float4 v = reinterpret_cast<const float4*>(rows + r * DP)[q];
@@ -1029,11 +1029,8 @@ __global__ void __launch_bounds__(kBs3Threads) bs3_smooth_kernel(const BSParams 
         if (k >= n_g) return;
         const int64_t c = chunk_of(ph, k);
         const int n = nrows(c);
-        const bool bd = bs2_prep<DP, false>(rl.stage(c), mrow, n, D, j, gm);
-        if (role == 0) {
-            bad |= bd;
-            for (int i = 0; i < n; i++) msum += (double)mrow[i];
-        }
+        const bool bd = bs2_prep<DP, false>(rl.stage(c), mrow, n, D, j, gm, role == 0 ? &msum : nullptr);
+        if (role == 0) bad |= bd;
     };
     auto flush = [&](int ph, int64_t k, int64_t n_g) {
         if (k < 0 || k >= n_g) return;
@@ -1047,7 +1044,11 @@ __global__ void __launch_bounds__(kBs3Threads) bs3_smooth_kernel(const BSParams 
             if (z >= 0 && zero_t < 0) zero_t = c * kBs3C + z;
             if (ph == 1) {  // smoothed = a_t o b_t / sum, in place over the kept b_t rows
                 float* brows = r1.stage(c);
-                for (int r = 0; r < n; r++) brows[r * DP + j] *= out[r * DP + j];
+                for_quads_c<DP, DP / 4>(n, j, [&](int r, int q) {  // gam_t = a_t o b_t, 16-B quads
+                    float4* pb = reinterpret_cast<float4*>(brows + r * DP) + q;
+                    const float4 x = *pb, y = reinterpret_cast<const float4*>(out + r * DP)[q];
+                    *pb = make_float4(x.x * y.x, x.y * y.y, x.z * y.z, x.w * y.w);
+                });
                 __syncwarp(gm);
                 bs2_flush<DP>(brows, n, smo + c * kBs3C * D, D, j, gm, inv, dummy, dl, vec);
             }
@@ -1086,6 +1087,8 @@ __global__ void __launch_bounds__(kBs3Threads) bs3_smooth_kernel(const BSParams 
     }
     __syncthreads();  // the recursion warp's exponent sum
     bad = __any_sync(gm, bad);
+#pragma unroll
+    for (int o = DP / 2; o >= 1; o >>= 1) msum += __shfl_xor_sync(gm, msum, o, DP);  // fixed-order tree
     if (role == 0 && live && j == 0) {
         const double logz = log((double)lastsum) - (double)s_es[g] * (double)kLn2 + msum;
         p.scalar_out[b] = logz;
