@@ -558,11 +558,13 @@ __device__ __forceinline__ bool bs2_prep(float* rows, float* mrow, int n, int D,
         float cs = 0.0f;
 #pragma unroll
         for (int k = 0; k < DP; k++) {
-            cs += (k < D) ? v[k] : 0.0f;
+            if constexpr (MP) cs += (k < D) ? v[k] : 0.0f;
             v[k] = (k < D) ? v[k] : neg_inf();
         }
         const float m = tmax<DP>(v);
-        bad |= (cs != cs) || (cs == INFINITY);
+        // max-plus: FMNMX drops NaN, so NaN / +inf inputs are flagged here; sum-product: they reach the
+        // forward rows (l = exp(NaN)) and the filtered flush's row sums flag them
+        if constexpr (MP) bad |= (cs != cs) || (cs == INFINITY);
         mrow[r] = (m > -FLT_MAX) ? m : 0.0f;
         if (msum) *msum += (double)mrow[r];  // this lane's share of sum m_t (rows j, j + DP, ..)
     }
@@ -585,7 +587,7 @@ __device__ __forceinline__ bool bs2_prep(float* rows, float* mrow, int n, int D,
     return bad;  // lane-local: callers OR it over the lane group once, at the end
 }
 // normalise n staged rows and store them to dst (pitch D); first zero-mass row (or -1), sum of row n-1
-template <int DP>
+template <int DP, bool ZERO = true>
 __device__ __forceinline__ int bs2_flush(const float* rows, int n, float* dst, int D, int j, unsigned gm, float* inv,
                                          bool& bad, float& last, bool vec) {
     uint32_t zm = 0u;
@@ -602,8 +604,10 @@ __device__ __forceinline__ int bs2_flush(const float* rows, int n, float* dst, i
     }
     __syncwarp(gm);
     // OR of the groups' zero masks (bit r = row r), first set bit
+    if constexpr (ZERO) {
 #pragma unroll
-    for (int o = DP / 2; o >= 1; o >>= 1) zm |= __shfl_xor_sync(gm, zm, o, DP);
+        for (int o = DP / 2; o >= 1; o >>= 1) zm |= __shfl_xor_sync(gm, zm, o, DP);
+    }
     bad |= nan;  // lane-local (OR-ed over the lane group at the end)
     last = __shfl_sync(gm, mylast, (n - 1) % DP, DP);  // the row sum of row n-1, from the lane that took it
     if (vec) {  // 16-B stores: lane j takes quads j, j + DP, .. of the chunk's n x D/4
@@ -1050,11 +1054,11 @@ __global__ void __launch_bounds__(kBs3Threads) bs3_smooth_kernel(const BSParams 
                     *pb = make_float4(x.x * y.x, x.y * y.y, x.z * y.z, x.w * y.w);
                 });
                 __syncwarp(gm);
-                bs2_flush<DP>(brows, n, smo + c * kBs3C * D, D, j, gm, inv, dummy, dl, vec);
+                bs2_flush<DP, false>(brows, n, smo + c * kBs3C * D, D, j, gm, inv, dummy, dl, vec);
             }
         } else {
             float* dst = ph == 0 ? sb + (c * kBs3C - mid) * D : smo + c * kBs3C * D;
-            bs2_flush<DP>(out, n, dst, D, j, gm, inv, dummy, dl, vec);
+            bs2_flush<DP, false>(out, n, dst, D, j, gm, inv, dummy, dl, vec);
         }
     };
     for (int ph = 0; ph < 2; ph++) {
