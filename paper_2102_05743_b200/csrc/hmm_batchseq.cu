@@ -673,11 +673,17 @@ __global__ void __launch_bounds__(kBs2Threads) bs2_viterbi_kernel(const BSParams
         float o = tmax<DP>(v);
         dead = !(o > neg_inf());
         if (dead) o = 0.0f;
+        // scores v_k + LA_k, the max subtracted once from the winner (D adds fewer than normalising v);
+        // smallest maximising k by a select chain (off the recursion's critical path)
         float sc[DP];
 #pragma unroll
-        for (int k = 0; k < DP; k++) sc[k] = (v[k] - o) + LA[k];
-        best = tmax<DP>(sc);
-        arg = first_argmax<DP>(sc, best);
+        for (int k = 0; k < DP; k++) sc[k] = v[k] + LA[k];
+        const float bm = tmax<DP>(sc);
+        int a = DP - 1;
+#pragma unroll
+        for (int k = DP - 2; k >= 0; k--) a = (sc[k] == bm) ? k : a;
+        arg = a;
+        best = bm - o;
         return o;
     };
     double cf = 0.0;  // forward offset: V_t = V~_t + cf
