@@ -523,7 +523,7 @@ struct Bs2Ring {
     const float* src;
     int64_t T;
     int D, j;
-    __device__ __forceinline__ float* stage(int64_t c) const { return buf + (size_t)(c % kBs2Stages) * kBsC * DP; }
+    __device__ __forceinline__ float* stage(int64_t c) const { return buf + (size_t)((uint32_t)c % (uint32_t)kBs2Stages) * kBsC * DP; }
     bool vec;    // D % 4 == 0 and 16-B aligned rows: 16-B copies
     __device__ __forceinline__ void issue(int64_t c, bool live) const {
         if (live && c >= 0 && c * kBsC < T) {
@@ -871,7 +871,7 @@ struct Bs3Ring {
     int64_t T;
     int D, j;
     bool vec;
-    __device__ __forceinline__ float* stage(int64_t c) const { return buf + (size_t)(c % 3) * kBs3C * DP; }
+    __device__ __forceinline__ float* stage(int64_t c) const { return buf + (size_t)((uint32_t)c % 3u) * kBs3C * DP; }
     __device__ __forceinline__ void issue(int64_t c, bool ok) const {
         if (ok && c >= 0 && c * kBs3C < T) {
             const int64_t r0 = c * kBs3C;
