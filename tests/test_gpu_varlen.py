@@ -155,3 +155,19 @@ def test_varlen_long_sequences_chunked(D):
     models, lls, off = _batch(D, lengths, seed=40 + D, per_seq=True)
     res = _run(D, models, lls, off, True)
     _check(models, lls, off, res, True)
+
+
+@pytest.mark.parametrize("D", [9, 12, 16, 20, 32])
+def test_varlen_batch_plan_chunk_edges(D):
+    """The bidirectional batch plan forced on ragged lengths at its chunk edges (16-step smoother chunks,
+    32-step Viterbi chunks, mid = ceil(chunks / 2)): lengths 1, 15..17, 31..33, 47..49, 63..65, 95..97 and
+    a long one, an odd batch (an idle lane group at D <= 16), per-sequence models; every sequence vs the
+    oracle."""
+    lengths = [1, 15, 16, 17, 31, 32, 33, 47, 48, 49, 63, 64, 65, 95, 96, 97, 1000]
+    models, lls, off = _batch(D, lengths, seed=300 + D, per_seq=True)
+    H.force_path(4)
+    try:
+        res = _run(D, models, lls, off, True)
+    finally:
+        H.force_path(0)
+    _check(models, lls, off, res, True)
