@@ -735,7 +735,8 @@ __global__ void __launch_bounds__(stream_nt(D)) hmm_stream_kernel(const SParams 
     // a warp are n steps apart, so per-lane bulk copies (UBLKCP takes uniform operands: the compiler
     // serialises them over the lanes) cost ~10 instructions per lane.  Instead the warp moves its 32
     // slices with 16-B per-thread accesses, CPL consecutive threads per lane slice: cp.async (LDGSTS)
-    // for loads into the ring, LDS + streaming STG.128 for stores -- fully coalesced segments.
+    // for loads into the ring, LDS + STG.128 for stores -- fully coalesced segments.  (Plain stores:
+    // the evict-first st.global.cs form measured ~10 us slower at T = 1e8.)
     constexpr int CPL = S * D / 4;  // 16-B chunks per full lane slice
     // symbol inputs: the S symbol bytes of a lane slice sit at the END of its row area, so the in-order
     // sweep that overwrites rows with l_t (smoother pass 2) only ever overwrites symbols it has consumed:
@@ -836,7 +837,7 @@ __global__ void __launch_bounds__(stream_nt(D)) hmm_stream_kernel(const SParams 
             if (warp_full(k)) {
 #pragma unroll
                 for (int it = 0; it < CPL; it++) {
-                    __stcs(reinterpret_cast<float4*>(dst), *reinterpret_cast<const float4*>(src));
+                    *reinterpret_cast<float4*>(dst) = *reinterpret_cast<const float4*>(src);
                     dst += (int64_t)LPI * n * D;
                     src += LPI * PITCH;
                 }
@@ -845,7 +846,7 @@ __global__ void __launch_bounds__(stream_nt(D)) hmm_stream_kernel(const SParams 
                 const int nv = (jp - j0 + LPI - 1) / LPI;
 #pragma unroll
                 for (int it = 0; it < CPL; it++) {
-                    if (it < nv) __stcs(reinterpret_cast<float4*>(dst), *reinterpret_cast<const float4*>(src));
+                    if (it < nv) *reinterpret_cast<float4*>(dst) = *reinterpret_cast<const float4*>(src);
                     dst += (int64_t)LPI * n * D;
                     src += LPI * PITCH;
                 }
@@ -854,7 +855,7 @@ __global__ void __launch_bounds__(stream_nt(D)) hmm_stream_kernel(const SParams 
                     if (rem > 0) {
                         float* d2 = g + (wbase + (int64_t)jp * n + (int64_t)k * S) * D + ch * 4;
                         const float* s2 = reinterpret_cast<const float*>(sbase + (size_t)jp * PITCH + ch * 16);
-                        if (rem >= 4) __stcs(reinterpret_cast<float4*>(d2), *reinterpret_cast<const float4*>(s2));
+                        if (rem >= 4) *reinterpret_cast<float4*>(d2) = *reinterpret_cast<const float4*>(s2);
                         else for (int f = 0; f < rem; f++) d2[f] = s2[f];
                     }
                 }
@@ -869,7 +870,7 @@ __global__ void __launch_bounds__(stream_nt(D)) hmm_stream_kernel(const SParams 
                 float* dst = g + (wbase + (int64_t)j * n + (int64_t)k * S) * D + f0;
                 const float* src = reinterpret_cast<const float*>(sbase + (size_t)j * PITCH) + f0;
                 if (f0 + 4 <= fl) {
-                    __stcs(reinterpret_cast<float4*>(dst), *reinterpret_cast<const float4*>(src));
+                    *reinterpret_cast<float4*>(dst) = *reinterpret_cast<const float4*>(src);
                 } else {
                     for (int f = 0; f < fl - f0; f++) dst[f] = src[f];
                 }
@@ -1348,7 +1349,7 @@ __global__ void __launch_bounds__(stream_nt(D)) hmm_stream_kernel(const SParams 
                     const int32_t* src = reinterpret_cast<const int32_t*>(pbuf + (size_t)(warp * 32 + j) * PPITCH) + 4 * ch;
                     int32_t* dst = p.path + wbase + (int64_t)j * n + so;
                     if (nv >= 4) {
-                        __stcs(reinterpret_cast<int4*>(dst), *reinterpret_cast<const int4*>(src));
+                        *reinterpret_cast<int4*>(dst) = *reinterpret_cast<const int4*>(src);
                     } else {
                         for (int w = 0; w < nv; w++) dst[w] = src[w];
                     }
